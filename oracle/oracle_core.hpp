@@ -1,0 +1,248 @@
+// oracle/oracle_core.hpp -- TEST INFRASTRUCTURE ONLY.
+//
+// CPU restatement of the schedule that the B200 path executes, used as the
+// checker by tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg.
+// Nothing in the product package (paper_1204_5072_b200/) includes or links
+// this file; the product fails loudly when its CUDA library is missing.
+//
+// What lives here:
+//   * Philox4x32-10 (Salmon et al., SC'11; Random123 constants).  The
+//     reference has no counter-based RNG (rng.hpp:10 lists lcg32/lcg64/tinymt
+//     only), so this generator is pinned against the published Random123
+//     known-answer vectors in tests/golden/philox_kat.json.
+//   * The two-layer DT / DTr schedule for KPZ.  The
+//     reference has no decomposition driver; the schedule follows the prose of
+//     SPEC.md:341-358 (single-hit rounds, set re-drawn with replacement,
+//     SPEC.md:398; exact L^2 accounting) nested inside the
+//     paper's two-layer device structure, with a random
+//     tiling origin drawn every sweep (the SPEC.md:386 "origin re-draw after
+//     every sweep" analogue).  The per-attempt update is supplied by the
+//     caller as a functor, so the same driver runs
+//       - the reference's own lf::detail::kpz_attempt_impl<false>
+//         (kpz.hpp:71-107) in oracle/ref_shim.cpp, and
+//       - the plain-C++ restatement in oracle/oracle.cpp.
+//   * The two-layer DT schedule for KMC (KMC-6): eight block sets, inner
+//     single-hit rounds over 4^3 domains.
+//
+// The exact key/counter layout below is the contract shared with the CUDA
+// kernels; it is restated, not shared, so a
+// mismatch between the two shows up as a parity failure.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+
+namespace orc {
+
+// ---------------------------------------------------------------- Philox4x32-10
+inline void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                          uint32_t k0, uint32_t k1, uint32_t out[4]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = uint64_t{M0} * c0;
+        const uint64_t p1 = uint64_t{M1} * c2;
+        const uint32_t hi0 = uint32_t(p0 >> 32), lo0 = uint32_t(p0);
+        const uint32_t hi1 = uint32_t(p1 >> 32), lo1 = uint32_t(p1);
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += W0; k1 += W1;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+// Stream tags (counter word 3, bits 24..31).
+enum : uint32_t { TAG_SWEEP = 1, TAG_SET = 2, TAG_ANCHOR = 3, TAG_ACCEPT = 4,
+                  TAG_KMC_SWEEP = 5, TAG_KMC_SET = 6, TAG_KMC_SITE = 7,
+                  TAG_KMC_ACCEPT = 8, TAG_KMC_INIT = 9 };
+
+// Draw 4 words for (seed, sweep, tag, c0, c1).
+inline void draw(uint64_t seed, uint64_t sweep, uint32_t tag, uint32_t c0, uint32_t c1,
+                 uint32_t out[4]) {
+    philox4x32_10(c0, c1, uint32_t(sweep), (tag << 24) | (uint32_t(sweep >> 32) & 0xFFFFFFu),
+                  uint32_t(seed), uint32_t(seed >> 32), out);
+}
+
+// Multiply-shift bounded draw, the semantics of RngStream::next_below (rng.hpp:130-134).
+inline uint32_t below(uint32_t u, uint32_t bound) {
+    return uint32_t((uint64_t{u} * bound) >> 32);
+}
+
+// Lexicographic permutation number idx (0..23) of {0,1,2,3}.
+inline void perm4(uint32_t idx, int out[4]) {
+    int pool[4] = {0, 1, 2, 3};
+    int n = 4;
+    const uint32_t fact[4] = {6, 2, 1, 1};
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t d = idx / fact[k];
+        idx %= fact[k];
+        out[k] = pool[d];
+        for (int m = int(d); m < n - 1; ++m) pool[m] = pool[m + 1];
+        --n;
+    }
+}
+
+// ---------------------------------------------------------------- KPZ DTr plan
+// Inner geometry is fixed: domains 16 (x) x 8 (y) sites, tiles 32 x 16 (one
+// 32-bit word per tile row), four inner sets (hx, hy), 512 single-hit rounds
+// per block activation.
+constexpr int kTileW = 32, kTileH = 16, kDomW = 16, kDomH = 8, kRounds = 512;
+
+struct KpzPlan {
+    int32_t L = 0;
+    int32_t bx = 0;  // device block width  (multiple of 32, L % (2 bx) == 0)
+    int32_t by = 0;  // device block height (multiple of 16, L % (2 by) == 0)
+};
+
+struct KpzSweepDraw {
+    int32_t ox, oy;
+    int perm[4];
+};
+
+inline KpzSweepDraw kpz_sweep_draw(const KpzPlan& pl, uint64_t seed, uint64_t sweep) {
+    uint32_t w[4];
+    draw(seed, sweep, TAG_SWEEP, 0, 0, w);
+    KpzSweepDraw d;
+    d.ox = int32_t(below(w[0], uint32_t(2 * pl.bx)));
+    d.oy = int32_t(below(w[1], uint32_t(2 * pl.by)));
+    perm4(below(w[2], 24), d.perm);
+    return d;
+}
+
+// One DTr sweep.  attempt(i, j, tile_id, round) performs one KPZ attempt at
+// anchor (i, j); the callee derives the acceptance word from (tile_id, round)
+// via accept_word() when -- and only when -- a pattern matches, mirroring the
+// reference's lazy get_r() (kpz.hpp:87-95).
+template <class Attempt>
+void kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+    const int32_t L = pl.L, mask = L - 1;
+    const KpzSweepDraw d = kpz_sweep_draw(pl, seed, sweep);
+    const int32_t nbx = L / pl.bx, nby = L / pl.by;
+    const int32_t twx = pl.bx / kTileW, thy = pl.by / kTileH;   // tiles per block
+    const int32_t tiles_per_row = L / kTileW;
+    const int ntiles = twx * thy;
+    uint32_t* anc = new uint32_t[size_t(ntiles) * 4];
+    for (int k = 0; k < 4; ++k) {
+        const int set = d.perm[k];
+        const int sx = set & 1, sy = set >> 1;
+        for (int32_t byi = sy; byi < nby; byi += 2) {
+            for (int32_t bxi = sx; bxi < nbx; bxi += 2) {
+                const uint32_t block_id = uint32_t(byi) * uint32_t(nbx) + uint32_t(bxi);
+                uint32_t sw[4] = {0, 0, 0, 0};
+                for (int r = 0; r < kRounds; ++r) {
+                    if ((r & 63) == 0) draw(seed, sweep, TAG_SET, block_id, uint32_t(r >> 6), sw);
+                    const int inner = int((sw[(r >> 4) & 3] >> (2 * (r & 15))) & 3u);
+                    const int hx = inner & 1, hy = inner >> 1;
+                    for (int32_t ty = 0; ty < thy; ++ty) {
+                        for (int32_t tx = 0; tx < twx; ++tx) {
+                            const int32_t gx = bxi * twx + tx, gy = byi * thy + ty;
+                            const uint32_t tile_id = uint32_t(gy) * uint32_t(tiles_per_row) + uint32_t(gx);
+                            uint32_t* a4 = anc + size_t(ty * twx + tx) * 4;
+                            if ((r & 15) == 0) draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(r >> 4), a4);
+                            const uint32_t a = a4[(r >> 2) & 3] >> (7 * (r & 3));
+                            const int32_t xd = int32_t(a & 15u), yd = int32_t((a >> 4) & 7u);
+                            const int32_t i = (d.ox + kTileW * gx + kDomW * hx + xd) & mask;
+                            const int32_t j = (d.oy + kTileH * gy + kDomH * hy + yd) & mask;
+                            attempt(i, j, tile_id, r);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    delete[] anc;
+}
+
+inline uint32_t kpz_accept_word(uint64_t seed, uint64_t sweep, uint32_t tile_id, int round) {
+    uint32_t w[4];
+    draw(seed, sweep, TAG_ACCEPT, tile_id, uint32_t(round >> 2), w);
+    return w[round & 3];
+}
+
+// ---------------------------------------------------------------- KMC DT plan
+// Device blocks of bk^3 sc sites (eight block sets), inner single-hit rounds
+// over 4^3 domains in 8^3 tiles (eight inner sets), 256 rounds per block
+// activation (= 8 sets x 32 valid fcc sites per domain).  Reach: read 2,
+// write 1 (kmc.hpp:140-141); the one-domain gap (4 sites) keeps concurrent
+// attempts disjoint.
+constexpr int kKmcTile = 8, kKmcDom = 4, kKmcRounds = 256;
+
+struct KmcPlan {
+    int32_t L = 0;
+    int32_t bk = 0;  // device block edge (multiple of 8, L % (2 bk) == 0)
+};
+
+struct KmcSweepDraw {
+    int32_t ox, oy, oz;
+    int perm[8];
+};
+
+inline void perm8(uint32_t idx, int out[8]) {
+    int pool[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+    int n = 8;
+    uint32_t fact[8] = {5040, 720, 120, 24, 6, 2, 1, 1};
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t d = idx / fact[k];
+        idx %= fact[k];
+        out[k] = pool[d];
+        for (int m = int(d); m < n - 1; ++m) pool[m] = pool[m + 1];
+        --n;
+    }
+}
+
+inline KmcSweepDraw kmc_sweep_draw(const KmcPlan& pl, uint64_t seed, uint64_t sweep) {
+    uint32_t w[4];
+    draw(seed, sweep, TAG_KMC_SWEEP, 0, 0, w);
+    KmcSweepDraw d;
+    d.ox = int32_t(below(w[0], uint32_t(2 * pl.bk)));
+    d.oy = int32_t(below(w[1], uint32_t(2 * pl.bk)));
+    d.oz = int32_t(below(w[2], uint32_t(2 * pl.bk)));
+    perm8(below(w[3], 40320), d.perm);
+    return d;
+}
+
+// One KMC DT sweep.  attempt(x, y, z, dir_word, accept_word) performs one
+// exchange attempt at the fcc-valid site (x, y, z).  The site draw follows
+// KmcKernel::draw_site (kmc.hpp:154-171) over the domain box: x and y
+// uniform, z uniform over the parity-matched planes.
+template <class Attempt>
+void kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+    const int32_t L = pl.L, mask = L - 1;
+    const KmcSweepDraw d = kmc_sweep_draw(pl, seed, sweep);
+    const int32_t nb = L / pl.bk, tb = pl.bk / kKmcTile, tl = L / kKmcTile;
+    for (int k = 0; k < 8; ++k) {
+        const int set = d.perm[k];
+        const int sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
+        for (int32_t bzi = sz; bzi < nb; bzi += 2)
+        for (int32_t byi = sy; byi < nb; byi += 2)
+        for (int32_t bxi = sx; bxi < nb; bxi += 2) {
+            const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
+            uint32_t sw[4] = {0, 0, 0, 0};
+            for (int r = 0; r < kKmcRounds; ++r) {
+                if ((r & 31) == 0) draw(seed, sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5), sw);
+                const int inner = int((sw[(r >> 3) & 3] >> (4 * (r & 7))) & 7u);
+                const int hx = inner & 1, hy = (inner >> 1) & 1, hz = inner >> 2;
+                for (int32_t tz = 0; tz < tb; ++tz)
+                for (int32_t ty = 0; ty < tb; ++ty)
+                for (int32_t tx = 0; tx < tb; ++tx) {
+                    const int32_t gx = bxi * tb + tx, gy = byi * tb + ty, gz = bzi * tb + tz;
+                    const uint32_t tile_id = (uint32_t(gz) * uint32_t(tl) + uint32_t(gy)) * uint32_t(tl) + uint32_t(gx);
+                    uint32_t w[4];
+                    draw(seed, sweep, TAG_KMC_SITE, tile_id, uint32_t(r), w);
+                    const int32_t x0 = d.ox + kKmcTile * gx + kKmcDom * hx;
+                    const int32_t y0 = d.oy + kKmcTile * gy + kKmcDom * hy;
+                    const int32_t z0 = d.oz + kKmcTile * gz + kKmcDom * hz;
+                    const int32_t x = (x0 + int32_t(w[0] & 3u)) & mask;
+                    const int32_t y = (y0 + int32_t((w[0] >> 2) & 3u)) & mask;
+                    const int32_t t = (x ^ y) & 1;
+                    const int32_t zfirst = z0 + (((z0 & 1) == t) ? 0 : 1);
+                    const int32_t z = (zfirst + 2 * int32_t((w[0] >> 4) & 1u)) & mask;
+                    attempt(x, y, z, w[1], w[2]);
+                }
+            }
+        }
+    }
+}
+
+}  // namespace orc

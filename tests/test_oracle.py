@@ -1,0 +1,209 @@
+"""CPU tests: the oracle restatement pinned against the reference.
+
+Two anchors (AGENTS: parity is proven through the oracle):
+  * tests/golden/golden.json -- produced by the unmodified reference sources
+    (tests/golden/make_golden.py); checked everywhere, including GPU boxes.
+  * oracle/_ref/liblfref.so -- the reference itself, live, where it was built.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ----------------------------------------------------------------- RNG
+def test_philox_kat(oracle, golden):
+    for k in golden["philox_kat"]:
+        assert oracle.philox(k["ctr"], k["key"]).tolist() == k["out"]
+
+
+def test_rng_suite_golden(oracle, golden):
+    for r in golden["rng"]:
+        got = oracle.rng_draws(r["kind"], r["seed"], len(r["draws"]), r["stream_id"], r.get("skip", 0))
+        assert got.tolist() == r["draws"], r
+    for s in golden["split_streams"]:
+        got = oracle.split_streams_lcg(s["kind"], s["seed"], s["count"], s["stride"])
+        assert [int(v) for v in got] == s["states"]
+
+
+def test_lcg64_skip_ahead_property(oracle):
+    # SPEC acceptance 8: skip_ahead(n) == n sequential steps; composition law.
+    rs = np.random.RandomState(0)
+    for _ in range(20):
+        seed = int(rs.randint(0, 2**62))
+        n = int(rs.randint(0, 5000))
+        a = oracle.rng_draws("lcg64", seed, n + 1)
+        b = oracle.rng_draws("lcg64", seed, 1, skip=n)
+        assert a[n] == b[0]
+        m = int(rs.randint(0, 10**6))
+        assert oracle.lcg64_skip(oracle.lcg64_skip(seed, m), n) == oracle.lcg64_skip(seed, m + n)
+
+
+def test_rng_live_vs_ref(oracle, reflib):
+    for kind in ("lcg32", "lcg64", "tinymt"):
+        for seed in (0, 1, 99, 2**63 + 5):
+            for sid in (0, 1, 17):
+                assert (oracle.rng_draws(kind, seed, 64, sid) == reflib.rng_draws(kind, seed, 64, sid)).all()
+
+
+# ----------------------------------------------------------------- KPZ
+def test_flat_golden(oracle, golden):
+    for f in golden["kpz_flat"]:
+        L = f["L"]
+        x, y = oracle.kpz_flat(L)
+        assert sha(x) == f["sx"] and sha(y) == f["sy"]
+        assert oracle.interface_width(L, x, y) == f["w2"] == 0.5
+        assert oracle.kpz_width_sums(L, x, y) == (f["sum"], f["sum2"])
+        assert oracle.closure_holds(L, x, y)
+
+
+def test_flat_rejects_bad_size(oracle):
+    for L in (0, 2, 6, 100):
+        with pytest.raises(ValueError):
+            oracle.kpz_flat(L)
+
+
+def test_single_attempts_golden(oracle, golden):
+    # Appendix A: anchor (1,1) on flat L=8 deposits; (0,0) is the detach pattern.
+    for a in golden["kpz_attempt_flat8"]:
+        x, y = oracle.kpz_flat(8)
+        # drive one attempt through the sequential restatement is not possible at a
+        # chosen site; compare with a DTr-free manual application instead
+        xs, ys = np.array(a["x"], np.uint64), np.array(a["y"], np.uint64)
+        if a["outcome"] == 2:
+            assert (xs == x).all() and (ys == y).all()
+        else:
+            h0 = oracle.reconstruct_heights(8, x, y).astype(np.int64).sum()
+            h1 = oracle.reconstruct_heights(8, xs, ys).astype(np.int64).sum()
+            assert h1 - h0 == 2  # one deposition raises the anchored sum by 2
+
+
+def test_sequential_golden(oracle, golden):
+    for s in golden["kpz_sequential"]:
+        L = s["L"]
+        x, y = oracle.kpz_flat(L)
+        c, st = oracle.kpz_sweep_sequential(L, x, y, s["p"], s["q"], "lcg64", s["seed"], s["sweeps"])
+        assert int(c[0]) == s["attempts"] and int(c[1]) == s["successes"] and st == s["state"]
+        assert sha(x) == s["sx"] and sha(y) == s["sy"]
+        assert oracle.interface_width(L, x, y) == s["w2"]
+
+
+def test_c1_head_golden(oracle, golden):
+    L = 1024
+    x, y = oracle.kpz_flat(L)
+    st, t = 1, 0
+    for pt in golden["kpz_c1_head"]:
+        _, st = oracle.kpz_sweep_sequential(L, x, y, 1.0, 0.0, "lcg64", st, pt["t"] - t)
+        t = pt["t"]
+        assert oracle.interface_width(L, x, y) == pt["w2"]
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_dtr_golden(oracle, golden, case):
+    g = golden["kpz_dtr"][case]
+    if g["L"] > 1024:
+        pytest.skip("covered by the GPU tier")
+    L = g["L"]
+    x, y = oracle.kpz_flat(L)
+    c = oracle.kpz_sweep_dtr(L, x, y, g["p"], g["q"], g["seed"], g["sweep0"], g["nsweeps"], g["bx"], g["by"])
+    assert [int(v) for v in c] == g["counters"]
+    assert sha(x) == g["sx"] and sha(y) == g["sy"]
+    assert oracle.interface_width(L, x, y) == g["w2"]
+    assert oracle.kpz_width_sums(L, x, y) == (g["sum"], g["sum2"])
+    assert oracle.closure_holds(L, x, y)
+
+
+def test_dtr_live_vs_ref(oracle, reflib):
+    rs = np.random.RandomState(1)
+    for _ in range(6):
+        L = int(rs.choice([64, 128, 256]))
+        bx = int(rs.choice([b for b in (32, 64, 128) if 2 * b <= L]))
+        by = int(rs.choice([b for b in (16, 32, 64) if 2 * b <= L]))
+        p, q = [(1.0, 0.0), (0.95, 0.05), (0.3, 0.7), (0.0, 1.0)][rs.randint(4)]
+        seed = int(rs.randint(0, 2**63))
+        x1, y1 = oracle.kpz_flat(L)
+        x2, y2 = reflib.make_flat(L)
+        c1 = oracle.kpz_sweep_dtr(L, x1, y1, p, q, seed, 123, 2, bx, by)
+        c2 = reflib.kpz_sweep_dtr(L, x2, y2, p, q, seed, 123, 2, bx, by)
+        assert (c1 == c2).all() and (x1 == x2).all() and (y1 == y2).all()
+        assert oracle.interface_width(L, x1, y1) == reflib.interface_width(L, x2, y2)
+        assert (oracle.reconstruct_heights(L, x1, y1) == reflib.reconstruct_heights(L, x2, y2)).all()
+
+
+def test_dtr_attempt_accounting_and_closure(oracle):
+    # SPEC.md:349 exact accounting; closure invariant under the DTr scheduler.
+    for L, bx, by in ((64, 32, 16), (128, 64, 64)):
+        x, y = oracle.kpz_flat(L)
+        c = oracle.kpz_sweep_dtr(L, x, y, 0.7, 0.3, 5, 0, 5, bx, by)
+        assert c[0] == 5 * L * L and c[1] == c[2] + c[3]
+        assert oracle.closure_holds(L, x, y)
+
+
+def test_sweep_draw_ranges(oracle):
+    seen = set()
+    for s in range(400):
+        d = oracle.kpz_sweep_draw(1024, 512, 128, 42, s)
+        assert 0 <= d[0] < 1024 and 0 <= d[1] < 256
+        assert sorted(d[2:].tolist()) == [0, 1, 2, 3]
+        seen.add(tuple(d[2:].tolist()))
+    assert len(seen) == 24  # every block-set order occurs
+
+
+def test_closure_violation_detected(oracle):
+    L = 8
+    x, y = oracle.kpz_flat(L)
+    x[0] ^= np.uint64(1)
+    assert not oracle.closure_holds(L, x, y)
+    with pytest.raises(RuntimeError):
+        oracle.reconstruct_heights(L, x, y)
+
+
+# ----------------------------------------------------------------- KMC
+def test_alloy_golden(oracle, golden):
+    for a in golden["kmc_alloy"]:
+        w, st = oracle.kmc_random_alloy(a["L"], a["c"], "lcg64", a["seed"])
+        assert sha(w) == a["sha"] and st == a["state"]
+        assert oracle.kmc_count_b(a["L"], w) == a["count_b"]
+        npart, nopen = oracle.kmc_open_bond_sums(a["L"], w)
+        assert npart == a["count_b"] and nopen / npart == a["open_bonds"]
+
+
+def test_kmc_sequential_golden(oracle, golden):
+    for s in golden["kmc_sequential"]:
+        w, st = oracle.kmc_random_alloy(16, 0.5, "lcg64", 5)
+        c, _ = oracle.kmc_sweep_sequential(16, w, s["eps"], s["both"], "lcg64", st, 1)
+        assert int(c[0]) == s["attempts"] and int(c[1]) == s["successes"] and sha(w) == s["sha"]
+
+
+def test_kmc_dt_golden(oracle, golden):
+    for g in golden["kmc_dt"]:
+        w, _ = oracle.kmc_random_alloy(g["L"], g["c"], "lcg64", g["alloy_seed"])
+        c = oracle.kmc_sweep_dt(g["L"], w, g["eps"], g["both"], g["seed"], g["sweep0"], g["nsweeps"], g["bk"])
+        assert [int(v) for v in c] == g["counters"]
+        assert sha(w) == g["sha"]
+        assert oracle.kmc_count_b(g["L"], w) == g["count_b"]
+
+
+def test_kmc_dt_live_vs_ref(oracle, reflib):
+    for both in (0, 1):
+        for eps in (0.0, 1.5, 3.0):
+            w1, _ = oracle.kmc_random_alloy(32, 0.4, "lcg64", 8)
+            w2 = w1.copy()
+            c1 = oracle.kmc_sweep_dt(32, w1, eps, both, 77, 5, 2, 16)
+            c2 = reflib.kmc_sweep_dt(32, w2, eps, both, 77, 5, 2, 16)
+            assert (c1 == c2).all() and (w1 == w2).all()
+
+
+def test_metropolis_golden(golden):
+    import math
+
+    vals = golden["metropolis_eps1.5"]
+    assert vals[0] == 1.0
+    for d in range(1, 13):
+        assert vals[d] == math.exp(-d * 1.5)
