@@ -1,0 +1,127 @@
+/* lfg.h -- C ABI of the B200 lattice library (liblfg.so).
+ *
+ * This is the drop-in boundary for the reference's simulation API (namespace
+ * lf, /root/reference/proj/include/lf).  The reference is a C++ library with
+ * free functions and no FFI; each entry point below names the reference
+ * symbol it replaces (file:line relative to /root/reference/proj).  The C++
+ * drop-in wrapper (include/lf_gpu.hpp) re-exposes the reference signatures
+ * on top of this ABI and rethrows the reference's exception types.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; lattice words use the reference layout:
+ *     SlopeField planes (lattice.hpp:56-97) and OccupancyLattice bits
+ *     (lattice.hpp:107-135) as little-endian uint64 words, site index
+ *     j*L+i (KPZ) or (z*L+y)*L+x (KMC), bit idx&63 of word idx>>6;
+ *   - every function returns an lfg_status; lfg_last_error() gives the
+ *     message of the last failure on the calling thread, worded like the
+ *     reference's exception text;
+ *   - a handle is not thread-safe (one host thread per handle, as
+ *     RngStream/lattice ownership in the reference, rng.hpp:38-39); all
+ *     device work is ordered on the handle's CUDA stream; calls that return
+ *     host data are synchronous.
+ */
+#ifndef LFG_H
+#define LFG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LFG_API __attribute__((visibility("default")))
+#else
+#define LFG_API
+#endif
+
+typedef enum lfg_status {
+    LFG_OK = 0,
+    LFG_EINVAL = 1,   /* std::invalid_argument  (lattice.cpp:10-16, kpz.hpp:19-26, kmc.hpp:24-26, ...) */
+    LFG_ECLOSURE = 2, /* std::runtime_error     (reconstruct_heights closure violation, kpz.cpp:42-44) */
+    LFG_EDOMAIN = 3,  /* std::domain_error      (no B particles, kmc.cpp:36-38) */
+    LFG_ECUDA = 4,    /* CUDA runtime failure (no reference analogue) */
+    LFG_ENCCL = 5,    /* collective/transport failure on the sharded path */
+    LFG_ENOMEM = 6    /* device allocation failure */
+} lfg_status;
+
+/* Attempt accounting, lf::Counters (counters.hpp:10-19) plus the
+ * deposit/detach split needed for <h>(t). */
+typedef struct lfg_counters {
+    int64_t attempts;
+    int64_t successes;
+    int64_t deposits;  /* KPZ: depositions; KMC: exchanges */
+    int64_t detaches;  /* KPZ: detachments; KMC: 0 */
+} lfg_counters;
+
+LFG_API const char* lfg_last_error(void);
+LFG_API int lfg_abi_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+LFG_API int lfg_device_count(int* count);
+
+/* ======================================================================= KPZ */
+typedef struct lfg_kpz lfg_kpz;
+
+/* Two-layer DTr geometry: device blocks block_x x block_y sites (0 = auto:
+ * min(1024, L/2) x min(128, L/2)); inner 16x8 single-hit domains are fixed. */
+typedef struct lfg_kpz_plan {
+    int32_t block_x;
+    int32_t block_y;
+} lfg_kpz_plan;
+
+/* SlopeField(L) + KpzParams{p,q}.validate() + the seeding of
+ * RngStream::make (rng.cpp:49-69): a Philox4x32-10 key.  The lattice starts
+ * all-zero slopes like SlopeField's constructor (lattice.cpp:20-25). */
+LFG_API int lfg_kpz_create(lfg_kpz** h, int32_t L, double p, double q, uint64_t seed, const lfg_kpz_plan* plan,
+                   int32_t device);
+/* `replicas` independent lattices (seed per replica) advanced by one launch. */
+LFG_API int lfg_kpz_create_batch(lfg_kpz** h, int32_t L, double p, double q, const uint64_t* seeds, int32_t replicas,
+                         const lfg_kpz_plan* plan, int32_t device);
+LFG_API int lfg_kpz_destroy(lfg_kpz* h);
+LFG_API int lfg_kpz_get_plan(const lfg_kpz* h, lfg_kpz_plan* out);
+
+/* make_flat_slopes (lattice.cpp:71-82), all replicas. */
+LFG_API int lfg_kpz_init_flat(lfg_kpz* h);
+/* Copy a host SlopeField (words_x()/words_y(), lattice.hpp:81-84) in/out.
+ * nwords = L*L/64.  Upload rejects a non-integrable field with LFG_ECLOSURE
+ * (the reference's reconstruct_heights error, kpz.cpp:42-44). */
+LFG_API int lfg_kpz_upload(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords);
+LFG_API int lfg_kpz_download(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size_t nwords);
+
+/* kpz_sweep_sequential (kpz.cpp:5-19) replaced by n_mcs two-layer DTr sweeps.
+ * out: NULL or an array of `replicas` counters for this call. */
+LFG_API int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out);
+/* Enqueue n_mcs sweeps without synchronising (counters accumulate on device). */
+LFG_API int lfg_kpz_sweep_async(lfg_kpz* h, int64_t n_mcs);
+/* Enqueue one device-layer phase (0..3) of sweep `sweep` (profiling / sharded driver). */
+LFG_API int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase);
+/* Cumulative counters since create / reset (synchronises). */
+LFG_API int lfg_kpz_counters(lfg_kpz* h, int32_t replica, lfg_counters* out);
+LFG_API int lfg_kpz_reset_counters(lfg_kpz* h);
+
+/* interface_width(const SlopeField&) (kpz.cpp:62-81): exact int64 sums with
+ * h(0,0)=0; W2 = sum2/n - (sum/n)^2 finished on the host exactly as kpz.cpp:78-80. */
+LFG_API int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2);
+LFG_API int lfg_kpz_interface_width(lfg_kpz* h, int32_t replica, double* w2);
+/* reconstruct_heights (kpz.cpp:21-49): n = L*L int32, row-major j*L+i. */
+LFG_API int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n);
+
+LFG_API int lfg_kpz_set_params(lfg_kpz* h, double p, double q);
+/* Counter-based RNG state: (seed, next sweep index) -> exact resume. */
+LFG_API int lfg_kpz_set_sweep_index(lfg_kpz* h, uint64_t sweep);
+LFG_API int lfg_kpz_get_sweep_index(const lfg_kpz* h, uint64_t* sweep);
+LFG_API int lfg_kpz_set_seed(lfg_kpz* h, int32_t replica, uint64_t seed);
+LFG_API int lfg_kpz_set_stream(lfg_kpz* h, void* cuda_stream);
+LFG_API int lfg_kpz_synchronize(lfg_kpz* h);
+/* Device pointer of a replica's spin words ([L][L/32] uint32) for zero-copy
+ * interop (torch.distributed halo exchange on the sharded path). */
+LFG_API int lfg_kpz_device_spins(lfg_kpz* h, int32_t replica, void** dev_ptr, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFG_H */

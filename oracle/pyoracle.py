@@ -188,6 +188,11 @@ class RefLib:
         _sig(lib, "ref_kpz_params_validate", I, D, D)
         _sig(lib, "ref_kpz_sweep_sequential", I, I32, u64p, u64p, D, D, I, C.POINTER(U64), I, i64p)
         _sig(lib, "ref_kpz_attempt", I, I32, u64p, u64p, I32, I32, D, D, D, C.POINTER(I))
+        _sig(lib, "ref_kpz_attempts_sequential", I, I32, u64p, u64p, D, D, I, C.POINTER(U64), I64, i64p)
+        _sig(lib, "ref_kmc_attempts_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I64, i64p)
+        _sig(lib, "ref_kpz_field_create", C.c_void_p, I32, u64p, u64p)
+        _sig(lib, "ref_kpz_field_destroy", None, C.c_void_p)
+        _sig(lib, "ref_kpz_field_attempts", I, C.c_void_p, D, D, I, C.POINTER(U64), I64, i64p)
         _sig(lib, "ref_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, i64p)
         _sig(lib, "ref_make_random_alloy", I, I32, D, I, U64, u64p, C.POINTER(U64))
         _sig(lib, "ref_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
@@ -237,6 +242,38 @@ class RefLib:
         c = np.zeros(2, np.int64)
         st = C.c_uint64(state)
         self._check(self.lib.ref_kpz_sweep_sequential(L, x, y, p, q, KIND[kind], C.byref(st), sweeps, c))
+        return c, st.value
+
+    def kpz_attempts_sequential(self, L, x, y, p, q, kind, state, n):
+        """Bounded sample of kpz_sweep_sequential's loop (n attempts)."""
+        c = np.zeros(2, np.int64)
+        st = C.c_uint64(state)
+        self._check(self.lib.ref_kpz_attempts_sequential(L, x, y, p, q, KIND[kind], C.byref(st), n, c))
+        return c, st.value
+
+    def kpz_field(self, L, x, y):
+        """A reference lf::SlopeField held across calls (timed loops exclude copies)."""
+        ptr = self.lib.ref_kpz_field_create(L, x, y)
+        if not ptr:
+            raise RefError(1, self.lib.ref_last_error().decode())
+        ref = self
+
+        class _Field:
+            def attempts(self, p, q, kind, state, n):
+                c = np.zeros(2, np.int64)
+                st = C.c_uint64(state)
+                ref._check(ref.lib.ref_kpz_field_attempts(ptr, p, q, KIND[kind], C.byref(st), n, c))
+                return c, st.value
+
+            def close(self):
+                ref.lib.ref_kpz_field_destroy(ptr)
+
+        return _Field()
+
+    def kmc_attempts_sequential(self, L, w, eps, both, kind, state, n):
+        c = np.zeros(2, np.int64)
+        st = C.c_uint64(state)
+        self._check(self.lib.ref_kmc_attempts_sequential(L, w, eps, int(both), KIND[kind], C.byref(st), n, c))
         return c, st.value
 
     def kpz_attempt(self, L, x, y, i, j, p, q, r):

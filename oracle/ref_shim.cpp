@@ -134,6 +134,96 @@ int ref_kpz_sweep_sequential(int32_t L, uint64_t* x, uint64_t* y, double p, doub
     });
 }
 
+// A bounded sample of kpz_sweep_sequential: the loop body of kpz.cpp:12-16
+// (two next_below draws, then KpzKernel<false>::attempt) for n_attempts
+// attempts, so bench.py can time the reference on L=2^16 without a 10-minute
+// full MCS.  counters: [attempts, successes].
+int ref_kpz_attempts_sequential(int32_t L, uint64_t* x, uint64_t* y, double p, double q, int kind,
+                                uint64_t* lcg_state, int64_t n_attempts, int64_t* counters) {
+    return guarded([&] {
+        const lf::KpzParams params{p, q};
+        params.validate();
+        lf::SlopeField f(L);
+        std::memcpy(f.words_x(), x, words2(L) * 8);
+        std::memcpy(f.words_y(), y, words2(L) * 8);
+        auto rng = lf::RngStream::make(kind_of(kind), 0);
+        rng.lcg = *lcg_state;
+        lf::KpzKernel<false> kernel{&f, params};
+        const auto Lu = static_cast<uint32_t>(L);
+        int64_t succ = 0;
+        for (int64_t n = 0; n < n_attempts; ++n) {
+            auto i = static_cast<int32_t>(rng.next_below(Lu));
+            auto j = static_cast<int32_t>(rng.next_below(Lu));
+            succ += kernel.attempt({i, j}, rng);
+        }
+        std::memcpy(x, f.words_x(), words2(L) * 8);
+        std::memcpy(y, f.words_y(), words2(L) * 8);
+        *lcg_state = rng.lcg;
+        counters[0] += n_attempts;
+        counters[1] += succ;
+    });
+}
+
+// Persistent reference SlopeField so a timed sample excludes host copies
+// (wall time around the update loops only).
+void* ref_kpz_field_create(int32_t L, const uint64_t* x, const uint64_t* y) {
+    try {
+        auto* f = new lf::SlopeField(L);
+        std::memcpy(f->words_x(), x, words2(L) * 8);
+        std::memcpy(f->words_y(), y, words2(L) * 8);
+        return f;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_kpz_field_destroy(void* f) { delete static_cast<lf::SlopeField*>(f); }
+
+int ref_kpz_field_attempts(void* fp, double p, double q, int kind, uint64_t* lcg_state, int64_t n_attempts,
+                           int64_t* counters) {
+    return guarded([&] {
+        auto& f = *static_cast<lf::SlopeField*>(fp);
+        const lf::KpzParams params{p, q};
+        params.validate();
+        auto rng = lf::RngStream::make(kind_of(kind), 0);
+        rng.lcg = *lcg_state;
+        lf::KpzKernel<false> kernel{&f, params};
+        const auto Lu = static_cast<uint32_t>(f.size());
+        int64_t succ = 0;
+        for (int64_t n = 0; n < n_attempts; ++n) {  // kpz.cpp:12-16
+            auto i = static_cast<int32_t>(rng.next_below(Lu));
+            auto j = static_cast<int32_t>(rng.next_below(Lu));
+            succ += kernel.attempt({i, j}, rng);
+        }
+        *lcg_state = rng.lcg;
+        counters[0] += n_attempts;
+        counters[1] += succ;
+    });
+}
+
+// Same for KMC: the loop body of kmc.cpp:13-15 for n_attempts attempts.
+int ref_kmc_attempts_sequential(int32_t L, uint64_t* words, double eps, int both, int kind,
+                                uint64_t* lcg_state, int64_t n_attempts, int64_t* counters) {
+    return guarded([&] {
+        lf::OccupancyLattice lat(L);
+        std::memcpy(lat.words(), words, words3(L) * 8);
+        auto rng = lf::RngStream::make(kind_of(kind), 0);
+        rng.lcg = *lcg_state;
+        lf::KmcParams params{eps, both ? lf::ActiveMode::both : lf::ActiveMode::b_only};
+        params.validate();
+        lf::KmcKernel<false> kernel{&lat, params};
+        const lf::Coord3 lo{0, 0, 0};
+        const lf::Coord3 ext{L, L, L};
+        int64_t succ = 0;
+        for (int64_t n = 0; n < n_attempts; ++n) succ += kernel.attempt(kernel.draw_site(lo, ext, rng), rng);
+        std::memcpy(words, lat.words(), words3(L) * 8);
+        *lcg_state = rng.lcg;
+        counters[0] += n_attempts;
+        counters[1] += succ;
+    });
+}
+
 // One reference attempt at (i, j) with an externally supplied r (kpz.hpp:112-116).
 int ref_kpz_attempt(int32_t L, uint64_t* x, uint64_t* y, int32_t i, int32_t j, double p, double q,
                     double r, int* outcome) {

@@ -1,0 +1,296 @@
+"""B200-native KPZ octahedron DT/DTr sweep and binary-alloy KMC (arXiv 1204.5072).
+
+Host-side mirror of the reference's simulation API (namespace ``lf``,
+/root/reference/proj/include/lf) over the C ABI in include/lfg.h.  The
+compute path is the sm_100a library ``_lib/liblfg.so``; there is no CPU
+fallback.  Names follow the reference:
+
+    lf::SlopeField + make_flat_slopes + kpz_sweep_sequential + interface_width
+        -> KpzLattice(L, p, q, seed).make_flat_slopes() / .sweep(n) / .interface_width()
+    lf::OccupancyLattice + make_random_alloy + kmc_mcs_sequential + open_bonds_per_particle
+        -> KmcLattice(L, eps, both_active, seed).make_random_alloy(c) / .sweep(n) / ...
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native
+from ._native import (ClosureError, Counters, CudaError, DeviceOutOfMemory, DomainError,  # noqa: F401
+                      InvalidArgument, KmcPlan, KpzPlan, LfgError, TransportError, check, device_count)
+
+__all__ = ["KpzLattice", "KmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
+           "DomainError", "CudaError", "device_count", "words2", "words3"]
+
+
+def words2(L: int) -> int:
+    return (L * L + 63) // 64
+
+
+def words3(L: int) -> int:
+    return (L * L * L + 63) // 64
+
+
+def _u64(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint64)
+    return a
+
+
+class KpzLattice:
+    """Device-resident slope field(s) advanced by the two-layer DTr sweep.
+
+    ``replicas > 1`` (or ``seeds=[...]``) holds independent lattices that one
+    launch advances together (ensembles, e.g. W(t) over 16 seeds).
+    """
+
+    def __init__(self, L: int, p: float = 1.0, q: float = 0.0, seed: int = 1, *, seeds=None,
+                 block_x: int = 0, block_y: int = 0, device: int = 0):
+        self._h = None
+        L_ = _native.lib()
+        seeds = [int(seed)] if seeds is None else [int(s) for s in seeds]
+        arr = (C.c_uint64 * len(seeds))(*seeds)
+        plan = KpzPlan(block_x, block_y)
+        h = C.c_void_p()
+        check(L_.lfg_kpz_create_batch(C.byref(h), L, float(p), float(q), arr, len(seeds), C.byref(plan), device))
+        self._h = h
+        self.L = int(L)
+        self.replicas = len(seeds)
+        self.device = device
+        got = KpzPlan()
+        check(L_.lfg_kpz_get_plan(h, C.byref(got)))
+        self.plan = (int(got.block_x), int(got.block_y))
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self) -> None:
+        if self._h is not None:
+            _native.lib().lfg_kpz_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- lattice state ----------------------------------------------------
+    def make_flat_slopes(self) -> "KpzLattice":
+        """make_flat_slopes (lattice.cpp:71-82) on every replica."""
+        check(_native.lib().lfg_kpz_init_flat(self._h))
+        return self
+
+    init_flat = make_flat_slopes
+
+    def upload(self, x, y, replica: int = 0) -> None:
+        x, y = _u64(x), _u64(y)
+        n = words2(self.L)
+        if x.size != n or y.size != n:
+            raise InvalidArgument(f"upload: expected {n} words per plane")
+        check(_native.lib().lfg_kpz_upload(self._h, replica, x.ctypes.data, y.ctypes.data, n))
+
+    def upload_ptr(self, x_ptr: int, y_ptr: int, replica: int = 0) -> None:
+        """Upload from raw host pointers (e.g. pinned torch tensors)."""
+        check(_native.lib().lfg_kpz_upload(self._h, replica, x_ptr, y_ptr, words2(self.L)))
+
+    def download(self, replica: int = 0):
+        n = words2(self.L)
+        x = np.empty(n, np.uint64)
+        y = np.empty(n, np.uint64)
+        check(_native.lib().lfg_kpz_download(self._h, replica, x.ctypes.data, y.ctypes.data, n))
+        return x, y
+
+    def download_ptr(self, x_ptr: int, y_ptr: int, replica: int = 0) -> None:
+        check(_native.lib().lfg_kpz_download(self._h, replica, x_ptr, y_ptr, words2(self.L)))
+
+    # -- dynamics ---------------------------------------------------------
+    def sweep(self, sweeps: int = 1):
+        """kpz_sweep_sequential(f, params, rng, sweeps) (kpz.cpp:5-19) -> Counters
+        (a list of Counters when replicas > 1)."""
+        out = (Counters * self.replicas)()
+        check(_native.lib().lfg_kpz_sweep(self._h, int(sweeps), out))
+        return out[0] if self.replicas == 1 else list(out)
+
+    def sweep_async(self, sweeps: int = 1) -> None:
+        check(_native.lib().lfg_kpz_sweep_async(self._h, int(sweeps)))
+
+    def phase(self, sweep: int, phase: int) -> None:
+        check(_native.lib().lfg_kpz_phase(self._h, int(sweep), int(phase)))
+
+    def counters(self, replica: int = 0) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kpz_counters(self._h, replica, C.byref(c)))
+        return c
+
+    def reset_counters(self) -> None:
+        check(_native.lib().lfg_kpz_reset_counters(self._h))
+
+    # -- observables ------------------------------------------------------
+    def width_sums(self, replica: int = 0):
+        s, s2 = C.c_int64(), C.c_int64()
+        check(_native.lib().lfg_kpz_width_sums(self._h, replica, C.byref(s), C.byref(s2)))
+        return int(s.value), int(s2.value)
+
+    def interface_width(self, replica: int = 0) -> float:
+        """interface_width(const SlopeField&) (kpz.cpp:62-81)."""
+        w = C.c_double()
+        check(_native.lib().lfg_kpz_interface_width(self._h, replica, C.byref(w)))
+        return float(w.value)
+
+    def reconstruct_heights(self, replica: int = 0) -> np.ndarray:
+        """reconstruct_heights (kpz.cpp:21-49) -> int32 [L, L] indexed [j, i]."""
+        h = np.empty(self.L * self.L, np.int32)
+        check(_native.lib().lfg_kpz_heights(self._h, replica, h.ctypes.data, h.size))
+        return h.reshape(self.L, self.L)
+
+    # -- state / plumbing -------------------------------------------------
+    def set_params(self, p: float, q: float) -> None:
+        check(_native.lib().lfg_kpz_set_params(self._h, float(p), float(q)))
+
+    @property
+    def sweep_index(self) -> int:
+        v = C.c_uint64()
+        check(_native.lib().lfg_kpz_get_sweep_index(self._h, C.byref(v)))
+        return int(v.value)
+
+    @sweep_index.setter
+    def sweep_index(self, v: int) -> None:
+        check(_native.lib().lfg_kpz_set_sweep_index(self._h, int(v)))
+
+    def set_seed(self, seed: int, replica: int = 0) -> None:
+        check(_native.lib().lfg_kpz_set_seed(self._h, replica, int(seed)))
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(_native.lib().lfg_kpz_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def synchronize(self) -> None:
+        check(_native.lib().lfg_kpz_synchronize(self._h))
+
+    def device_spins(self, replica: int = 0):
+        p, n = C.c_void_p(), C.c_size_t()
+        check(_native.lib().lfg_kpz_device_spins(self._h, replica, C.byref(p), C.byref(n)))
+        return int(p.value or 0), int(n.value)
+
+
+class KmcLattice:
+    """Device-resident fcc binary-alloy occupancy advanced by the two-layer DT sweep."""
+
+    def __init__(self, L: int, eps: float = 1.5, both_active: bool = False, seed: int = 1, *,
+                 block: int = 0, device: int = 0):
+        self._h = None
+        L_ = _native.lib()
+        if not hasattr(L_, "lfg_kmc_create"):
+            raise ImportError("liblfg.so was built without the KMC path")
+        plan = KmcPlan(block)
+        h = C.c_void_p()
+        check(L_.lfg_kmc_create(C.byref(h), L, float(eps), int(bool(both_active)), int(seed), C.byref(plan),
+                                device))
+        self._h = h
+        self.L = int(L)
+        self.device = device
+        got = KmcPlan()
+        check(L_.lfg_kmc_get_plan(h, C.byref(got)))
+        self.plan = int(got.block)
+
+    def close(self) -> None:
+        if self._h is not None:
+            _native.lib().lfg_kmc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def upload(self, words) -> None:
+        w = _u64(words)
+        n = words3(self.L)
+        if w.size != n:
+            raise InvalidArgument(f"upload: expected {n} words")
+        check(_native.lib().lfg_kmc_upload(self._h, w.ctypes.data, n))
+
+    def download(self) -> np.ndarray:
+        n = words3(self.L)
+        w = np.empty(n, np.uint64)
+        check(_native.lib().lfg_kmc_download(self._h, w.ctypes.data, n))
+        return w
+
+    def make_random_alloy(self, c: float, seed: int) -> "KmcLattice":
+        """make_random_alloy (lattice.cpp:117-132) with the device counter RNG."""
+        check(_native.lib().lfg_kmc_init_random_alloy(self._h, float(c), int(seed)))
+        return self
+
+    def sweep(self, steps: int = 1) -> Counters:
+        """kmc_mcs_sequential (kmc.cpp:5-18) -> Counters."""
+        c = Counters()
+        check(_native.lib().lfg_kmc_sweep(self._h, int(steps), C.byref(c)))
+        return c
+
+    def sweep_async(self, steps: int = 1) -> None:
+        check(_native.lib().lfg_kmc_sweep_async(self._h, int(steps)))
+
+    def phase(self, sweep: int, phase: int) -> None:
+        check(_native.lib().lfg_kmc_phase(self._h, int(sweep), int(phase)))
+
+    def counters(self) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kmc_counters(self._h, C.byref(c)))
+        return c
+
+    def reset_counters(self) -> None:
+        check(_native.lib().lfg_kmc_reset_counters(self._h))
+
+    def open_bond_sums(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(_native.lib().lfg_kmc_open_bond_sums(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def open_bonds_per_particle(self) -> float:
+        """open_bonds_per_particle (kmc.cpp:20-40)."""
+        v = C.c_double()
+        check(_native.lib().lfg_kmc_open_bonds_per_particle(self._h, C.byref(v)))
+        return float(v.value)
+
+    def count_b(self) -> int:
+        v = C.c_int64()
+        check(_native.lib().lfg_kmc_count_b(self._h, C.byref(v)))
+        return int(v.value)
+
+    def set_params(self, eps: float, both_active: bool) -> None:
+        check(_native.lib().lfg_kmc_set_params(self._h, float(eps), int(bool(both_active))))
+
+    @property
+    def sweep_index(self) -> int:
+        v = C.c_uint64()
+        check(_native.lib().lfg_kmc_get_sweep_index(self._h, C.byref(v)))
+        return int(v.value)
+
+    @sweep_index.setter
+    def sweep_index(self, v: int) -> None:
+        check(_native.lib().lfg_kmc_set_sweep_index(self._h, int(v)))
+
+    def set_seed(self, seed: int) -> None:
+        check(_native.lib().lfg_kmc_set_seed(self._h, int(seed)))
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(_native.lib().lfg_kmc_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def synchronize(self) -> None:
+        check(_native.lib().lfg_kmc_synchronize(self._h))
+
+    def device_words(self):
+        p, n = C.c_void_p(), C.c_size_t()
+        check(_native.lib().lfg_kmc_device_words(self._h, C.byref(p), C.byref(n)))
+        return int(p.value or 0), int(n.value)

@@ -1,0 +1,475 @@
+// capi_kpz.cu -- C ABI for the KPZ path (include/lfg.h), host orchestration.
+//
+// One handle = `replicas` L x L spin lattices resident in HBM (a single
+// allocation, replica-major) plus the counter-based RNG state (seed per
+// replica, next sweep index).  A sweep is four launches of the DTr phase
+// kernel, one per block set in the order drawn for that sweep; the kernel
+// derives origin/permutation from (seed, sweep) itself, so the host only
+// enqueues.  Counters accumulate on the device and are read back once per
+// lfg_kpz_sweep call.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "capi_common.cuh"
+#include "kpz_kernels.cuh"
+#include "lfg_common.cuh"
+
+namespace lfg {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace lfg
+
+using namespace lfg;
+
+struct lfg_kpz {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int32_t L = 0, bx = 0, by = 0, R = 1;
+    double p = 1.0, q = 0.0;
+    uint64_t sweep = 0;
+    std::vector<uint64_t> seeds;
+    uint32_t* f = nullptr;                  // [R][L][L/32]
+    uint64_t* dseeds = nullptr;             // [R]
+    unsigned long long* dcnt = nullptr;     // [R][2]
+    std::vector<unsigned long long> hcnt;   // cumulative host mirror (valid when !stale)
+    std::vector<int64_t> attempts;          // cumulative attempts per replica
+    // scratch (lazy)
+    uint32_t* sx = nullptr;                 // [L][L/32] slope planes staging
+    uint32_t* sy = nullptr;
+    uint8_t* f0 = nullptr;                  // [L]
+    uint32_t* fnew = nullptr;               // [L][L/32]
+    unsigned long long* dmis = nullptr;     // mismatch counter
+    int32_t* H0 = nullptr;                  // [L]
+    int32_t* P1 = nullptr;                  // [G][L]
+    int32_t* Dd = nullptr;                  // [G][L]
+    unsigned long long* wout = nullptr;     // [3]
+    int32_t* hbuf = nullptr;                // [L][L] heights (small L)
+    unsigned long long* hpin = nullptr;     // pinned readback [max(3, 2R)]
+
+    size_t words_per_replica() const { return size_t(L) * size_t(L / 32); }
+    uint32_t* rep(int r) const { return f + size_t(r) * words_per_replica(); }
+};
+
+namespace {
+
+void validate_params(double p, double q) {  // KpzParams::validate (kpz.hpp:19-26)
+    if (!(p >= 0.0 && p <= 1.0) || !(q >= 0.0 && q <= 1.0))
+        throw Error(LFG_EINVAL, "KpzParams: p and q must lie in [0,1]");
+    if (p + q <= 0.0) throw Error(LFG_EINVAL, "KpzParams: p + q must be positive");
+}
+
+void validate_size(int32_t L) {  // check_size (lattice.cpp:10-16)
+    if (L < 4 || !is_pow2(L))
+        throw Error(LFG_EINVAL, "SlopeField: size must be a power of two >= 4, got " + std::to_string(L));
+    if (L < 64)
+        throw Error(LFG_EINVAL, "DtrPlan: the KPZ two-layer DTr needs L >= 64 (two 32-site tiles per block "
+                                "set and axis), got " + std::to_string(L));
+}
+
+void resolve_plan(lfg_kpz* h, const lfg_kpz_plan* plan) {
+    int32_t bx = plan && plan->block_x ? plan->block_x : std::min<int32_t>(1024, h->L / 2);
+    int32_t by = plan && plan->block_y ? plan->block_y : std::min<int32_t>(128, h->L / 2);
+    if (bx < 32 || bx > 1024 || bx % 32 || !is_pow2(bx) || h->L % (2 * bx))
+        throw Error(LFG_EINVAL, "DtrPlan: block_x must be a power of two in [32, min(1024, L/2)], got " +
+                                    std::to_string(bx));
+    if (by < 16 || by > 128 || by % 16 || !is_pow2(by) || h->L % (2 * by))
+        throw Error(LFG_EINVAL, "DtrPlan: block_y must be a power of two in [16, min(128, L/2)], got " +
+                                    std::to_string(by));
+    h->bx = bx;
+    h->by = by;
+}
+
+void check_handle(const lfg_kpz* h) {
+    if (!h) throw Error(LFG_EINVAL, "null lfg_kpz handle");
+}
+
+void check_replica(const lfg_kpz* h, int32_t r) {
+    if (r < 0 || r >= h->R) throw Error(LFG_EINVAL, "replica index out of range: " + std::to_string(r));
+}
+
+void ensure_slope_scratch(lfg_kpz* h) {
+    if (!h->sx) h->sx = dmalloc<uint32_t>(h->words_per_replica(), "alloc slope staging");
+    if (!h->sy) h->sy = dmalloc<uint32_t>(h->words_per_replica(), "alloc slope staging");
+}
+
+void ensure_width_scratch(lfg_kpz* h) {
+    const int S = kpz_width_segment_rows(h->L), G = h->L / S;
+    if (!h->H0) h->H0 = dmalloc<int32_t>(size_t(h->L), "alloc width scratch");
+    if (!h->P1) h->P1 = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
+    if (!h->Dd) h->Dd = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
+    if (!h->wout) h->wout = dmalloc<unsigned long long>(3, "alloc width scratch");
+}
+
+void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel execution"); }
+
+void enqueue_sweeps(lfg_kpz* h, int64_t n) {
+    KpzPhaseArgs a{};
+    a.f = h->f;
+    a.counters = h->dcnt;
+    a.L = h->L;
+    a.bx = h->bx;
+    a.by = h->by;
+    a.thrP = threshold32(h->p);
+    a.thrQ = threshold32(h->q);
+    a.general = !(h->p == 1.0 && h->q == 0.0);
+    for (int64_t s = 0; s < n; ++s) {
+        a.sweep = h->sweep + uint64_t(s);
+        for (int k = 0; k < 4; ++k) {
+            a.phase = k;
+            cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
+        }
+    }
+    h->sweep += uint64_t(n);
+    for (int r = 0; r < h->R; ++r) h->attempts[size_t(r)] += int64_t(h->L) * h->L * n;
+}
+
+void read_counters(lfg_kpz* h) {
+    cuda_check(cudaMemcpyAsync(h->hpin, h->dcnt, sizeof(unsigned long long) * 2 * h->R, cudaMemcpyDeviceToHost,
+                               h->stream), "counter readback");
+    sync(h);
+    std::memcpy(h->hcnt.data(), h->hpin, sizeof(unsigned long long) * 2 * h->R);
+}
+
+lfg_counters make_counters(int64_t att, unsigned long long dep, unsigned long long det) {
+    lfg_counters c;
+    c.attempts = att;
+    c.deposits = int64_t(dep);
+    c.detaches = int64_t(det);
+    c.successes = c.deposits + c.detaches;
+    return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lfg_last_error(void) { return g_last_error.c_str(); }
+int lfg_abi_version(void) { return LFG_ABI_VERSION; }
+
+int lfg_device_count(int* count) {
+    return guarded([&] {
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *count = n;
+    });
+}
+
+int lfg_kpz_create_batch(lfg_kpz** out, int32_t L, double p, double q, const uint64_t* seeds, int32_t replicas,
+                         const lfg_kpz_plan* plan, int32_t device) {
+    return guarded([&] {
+        if (!out) throw Error(LFG_EINVAL, "null output handle");
+        *out = nullptr;
+        validate_size(L);
+        validate_params(p, q);
+        if (replicas < 1 || !seeds) throw Error(LFG_EINVAL, "replicas must be >= 1 with one seed each");
+        auto* h = new lfg_kpz();
+        try {
+            h->L = L;
+            h->p = p;
+            h->q = q;
+            h->R = replicas;
+            h->device = device;
+            resolve_plan(h, plan);
+            h->seeds.assign(seeds, seeds + replicas);
+            h->hcnt.assign(size_t(2 * replicas), 0);
+            h->attempts.assign(size_t(replicas), 0);
+            DeviceGuard g(device);
+            cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            h->own_stream = true;
+            cuda_check(kpz_phase_kernel_attrs(), "kernel attributes");
+            h->f = dmalloc<uint32_t>(h->words_per_replica() * size_t(replicas), "alloc lattice");
+            h->dseeds = dmalloc<uint64_t>(size_t(replicas), "alloc seeds");
+            h->dcnt = dmalloc<unsigned long long>(size_t(2 * replicas), "alloc counters");
+            cuda_check(cudaMallocHost(&h->hpin, sizeof(unsigned long long) * std::max(3, 2 * replicas)),
+                       "alloc pinned");
+            cuda_check(cudaMemcpyAsync(h->dseeds, seeds, sizeof(uint64_t) * replicas, cudaMemcpyHostToDevice,
+                                       h->stream), "seed upload");
+            cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 2 * replicas, h->stream), "memset");
+            // SlopeField(L) starts with every slope -1 (lattice.cpp:20-25): spins f(i,j) = (i + j) & 1.
+            cuda_check(kpz_launch_init_zero_slopes(h->f, L, replicas, h->stream), "init");
+            cuda_check(cudaStreamSynchronize(h->stream), "create");
+        } catch (...) {
+            lfg_kpz_destroy(h);
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int lfg_kpz_create(lfg_kpz** out, int32_t L, double p, double q, uint64_t seed, const lfg_kpz_plan* plan,
+                   int32_t device) {
+    return lfg_kpz_create_batch(out, L, p, q, &seed, 1, plan, device);
+}
+
+int lfg_kpz_destroy(lfg_kpz* h) {
+    if (!h) return LFG_OK;
+    {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(h->device);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        dfree(h->f);
+        dfree(h->dseeds);
+        dfree(h->dcnt);
+        dfree(h->sx);
+        dfree(h->sy);
+        dfree(h->f0);
+        dfree(h->fnew);
+        dfree(h->dmis);
+        dfree(h->H0);
+        dfree(h->P1);
+        dfree(h->Dd);
+        dfree(h->wout);
+        dfree(h->hbuf);
+        if (h->hpin) cudaFreeHost(h->hpin);
+        if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    delete h;
+    return LFG_OK;
+}
+
+int lfg_kpz_get_plan(const lfg_kpz* h, lfg_kpz_plan* out) {
+    return guarded([&] {
+        check_handle(h);
+        out->block_x = h->bx;
+        out->block_y = h->by;
+    });
+}
+
+int lfg_kpz_init_flat(lfg_kpz* h) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        cuda_check(kpz_launch_init_flat(h->f, h->L, h->R, h->stream), "init_flat");
+        sync(h);
+    });
+}
+
+int lfg_kpz_upload(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        const size_t need = size_t(h->L) * h->L / 64;
+        if (nwords != need || !x || !y)
+            throw Error(LFG_EINVAL, "upload: expected " + std::to_string(need) + " words per plane");
+        DeviceGuard g(h->device);
+        ensure_slope_scratch(h);
+        if (!h->f0) h->f0 = dmalloc<uint8_t>(size_t(h->L), "alloc scratch");
+        if (!h->fnew) h->fnew = dmalloc<uint32_t>(h->words_per_replica(), "alloc scratch");
+        if (!h->dmis) h->dmis = dmalloc<unsigned long long>(1, "alloc scratch");
+        const size_t bytes = need * 8;
+        cuda_check(cudaMemcpyAsync(h->sx, x, bytes, cudaMemcpyHostToDevice, h->stream), "upload x");
+        cuda_check(cudaMemcpyAsync(h->sy, y, bytes, cudaMemcpyHostToDevice, h->stream), "upload y");
+        cuda_check(kpz_launch_from_slopes(h->sx, h->sy, h->L, h->f0, h->fnew, h->stream), "slopes->spins");
+        cuda_check(cudaMemsetAsync(h->dmis, 0, 8, h->stream), "memset");
+        cuda_check(kpz_launch_to_slopes(h->fnew, h->L, nullptr, nullptr, h->sx, h->sy, h->dmis, h->stream),
+                   "closure check");
+        cuda_check(cudaMemcpyAsync(h->hpin, h->dmis, 8, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        if (h->hpin[0] != 0)
+            throw Error(LFG_ECLOSURE,
+                        "reconstruct_heights: slope field violates closure; heights would be path-dependent");
+        cuda_check(cudaMemcpyAsync(h->rep(replica), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice,
+                                   h->stream), "commit");
+        sync(h);
+    });
+}
+
+int lfg_kpz_download(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size_t nwords) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        const size_t need = size_t(h->L) * h->L / 64;
+        if (nwords != need || !x || !y)
+            throw Error(LFG_EINVAL, "download: expected " + std::to_string(need) + " words per plane");
+        DeviceGuard g(h->device);
+        ensure_slope_scratch(h);
+        cuda_check(kpz_launch_to_slopes(h->rep(replica), h->L, h->sx, h->sy, nullptr, nullptr, nullptr, h->stream),
+                   "spins->slopes");
+        cuda_check(cudaMemcpyAsync(x, h->sx, need * 8, cudaMemcpyDeviceToHost, h->stream), "download x");
+        cuda_check(cudaMemcpyAsync(y, h->sy, need * 8, cudaMemcpyDeviceToHost, h->stream), "download y");
+        sync(h);
+    });
+}
+
+int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out) {
+    return guarded([&] {
+        check_handle(h);
+        if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
+        DeviceGuard g(h->device);
+        read_counters(h);
+        std::vector<unsigned long long> before = h->hcnt;
+        enqueue_sweeps(h, n_mcs);
+        read_counters(h);
+        if (out)
+            for (int r = 0; r < h->R; ++r)
+                out[r] = make_counters(int64_t(h->L) * h->L * n_mcs, h->hcnt[2 * r] - before[2 * r],
+                                       h->hcnt[2 * r + 1] - before[2 * r + 1]);
+    });
+}
+
+int lfg_kpz_sweep_async(lfg_kpz* h, int64_t n_mcs) {
+    return guarded([&] {
+        check_handle(h);
+        if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
+        DeviceGuard g(h->device);
+        enqueue_sweeps(h, n_mcs);
+    });
+}
+
+int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase) {
+    return guarded([&] {
+        check_handle(h);
+        if (phase < 0 || phase > 3) throw Error(LFG_EINVAL, "phase must be in 0..3");
+        DeviceGuard g(h->device);
+        KpzPhaseArgs a{};
+        a.f = h->f;
+        a.counters = h->dcnt;
+        a.L = h->L;
+        a.bx = h->bx;
+        a.by = h->by;
+        a.thrP = threshold32(h->p);
+        a.thrQ = threshold32(h->q);
+        a.general = !(h->p == 1.0 && h->q == 0.0);
+        a.sweep = sweep;
+        a.phase = phase;
+        cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
+    });
+}
+
+int lfg_kpz_counters(lfg_kpz* h, int32_t replica, lfg_counters* out) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        DeviceGuard g(h->device);
+        read_counters(h);
+        *out = make_counters(h->attempts[size_t(replica)], h->hcnt[2 * replica], h->hcnt[2 * replica + 1]);
+    });
+}
+
+int lfg_kpz_reset_counters(lfg_kpz* h) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 2 * h->R, h->stream), "memset");
+        sync(h);
+        std::fill(h->hcnt.begin(), h->hcnt.end(), 0ull);
+        std::fill(h->attempts.begin(), h->attempts.end(), 0ll);
+    });
+}
+
+int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        DeviceGuard g(h->device);
+        ensure_width_scratch(h);
+        cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
+        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->wout, h->stream), "width scan");
+        cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        *sum = int64_t(h->hpin[0]);
+        *sum2 = int64_t(h->hpin[1] + h->hpin[2]);
+    });
+}
+
+int lfg_kpz_interface_width(lfg_kpz* h, int32_t replica, double* w2) {
+    int64_t s = 0, s2 = 0;
+    const int rc = lfg_kpz_width_sums(h, replica, &s, &s2);
+    if (rc != LFG_OK) return rc;
+    const double n = double(int64_t(h->L) * h->L);  // kpz.cpp:78-80
+    const double mean = double(s) / n;
+    *w2 = double(s2) / n - mean * mean;
+    return LFG_OK;
+}
+
+int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        const size_t need = size_t(h->L) * h->L;
+        if (n != need || !heights) throw Error(LFG_EINVAL, "heights: expected L*L entries");
+        if (h->L > 16384) throw Error(LFG_EINVAL, "heights: L*L int32 readout limited to L <= 16384");
+        DeviceGuard g(h->device);
+        ensure_width_scratch(h);
+        if (!h->hbuf) h->hbuf = dmalloc<int32_t>(need, "alloc heights");
+        cuda_check(kpz_launch_heights(h->rep(replica), h->L, h->H0, h->hbuf, h->stream), "heights");
+        cuda_check(cudaMemcpyAsync(heights, h->hbuf, need * 4, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+    });
+}
+
+int lfg_kpz_set_params(lfg_kpz* h, double p, double q) {
+    return guarded([&] {
+        check_handle(h);
+        validate_params(p, q);
+        h->p = p;
+        h->q = q;
+    });
+}
+
+int lfg_kpz_set_sweep_index(lfg_kpz* h, uint64_t sweep) {
+    return guarded([&] {
+        check_handle(h);
+        h->sweep = sweep;
+    });
+}
+
+int lfg_kpz_get_sweep_index(const lfg_kpz* h, uint64_t* sweep) {
+    return guarded([&] {
+        check_handle(h);
+        *sweep = h->sweep;
+    });
+}
+
+int lfg_kpz_set_seed(lfg_kpz* h, int32_t replica, uint64_t seed) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        DeviceGuard g(h->device);
+        h->seeds[size_t(replica)] = seed;
+        cuda_check(cudaMemcpyAsync(h->dseeds, h->seeds.data(), 8 * size_t(h->R), cudaMemcpyHostToDevice, h->stream),
+                   "seed upload");
+        sync(h);
+    });
+}
+
+int lfg_kpz_set_stream(lfg_kpz* h, void* stream) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        sync(h);
+        if (h->own_stream) cudaStreamDestroy(h->stream);
+        h->own_stream = false;
+        h->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int lfg_kpz_synchronize(lfg_kpz* h) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        sync(h);
+    });
+}
+
+int lfg_kpz_device_spins(lfg_kpz* h, int32_t replica, void** ptr, size_t* bytes) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        *ptr = h->rep(replica);
+        *bytes = h->words_per_replica() * 4;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,494 @@
+// kpz_kernels.cu -- sm_100a kernels for the 2+1-d KPZ octahedron model.
+//
+// Representation on the device ("spins").  The reference stores two slope
+// planes sigma_x, sigma_y (lattice.hpp:56-97).  The device stores ONE bit per
+// site, f(i,j), with
+//     sigma_x(i,j) = +1  <=>  f(i,j) == f(i-1,j)
+//     sigma_y(i,j) = +1  <=>  f(i,j) == f(i,j-1)
+// i.e. f = (h >> 1) ^ ((i+j) >> 1) (mod 2) for the integer height h.  Every
+// integrable slope field (closure, kpz.cpp:35-47) has exactly two spin fields
+// (f and ~f give the same slopes; the device fixes f(0,0)=0).  In spins the
+// octahedron move of kpz_attempt_impl (kpz.hpp:71-107) reads
+//     deposit  <=> f_R == f_S, f_U == f_S, f_L != f_S, f_D != f_S   (r < p)
+//     detach   <=> f_R != f_S, f_U != f_S, f_L == f_S, f_D == f_S   (r < q)
+// and flips the single bit f_S (which negates the four stencil slopes).  This
+// halves HBM/SMEM footprint and turns the 4-bit RMW into a 1-bit RMW; uploads
+// and downloads convert to/from the reference word layout exactly.
+//
+// Layout in HBM: replica-major, row-major, L/32 little-endian uint32 words per
+// row, bit i&31 of word i>>5 -- so row j is contiguous and 128-bit loadable.
+#include <algorithm>
+#include <cstdint>
+
+#include "kpz_kernels.cuh"
+#include "lfg_common.cuh"
+
+namespace lfg {
+
+// ============================================================ DTr phase kernel
+// One CTA = one active device block (bx x by sites) of one replica.
+// Threads: one warp per tile row (by/16 warps), lane = tile column (bx/32
+// lanes active).  Shared-memory layout (32-bit words, 256-byte lines):
+//   line 0, words 0..31     : the block's 512 inner-set draws (2 bits each)
+//   line R+8, word s        : staged spins of block row R (R = -1 .. by),
+//                             s = 0..Wt-1 tile words, s = Wt the right halo
+//                             word (H_R); the left halo word (H_L) of row R
+//                             sits at line R+7, word 63.
+// With a 64-word line stride every tile column owns one bank for all its
+// rows, so the per-round gathers (own/up/down words) are conflict-free, and
+// the neighbour-word gather is a lane rotation that lands the block's edge
+// lanes exactly on H_L / H_R (bank 31 / bank Wt).
+__device__ __forceinline__ int sm_slot(int R, int s) {
+    return s < 0 ? (R + 7) * 64 + 63 : (R + 8) * 64 + s;
+}
+
+__device__ __forceinline__ uint32_t sel4(const U4& v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ void count_if_nonzero(uint32_t& n, uint32_t v) {
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(n) : "r"(v));
+}
+
+// Inner single-hit rounds of one block activation.  Per round every tile's
+// active domain makes one attempt; the inner set (hx, hy) is block-uniform
+// and lives in uniform registers, the anchor is per lane:
+//   xd = bits 4(k&7) of A[k>>3], yd = bits 3k of A.z (k<10) / 3(k-10) of A.w.
+// Lane byte address of the anchor word = lane_base | (yd << 8): tile rows are
+// 256-byte lines and lane_base has bits 8..10 clear, so one LOP3 forms it.
+template <bool GENERAL, bool FULL>
+__device__ __forceinline__ void kpz_block_rounds(char* smb, uint32_t lane_base, bool active, uint64_t seed,
+                                                 uint64_t sweep, uint32_t block_id, uint32_t tile_id,
+                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
+    U4 V = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int m = 0; m < kRounds / 16; ++m) {
+        if ((m & 3) == 0) V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m >> 2));
+        const uint32_t setw = sel4(V, m & 3);
+        const U4 A = draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(m));
+        U4 Uw = {0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (GENERAL && (k & 3) == 0) Uw = draw(seed, sweep, TAG_ACCEPT, tile_id, uint32_t(4 * m + (k >> 2)));
+            const uint32_t s2 = (setw >> (2 * k)) & 3u;
+            const uint32_t hx = s2 & 1u;
+            const int hyoff = int(s2 >> 1) << 11;  // +8 rows
+            const int nbo = hx ? 4 : -4;
+            const uint32_t xw = k < 8 ? A.x : A.y;
+            const uint32_t c = ((xw >> (4 * (k & 7))) & 15u) | (hx << 4);
+            const uint32_t yw = k < 10 ? A.z : A.w;
+            const int ysh = 3 * (k < 10 ? k : k - 10);
+            const uint32_t ybits = ysh <= 8 ? (yw << (8 - ysh)) : (yw >> (ysh - 8));
+            const uint32_t addr = lane_base | (ybits & 0x700u);
+            if (FULL || active) {
+                char* pw = smb + hyoff + addr;
+                const uint32_t own = *reinterpret_cast<const uint32_t*>(pw);
+                const uint32_t up = *reinterpret_cast<const uint32_t*>(pw + 256);
+                const uint32_t dn = *reinterpret_cast<const uint32_t*>(pw - 256);
+                const uint32_t nb = *reinterpret_cast<const uint32_t*>(pw + nbo);
+                const uint32_t eR = own ^ __funnelshift_r(own, nb, 1);
+                const uint32_t eL = own ^ __funnelshift_l(nb, own, 1);
+                const uint32_t bit = 1u << c;
+                uint32_t flip;
+                if (!GENERAL) {
+                    flip = ~(eR | (own ^ up)) & eL & (own ^ dn) & bit;
+                    count_if_nonzero(ndep, flip);
+                } else {
+                    const uint32_t u = sel4(Uw, k & 3);
+                    const uint32_t okP = uint64_t(u) < thrP ? bit : 0u;
+                    const uint32_t okQ = uint64_t(u) < thrQ ? bit : 0u;
+                    const uint32_t dep = ~(eR | (own ^ up)) & eL & (own ^ dn) & okP;
+                    const uint32_t det = eR & (own ^ up) & ~(eL | (own ^ dn)) & okQ;
+                    flip = dep | det;
+                    count_if_nonzero(ndep, dep);
+                    count_if_nonzero(ndet, det);
+                }
+                *reinterpret_cast<uint32_t*>(pw) = own ^ flip;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <bool GENERAL, bool FULL>
+__global__ void __launch_bounds__(256, 6) kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int L = a.L, Lm = L - 1, wpr = L >> 5, wmask = wpr - 1;
+    const int Wt = a.bx >> 5, Ty = a.by >> 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int rep = a.rep0 + int(blockIdx.z);
+    const uint64_t seed = a.seeds[blockIdx.z];
+    const uint64_t sweep = a.sweep;
+    uint32_t* __restrict__ f = a.f + size_t(rep) * size_t(L) * size_t(wpr);
+
+    const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, sweep);
+    const int set = sw.set(a.phase);
+    const int bxi = 2 * int(blockIdx.x) + (set & 1);
+    const int byi = 2 * int(blockIdx.y) + (set >> 1);
+    const uint32_t block_id = uint32_t(byi) * uint32_t(L / a.bx) + uint32_t(bxi);
+    const int X0 = (sw.ox + bxi * a.bx) & Lm;
+    const int Y0 = (sw.oy + byi * a.by) & Lm;
+    const int b = X0 & 31;
+    const int w0 = ((X0 - 32 + L) & Lm) >> 5;
+
+    // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin away.
+    for (int R = warp - 1; R <= a.by; R += nwarps) {
+        const uint32_t* __restrict__ row = f + size_t((Y0 + R) & Lm) * wpr;
+        for (int k = lane; k < Wt + 2; k += 32) {
+            const uint32_t lo = row[(w0 + k) & wmask];
+            const uint32_t hi = row[(w0 + k + 1) & wmask];
+            sm[sm_slot(R, k - 1)] = __funnelshift_r(lo, hi, b);
+        }
+    }
+    __syncthreads();
+
+    const int tx = lane, ty = warp;
+    const uint32_t tile_id = uint32_t(byi * Ty + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
+    const uint32_t lane_base = uint32_t((16 * ty + 8) * 256 + 4 * tx);
+    uint32_t ndep = 0, ndet = 0;
+    kpz_block_rounds<GENERAL, FULL>(reinterpret_cast<char*>(sm), lane_base, tx < Wt, seed, sweep, block_id,
+                                    tile_id, a.thrP, a.thrQ, ndep, ndet);
+
+    // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
+    for (int R = warp; R < a.by; R += nwarps) {
+        uint32_t* __restrict__ row = f + size_t((Y0 + R) & Lm) * wpr;
+        for (int k = lane; k <= Wt; k += 32) {
+            if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
+            row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
+        }
+    }
+    // Counters: deposits, detaches per replica.
+    ndep = __reduce_add_sync(0xFFFFFFFFu, ndep);
+    if (GENERAL) ndet = __reduce_add_sync(0xFFFFFFFFu, ndet);
+    if (lane == 0) {
+        if (ndep) atomicAdd(a.counters + 2 * rep + 0, (unsigned long long)ndep);
+        if (GENERAL && ndet) atomicAdd(a.counters + 2 * rep + 1, (unsigned long long)ndet);
+    }
+}
+
+size_t kpz_phase_smem_bytes(int by) { return size_t(by + 9) * 256; }
+
+cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st) {
+    const dim3 block(unsigned(32 * (a.by / 16)));
+    const size_t smem = kpz_phase_smem_bytes(a.by);
+    const bool full = a.bx == 1024;
+    for (int r0 = 0; r0 < replicas; r0 += kMaxRepPerLaunch) {
+        KpzPhaseArgs b = a;
+        b.rep0 = r0;
+        const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
+        for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
+        const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.L / a.by / 2), unsigned(nr));
+        if (a.general) {
+            if (full) kpz_dtr_phase_kernel<true, true><<<grid, block, smem, st>>>(b);
+            else kpz_dtr_phase_kernel<true, false><<<grid, block, smem, st>>>(b);
+        } else {
+            if (full) kpz_dtr_phase_kernel<false, true><<<grid, block, smem, st>>>(b);
+            else kpz_dtr_phase_kernel<false, false><<<grid, block, smem, st>>>(b);
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_phase_kernel_attrs() {
+    const int smem = int(kpz_phase_smem_bytes(128));
+    cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+    return e;
+}
+
+// ============================================================ init / convert
+// Row-periodic spin patterns: word = pat[j & 3] for row j.
+//   make_flat_slopes (lattice.cpp:71-82): f(i,j) = ((i+1)>>1 ^ (j+1)>>1) & 1
+//   SlopeField(L) all-zero slopes (lattice.cpp:20-25): f(i,j) = (i+j) & 1
+__global__ void kpz_init_pattern_kernel(uint32_t* f, int L, size_t nwords_total, uint4 pat) {
+    const int wpr = L >> 5;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nwords_total;
+         k += size_t(gridDim.x) * blockDim.x) {
+        const int j = int((k / size_t(wpr)) % size_t(L)) & 3;
+        f[k] = j == 0 ? pat.x : (j == 1 ? pat.y : (j == 2 ? pat.z : pat.w));
+    }
+}
+
+// Column-0 spins: f(0,j) = XOR_{k=1..j} ~sigma_y(0,k).  One CTA.
+__global__ void kpz_col0_kernel(const uint32_t* __restrict__ Y, int L, uint8_t* __restrict__ f0) {
+    __shared__ uint32_t part[1024];
+    const int wpr = L >> 5;
+    const int nt = blockDim.x, t = threadIdx.x;
+    const int chunk = (L + nt - 1) / nt;
+    const int j0 = t * chunk, j1 = min(L, j0 + chunk);
+    uint32_t p = 0;
+    for (int j = j0; j < j1; ++j)
+        if (j > 0) p ^= (~Y[size_t(j) * wpr]) & 1u;
+    part[t] = p;
+    __syncthreads();
+    // exclusive XOR scan over threads (serial over 1024 entries by thread 0 is cheap enough)
+    if (t == 0) {
+        uint32_t acc = 0;
+        for (int k = 0; k < nt; ++k) {
+            const uint32_t v = part[k];
+            part[k] = acc;
+            acc ^= v;
+        }
+    }
+    __syncthreads();
+    uint32_t acc = part[t];
+    for (int j = j0; j < j1; ++j) {
+        if (j > 0) acc ^= (~Y[size_t(j) * wpr]) & 1u;
+        f0[j] = uint8_t(acc);
+    }
+}
+
+__device__ __forceinline__ uint32_t prefix_xor32(uint32_t t) {
+    t ^= t << 1;
+    t ^= t << 2;
+    t ^= t << 4;
+    t ^= t << 8;
+    t ^= t << 16;
+    return t;
+}
+
+// Row spins: f(i,j) = f(0,j) ^ XOR_{k=1..i} ~sigma_x(k,j).  One warp per row.
+__global__ void kpz_rows_from_slopes_kernel(const uint32_t* __restrict__ X, const uint8_t* __restrict__ f0,
+                                            int L, uint32_t* __restrict__ f) {
+    const int wpr = L >> 5;
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (j >= L) return;
+    const int cs = (wpr + 31) / 32;
+    const int wbeg = lane * cs, wend = min(wpr, wbeg + cs);
+    const uint32_t* __restrict__ xr = X + size_t(j) * wpr;
+    uint32_t par = 0;
+    for (int w = wbeg; w < wend; ++w) {
+        uint32_t t = ~xr[w];
+        if (w == 0) t &= ~1u;
+        par ^= __popc(t) & 1u;
+    }
+    // exclusive XOR scan of parities across lanes
+    uint32_t inc = par;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc ^= v;
+    }
+    uint32_t carry = (inc ^ par) ^ uint32_t(f0[j]);
+    uint32_t* __restrict__ fr = f + size_t(j) * wpr;
+    for (int w = wbeg; w < wend; ++w) {
+        uint32_t t = ~xr[w];
+        if (w == 0) t &= ~1u;
+        const uint32_t p = prefix_xor32(t);
+        fr[w] = p ^ (carry ? 0xFFFFFFFFu : 0u);
+        carry ^= p >> 31;
+    }
+}
+
+// spins -> slopes, optionally comparing against given planes (mismatch count).
+__global__ void kpz_spins_to_slopes_kernel(const uint32_t* __restrict__ f, int L, uint32_t* __restrict__ X,
+                                           uint32_t* __restrict__ Y, const uint32_t* __restrict__ Xcmp,
+                                           const uint32_t* __restrict__ Ycmp, unsigned long long* mismatch) {
+    const int wpr = L >> 5, wmask = wpr - 1, Lm = L - 1;
+    const size_t n = size_t(L) * wpr;
+    unsigned long long bad = 0;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n; k += size_t(gridDim.x) * blockDim.x) {
+        const int j = int(k / size_t(wpr)), w = int(k % size_t(wpr));
+        const uint32_t F = f[k];
+        const uint32_t Fp = f[size_t(j) * wpr + ((w - 1) & wmask)];
+        const uint32_t Fd = f[size_t((j - 1) & Lm) * wpr + w];
+        const uint32_t sx = ~(F ^ ((F << 1) | (Fp >> 31)));
+        const uint32_t sy = ~(F ^ Fd);
+        if (X) X[k] = sx;
+        if (Y) Y[k] = sy;
+        if (Xcmp) bad += __popc(sx ^ Xcmp[k]) + __popc(sy ^ Ycmp[k]);
+    }
+    if (mismatch) {
+        bad = __reduce_add_sync(0xFFFFFFFFu, unsigned(bad));
+        if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatch, bad);
+    }
+}
+
+cudaError_t kpz_launch_init_flat(uint32_t* f, int L, int replicas, cudaStream_t st) {
+    const size_t n = size_t(replicas) * L * (L >> 5);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    kpz_init_pattern_kernel<<<blocks, 256, 0, st>>>(f, L, n,
+                                                    make_uint4(0x66666666u, 0x99999999u, 0x99999999u, 0x66666666u));
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_init_zero_slopes(uint32_t* f, int L, int replicas, cudaStream_t st) {
+    const size_t n = size_t(replicas) * L * (L >> 5);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    kpz_init_pattern_kernel<<<blocks, 256, 0, st>>>(f, L, n,
+                                                    make_uint4(0xAAAAAAAAu, 0x55555555u, 0xAAAAAAAAu, 0x55555555u));
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_from_slopes(const uint32_t* X, const uint32_t* Y, int L, uint8_t* f0_scratch,
+                                   uint32_t* f, cudaStream_t st) {
+    kpz_col0_kernel<<<1, 1024, 0, st>>>(Y, L, f0_scratch);
+    const int rows_per_block = 8;
+    kpz_rows_from_slopes_kernel<<<(L + rows_per_block - 1) / rows_per_block, 32 * rows_per_block, 0, st>>>(
+        X, f0_scratch, L, f);
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_to_slopes(const uint32_t* f, int L, uint32_t* X, uint32_t* Y, const uint32_t* Xcmp,
+                                 const uint32_t* Ycmp, unsigned long long* mismatch, cudaStream_t st) {
+    const size_t n = size_t(L) * (L >> 5);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    kpz_spins_to_slopes_kernel<<<blocks, 256, 0, st>>>(f, L, X, Y, Xcmp, Ycmp, mismatch);
+    return cudaGetLastError();
+}
+
+// ============================================================ W^2 scan
+// interface_width(const SlopeField&) (kpz.cpp:62-81): h(i,0) = sum_{k=1..i}
+// s_x(k,0); h(i,j) = h(i,j-1) + s_y(i,j); exact int64 sum and sum of squares.
+// Stage 1: row-0 heights H0[i] (one CTA).  Stage 2: per (row segment g, word
+// column w), relative column heights p (p = 0 at the segment's first row for
+// g = 0, else the first row's s_y) with P1 = sum p (per column), the final p
+// (D), and sum p^2 (global).  Stage 3: per column, walk the segments:
+//   sum h  += S_g H + P1,   sum h^2 += S_g H^2 + 2 H P1,   H += D.
+__global__ void kpz_row0_heights_kernel(const uint32_t* __restrict__ f, int L, int32_t* __restrict__ H0) {
+    __shared__ int32_t part[1024];
+    const int wpr = L >> 5, wmask = wpr - 1;
+    const int nt = blockDim.x, t = threadIdx.x;
+    const int chunk = (L + nt - 1) / nt;
+    const int i0 = t * chunk, i1 = min(L, i0 + chunk);
+    auto sx = [&](int i) -> int32_t {  // slope_x(i, 0) for i >= 1
+        const int w = i >> 5, bb = i & 31;
+        const uint32_t F = f[w];
+        const uint32_t left = bb ? (F >> (bb - 1)) : (f[(w - 1) & wmask] >> 31);
+        return (((F >> bb) ^ left) & 1u) ? -1 : 1;
+    };
+    int32_t s = 0;
+    for (int i = i0; i < i1; ++i)
+        if (i > 0) s += sx(i);
+    part[t] = s;
+    __syncthreads();
+    if (t == 0) {
+        int32_t acc = 0;
+        for (int k = 0; k < nt; ++k) {
+            const int32_t v = part[k];
+            part[k] = acc;
+            acc += v;
+        }
+    }
+    __syncthreads();
+    int32_t acc = part[t];
+    for (int i = i0; i < i1; ++i) {
+        if (i > 0) acc += sx(i);
+        H0[i] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(128) kpz_width_seg_kernel(const uint32_t* __restrict__ f, int L, int S,
+                                                            int32_t* __restrict__ P1, int32_t* __restrict__ D,
+                                                            unsigned long long* __restrict__ sum_p2) {
+    const int wpr = L >> 5, Lm = L - 1;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = blockIdx.y;
+    int32_t p[32], s1[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) { p[c] = 0; s1[c] = 0; }
+    long long s2 = 0;
+    if (w < wpr) {
+        const int j0 = g * S;
+        uint32_t prev = f[size_t((j0 - 1) & Lm) * wpr + w];
+        for (int j = j0; j < j0 + S; ++j) {
+            const uint32_t F = f[size_t(j) * wpr + w];
+            const uint32_t up = ~(F ^ prev);  // sigma_y(.,j) bits
+            prev = F;
+            const bool add = j > 0;
+            int32_t rowsq = 0;
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                if (add) p[c] += ((up >> c) & 1u) ? 1 : -1;
+                s1[c] += p[c];
+                rowsq += p[c] * p[c];
+            }
+            s2 += rowsq;
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+            P1[size_t(g) * L + 32 * w + c] = s1[c];
+            D[size_t(g) * L + 32 * w + c] = p[c];
+        }
+    }
+    // s2 >= 0 always; reduce within the warp then one atomic.
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_down_sync(0xFFFFFFFFu, s2, o);
+    if ((threadIdx.x & 31) == 0 && s2) atomicAdd(sum_p2, (unsigned long long)s2);
+}
+
+__global__ void kpz_width_combine_kernel(const int32_t* __restrict__ H0, const int32_t* __restrict__ P1,
+                                         const int32_t* __restrict__ D, int L, int S, int G,
+                                         unsigned long long* __restrict__ out /* sum, sum2 as int64 */) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    long long sh = 0, sh2 = 0;
+    if (c < L) {
+        long long H = H0[c];
+        for (int g = 0; g < G; ++g) {
+            const long long q1 = P1[size_t(g) * L + c];
+            sh += (long long)S * H + q1;
+            sh2 += (long long)S * H * H + 2 * H * q1;
+            H += D[size_t(g) * L + c];
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sh += __shfl_down_sync(0xFFFFFFFFu, sh, o);
+        sh2 += __shfl_down_sync(0xFFFFFFFFu, sh2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out + 0, (unsigned long long)sh);   // two's complement wraps exactly
+        atomicAdd(out + 1, (unsigned long long)sh2);
+    }
+}
+
+int kpz_width_segment_rows(int L) { return L >= 4096 ? 2048 : (L >= 256 ? 128 : L); }
+
+cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D,
+                             unsigned long long* out3, cudaStream_t st) {
+    const int S = kpz_width_segment_rows(L);
+    const int G = L / S;
+    const int wpr = L >> 5;
+    kpz_row0_heights_kernel<<<1, 1024, 0, st>>>(f, L, H0);
+    const dim3 g1(unsigned((wpr + 127) / 128), unsigned(G));
+    kpz_width_seg_kernel<<<g1, 128, 0, st>>>(f, L, S, P1, D, out3 + 2);
+    kpz_width_combine_kernel<<<(L + 255) / 256, 256, 0, st>>>(H0, P1, D, L, S, G, out3);
+    return cudaGetLastError();
+}
+
+// ============================================================ heights (small L)
+// reconstruct_heights (kpz.cpp:21-34) on the device: row 0 from H0, then each
+// column accumulates s_y.  Path-independence holds by construction for a
+// spin field (kpz.cpp:35-47 is checked at upload).
+__global__ void kpz_heights_kernel(const uint32_t* __restrict__ f, const int32_t* __restrict__ H0, int L,
+                                   int32_t* __restrict__ h) {
+    const int wpr = L >> 5, Lm = L - 1;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L) return;
+    int32_t v = H0[i];
+    h[i] = v;
+    const int w = i >> 5, bb = i & 31;
+    uint32_t prev = (f[w] >> bb) & 1u;
+    for (int j = 1; j < L; ++j) {
+        const uint32_t cur = (f[size_t(j) * wpr + w] >> bb) & 1u;
+        v += (cur == prev) ? 1 : -1;
+        prev = cur;
+        h[size_t(j) * L + i] = v;
+    }
+    (void)Lm;
+}
+
+cudaError_t kpz_launch_heights(const uint32_t* f, int L, int32_t* H0, int32_t* h, cudaStream_t st) {
+    kpz_row0_heights_kernel<<<1, 1024, 0, st>>>(f, L, H0);
+    kpz_heights_kernel<<<(L + 127) / 128, 128, 0, st>>>(f, H0, L, h);
+    return cudaGetLastError();
+}
+
+}  // namespace lfg

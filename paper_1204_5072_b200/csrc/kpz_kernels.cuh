@@ -1,0 +1,41 @@
+// kpz_kernels.cuh -- launchers for the KPZ device kernels (kpz_kernels.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace lfg {
+
+constexpr int kMaxRepPerLaunch = 64;
+
+// Passed as a __grid_constant__ kernel parameter: everything block-uniform
+// (seeds included) lives in the constant bank -> uniform registers.
+struct KpzPhaseArgs {
+    uint32_t* f;                    // spins, replica-major [R][L][L/32]
+    unsigned long long* counters;   // [R][2] deposits, detaches (device)
+    int32_t L, bx, by;
+    uint64_t sweep;                 // global sweep index
+    int32_t phase;                  // 0..3 position in the sweep's block-set order
+    uint64_t thrP, thrQ;            // ceil(p 2^32), ceil(q 2^32)
+    bool general;                   // false: p == 1, q == 0 fast path
+    int32_t rep0;                   // first replica of this launch (set by the launcher)
+    uint64_t seeds[kMaxRepPerLaunch];
+};
+
+size_t kpz_phase_smem_bytes(int by);
+cudaError_t kpz_phase_kernel_attrs();
+cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st);
+cudaError_t kpz_launch_init_flat(uint32_t* f, int L, int replicas, cudaStream_t st);
+cudaError_t kpz_launch_init_zero_slopes(uint32_t* f, int L, int replicas, cudaStream_t st);
+cudaError_t kpz_launch_from_slopes(const uint32_t* X, const uint32_t* Y, int L, uint8_t* f0_scratch,
+                                   uint32_t* f, cudaStream_t st);
+cudaError_t kpz_launch_to_slopes(const uint32_t* f, int L, uint32_t* X, uint32_t* Y, const uint32_t* Xcmp,
+                                 const uint32_t* Ycmp, unsigned long long* mismatch, cudaStream_t st);
+int kpz_width_segment_rows(int L);
+cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D,
+                             unsigned long long* out3, cudaStream_t st);
+cudaError_t kpz_launch_heights(const uint32_t* f, int L, int32_t* H0, int32_t* h, cudaStream_t st);
+
+}  // namespace lfg

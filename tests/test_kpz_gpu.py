@@ -1,0 +1,199 @@
+"""GPU parity tests for the KPZ DTr path (run with -m gpu on a B200).
+
+The CUDA path (paper_1204_5072_b200 -> liblfg.so) is compared bit-for-bit with
+  * the golden vectors produced by the unmodified reference
+    (tests/golden/golden.json: DTr schedule driving lf::detail::kpz_attempt_impl),
+  * the live oracle restatement (oracle/_build/liboracle.so) on seeded inputs.
+Tolerance: none -- integer/bit state must match exactly; W^2 is compared as
+the same double expression over exact int64 sums.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def lfg():
+    import paper_1204_5072_b200 as m
+
+    if m.device_count() < 1:
+        pytest.fail("no CUDA device visible to liblfg.so")
+    return m
+
+
+def test_flat_init_matches_reference(lfg, oracle, golden):
+    for g in golden["kpz_flat"]:
+        L = g["L"]
+        if L < 64:
+            continue
+        with lfg.KpzLattice(L) as k:
+            k.make_flat_slopes()
+            x, y = k.download()
+            assert sha(x) == g["sx"] and sha(y) == g["sy"]
+            assert k.interface_width() == g["w2"] == 0.5
+            assert k.width_sums() == (g["sum"], g["sum2"])
+
+
+def test_default_state_is_all_zero_slopes(lfg):
+    # SlopeField(L) constructor (lattice.cpp:20-25): all words zero.
+    with lfg.KpzLattice(64) as k:
+        x, y = k.download()
+        assert not x.any() and not y.any()
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_dtr_golden_bit_exact(lfg, golden, case):
+    g = golden["kpz_dtr"][case]
+    L = g["L"]
+    with lfg.KpzLattice(L, g["p"], g["q"], g["seed"], block_x=g["bx"], block_y=g["by"]) as k:
+        k.make_flat_slopes()
+        k.sweep_index = g["sweep0"]
+        c = k.sweep(g["nsweeps"])
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == g["counters"]
+        x, y = k.download()
+        assert sha(x) == g["sx"] and sha(y) == g["sy"]
+        assert k.width_sums() == (g["sum"], g["sum2"])
+        assert k.interface_width() == g["w2"]
+
+
+def test_dtr_live_oracle_random(lfg, oracle):
+    rs = np.random.RandomState(2024)
+    for _ in range(10):
+        L = int(rs.choice([64, 128, 256, 512]))
+        bx = int(rs.choice([b for b in (32, 64, 128, 256) if 2 * b <= L]))
+        by = int(rs.choice([b for b in (16, 32, 64, 128) if 2 * b <= L]))
+        p, q = [(1.0, 0.0), (0.95, 0.05), (0.3, 0.7), (0.0, 1.0), (1.0, 0.5)][rs.randint(5)]
+        seed = int(rs.randint(0, 2**63))
+        s0 = int(rs.randint(0, 1000))
+        x, y = oracle.kpz_flat(L)
+        c_ref = oracle.kpz_sweep_dtr(L, x, y, p, q, seed, s0, 3, bx, by)
+        with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by) as k:
+            k.make_flat_slopes()
+            k.sweep_index = s0
+            c = k.sweep(3)
+            gx, gy = k.download()
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist(), (L, bx, by, p, q)
+        assert (gx == x).all() and (gy == y).all(), (L, bx, by, p, q)
+
+
+def test_upload_download_roundtrip_and_continue(lfg, oracle):
+    L = 256
+    x, y = oracle.kpz_flat(L)
+    oracle.kpz_sweep_dtr(L, x, y, 0.7, 0.3, 9, 0, 4, 64, 32)  # a rough, closed field
+    with lfg.KpzLattice(L, 0.7, 0.3, 9, block_x=64, block_y=32) as k:
+        k.upload(x, y)
+        gx, gy = k.download()
+        assert (gx == x).all() and (gy == y).all()
+        assert k.width_sums() == oracle.kpz_width_sums(L, x, y)
+        assert (k.reconstruct_heights() == oracle.reconstruct_heights(L, x, y)).all()
+        # continue the trajectory from the uploaded state
+        k.sweep_index = 4
+        c = k.sweep(2)
+        c_ref = oracle.kpz_sweep_dtr(L, x, y, 0.7, 0.3, 9, 4, 2, 64, 32)
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist()
+        gx, gy = k.download()
+        assert (gx == x).all() and (gy == y).all()
+
+
+def test_upload_rejects_non_integrable(lfg, oracle):
+    L = 64
+    x, y = oracle.kpz_flat(L)
+    x[3] ^= np.uint64(1 << 5)  # single slope flip -> heights path-dependent
+    with lfg.KpzLattice(L) as k:
+        k.make_flat_slopes()
+        with pytest.raises(lfg.ClosureError, match="closure"):
+            k.upload(x, y)
+        # state unchanged after the failed upload
+        fx, fy = oracle.kpz_flat(L)
+        gx, gy = k.download()
+        assert (gx == fx).all() and (gy == fy).all()
+
+
+def test_wrong_word_count_rejected(lfg):
+    with lfg.KpzLattice(64) as k:
+        with pytest.raises(lfg.InvalidArgument):
+            k.upload(np.zeros(10, np.uint64), np.zeros(10, np.uint64))
+
+
+def test_split_sweeps_equal_one_call(lfg):
+    # counter-based RNG: (seed, sweep index) -> exact resume
+    L = 256
+    with lfg.KpzLattice(L, 1.0, 0.0, 5) as a, lfg.KpzLattice(L, 1.0, 0.0, 5) as b:
+        a.make_flat_slopes()
+        b.make_flat_slopes()
+        ca = a.sweep(5)
+        cb1 = b.sweep(2)
+        cb2 = b.sweep(3)
+        assert ca.successes == cb1.successes + cb2.successes
+        assert b.sweep_index == 5
+        xa, ya = a.download()
+        xb, yb = b.download()
+        assert (xa == xb).all() and (ya == yb).all()
+
+
+def test_phase_api_equals_sweep(lfg):
+    L = 512
+    with lfg.KpzLattice(L, 1.0, 0.0, 77) as a, lfg.KpzLattice(L, 1.0, 0.0, 77) as b:
+        a.make_flat_slopes()
+        b.make_flat_slopes()
+        a.sweep(2)
+        for s in range(2):
+            for ph in range(4):
+                b.phase(s, ph)
+        b.synchronize()
+        assert a.counters().deposits == b.counters().deposits
+        xa, ya = a.download()
+        xb, yb = b.download()
+        assert (xa == xb).all() and (ya == yb).all()
+
+
+def test_replica_batch_equals_single_runs(lfg):
+    L = 256
+    seeds = [3, 11, 2**40 + 7]
+    with lfg.KpzLattice(L, 0.95, 0.05, seeds=seeds) as kb:
+        kb.make_flat_slopes()
+        cs = kb.sweep(3)
+        for r, s in enumerate(seeds):
+            with lfg.KpzLattice(L, 0.95, 0.05, s) as k1:
+                k1.make_flat_slopes()
+                c1 = k1.sweep(3)
+                assert (cs[r].deposits, cs[r].detaches) == (c1.deposits, c1.detaches)
+                assert all((a == b).all() for a, b in zip(kb.download(r), k1.download()))
+
+
+def test_large_lattice_properties(lfg, oracle):
+    # L=4096 with the production block geometry (1024 x 128): exact accounting,
+    # closure, W^2 consistency between the device scan and the oracle scan.
+    L = 4096
+    with lfg.KpzLattice(L, 1.0, 0.0, 1) as k:
+        assert k.plan == (1024, 128)
+        k.make_flat_slopes()
+        c = k.sweep(3)
+        assert c.attempts == 3 * L * L and c.successes == c.deposits and c.detaches == 0
+        x, y = k.download()
+        assert oracle.closure_holds(L, x, y)
+        assert k.width_sums() == oracle.kpz_width_sums(L, x, y)
+        # mean height identity: sum over successes (p=1): anchored mean moves by 2 per deposit
+        # relative to the flat sum -L^2 only through the anchor; check via heights directly
+        h = k.reconstruct_heights().astype(np.int64)
+        assert (h.sum(), (h * h).sum()) == k.width_sums()
+
+
+def test_large_lattice_matches_oracle_one_sweep(lfg, oracle):
+    L = 2048
+    for (p, q) in ((1.0, 0.0), (0.95, 0.05)):
+        x, y = oracle.kpz_flat(L)
+        c_ref = oracle.kpz_sweep_dtr(L, x, y, p, q, 31, 0, 1, 1024, 128)
+        with lfg.KpzLattice(L, p, q, 31) as k:
+            k.make_flat_slopes()
+            c = k.sweep(1)
+            gx, gy = k.download()
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist()
+        assert (gx == x).all() and (gy == y).all()
