@@ -11,7 +11,7 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_lib", "liblfg.so")
+LIB_PATH = os.environ.get("LFG_LIB") or os.path.join(PKG, "_lib", "liblfg.so")
 HEADERS = [os.path.join(os.path.dirname(PKG), "include", h) for h in ("lfg.h", "lfg_kmc.h")]
 
 LFG_OK, LFG_EINVAL, LFG_ECLOSURE, LFG_EDOMAIN, LFG_ECUDA, LFG_ENCCL, LFG_ENOMEM = range(7)

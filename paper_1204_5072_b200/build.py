@@ -52,14 +52,16 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    target = out or LIB
+    if not force and out is None and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    tmp = target + ".tmp"
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-o", tmp,
+           *sources()]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(LIBDIR, "build.log")
+    log = target + ".build.log"
     with open(log, "w") as fh:
         fh.write(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)
     if res.returncode != 0:
@@ -67,9 +69,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="--verbose" in sys.argv))
+    args = sys.argv[1:]
+    out = None
+    defs = []
+    for a in args:
+        if a.startswith("--out="):
+            out = a.split("=", 1)[1]
+        elif a.startswith("-D"):
+            defs.append(a[2:])
+    print(build(force="--force" in args, verbose="--verbose" in args, out=out, defines=defs))

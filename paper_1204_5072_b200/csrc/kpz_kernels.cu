@@ -50,68 +50,107 @@ __device__ __forceinline__ void count_if_nonzero(uint32_t& n, uint32_t v) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(n) : "r"(v));
 }
 
-// Inner single-hit rounds of one block activation.  Per round every tile's
-// active domain makes one attempt; the inner set (hx, hy) is block-uniform
-// and lives in uniform registers, the anchor is per lane:
-//   xd = bits 4(k&7) of A[k>>3], yd = bits 3k of A.z (k<10) / 3(k-10) of A.w.
-// Lane byte address of the anchor word = lane_base | (yd << 8): tile rows are
-// 256-byte lines and lane_base has bits 8..10 clear, so one LOP3 forms it.
+template <int LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+}
+
+// One single-hit attempt of the tile's active domain (HX, HY) in round k.
+//   own/up/dn : spin words of anchor row j, j+1, j-1 (same tile column)
+//   nb        : the neighbouring tile word on the crossing side (left for the
+//               hx=0 half, right for hx=1); funnel shifts bring f(i-1) and
+//               f(i+1) into bit position i for all 32 columns at once.
+//   deposit   : f_R==f_S & f_U==f_S & f_L!=f_S & f_D!=f_S  (LUT 0x81 & 0x18)
+// The anchor bit selects the one column that is actually attempted.
+template <int HX, int HY, bool GENERAL>
+__device__ __forceinline__ void kpz_attempt_word(char* smb, uint32_t lane_base, uint32_t xd, uint32_t yd,
+                                                 uint32_t u, uint64_t thrP, uint64_t thrQ, uint32_t& fdep,
+                                                 uint32_t& fdet) {
+    char* pw = smb + (yd * 256u + lane_base) + (HY << 11);
+    const uint32_t own = *reinterpret_cast<const uint32_t*>(pw);
+    const uint32_t up = *reinterpret_cast<const uint32_t*>(pw + 256);
+    const uint32_t dn = *reinterpret_cast<const uint32_t*>(pw - 256);
+    const uint32_t nb = *reinterpret_cast<const uint32_t*>(pw + (HX ? 4 : -4));
+    const uint32_t Rw = __funnelshift_r(own, nb, 1);  // bit i = f(i+1)
+    const uint32_t Lw = __funnelshift_l(nb, own, 1);  // bit i = f(i-1)
+    const uint32_t bit = (HX ? 0x10000u : 1u) << xd;
+    if (!GENERAL) {
+        fdep = lop3<0x80>(lop3<0x81>(own, Rw, up),    // f_R == f_S && f_U == f_S
+                          lop3<0x18>(own, Lw, dn),    // f_L != f_S && f_D != f_S
+                          bit);
+        *reinterpret_cast<uint32_t*>(pw) = own ^ fdep;
+    } else {
+        const uint32_t okP = uint64_t(u) < thrP ? bit : 0u;
+        const uint32_t okQ = uint64_t(u) < thrQ ? bit : 0u;
+        fdep = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), okP);
+        fdet = lop3<0x80>(lop3<0x18>(own, Rw, up), lop3<0x81>(own, Lw, dn), okQ);
+        *reinterpret_cast<uint32_t*>(pw) = own ^ (fdep | fdet);
+    }
+}
+
+// Inner single-hit rounds of one block activation.  The inner set of each
+// round is block-uniform (drawn from Philox(seed, sweep, block) into uniform
+// registers once per 64 rounds), so a uniform branch selects one of four
+// specialised bodies whose row offset, neighbour direction and bit offset are
+// immediates.  Anchor of round k of a 16-round batch (A = Philox(tile,
+// batch)), fields consumed from the top of each word with IMAD.HI/IMAD.SHL
+// (FMA pipe -- the ALU pipe is this kernel's binding unit):
+//   xd = bits [28-4(k&7), +4) of A[k>>3];  yd = bits [29-3k, +3) of A.z (k<10),
+//   [29-3(k-10), +3) of A.w.
 template <bool GENERAL, bool FULL>
 __device__ __forceinline__ void kpz_block_rounds(char* smb, uint32_t lane_base, bool active, uint64_t seed,
                                                  uint64_t sweep, uint32_t block_id, uint32_t tile_id,
                                                  uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
-    U4 V = {0, 0, 0, 0};
 #pragma unroll 1
-    for (int m = 0; m < kRounds / 16; ++m) {
-        if ((m & 3) == 0) V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m >> 2));
-        const uint32_t setw = sel4(V, m & 3);
-        const U4 A = draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(m));
-        U4 Uw = {0, 0, 0, 0};
+    for (int m4 = 0; m4 < kRounds / 64; ++m4) {
+        const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t setw = sel4(V, j);
+            const int m = 4 * m4 + j;
+            const U4 A = draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(m));
+            uint32_t xw = A.x, yw = A.z;
+            U4 Uw = {0, 0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            if (GENERAL && (k & 3) == 0) Uw = draw(seed, sweep, TAG_ACCEPT, tile_id, uint32_t(4 * m + (k >> 2)));
-            const uint32_t s2 = (setw >> (2 * k)) & 3u;
-            const uint32_t hx = s2 & 1u;
-            const int hyoff = int(s2 >> 1) << 11;  // +8 rows
-            const int nbo = hx ? 4 : -4;
-            const uint32_t xw = k < 8 ? A.x : A.y;
-            const uint32_t c = ((xw >> (4 * (k & 7))) & 15u) | (hx << 4);
-            const uint32_t yw = k < 10 ? A.z : A.w;
-            const int ysh = 3 * (k < 10 ? k : k - 10);
-            const uint32_t ybits = ysh <= 8 ? (yw << (8 - ysh)) : (yw >> (ysh - 8));
-            const uint32_t addr = lane_base | (ybits & 0x700u);
-            if (FULL || active) {
-                char* pw = smb + hyoff + addr;
-                const uint32_t own = *reinterpret_cast<const uint32_t*>(pw);
-                const uint32_t up = *reinterpret_cast<const uint32_t*>(pw + 256);
-                const uint32_t dn = *reinterpret_cast<const uint32_t*>(pw - 256);
-                const uint32_t nb = *reinterpret_cast<const uint32_t*>(pw + nbo);
-                const uint32_t eR = own ^ __funnelshift_r(own, nb, 1);
-                const uint32_t eL = own ^ __funnelshift_l(nb, own, 1);
-                const uint32_t bit = 1u << c;
-                uint32_t flip;
-                if (!GENERAL) {
-                    flip = ~(eR | (own ^ up)) & eL & (own ^ dn) & bit;
-                    count_if_nonzero(ndep, flip);
-                } else {
-                    const uint32_t u = sel4(Uw, k & 3);
-                    const uint32_t okP = uint64_t(u) < thrP ? bit : 0u;
-                    const uint32_t okQ = uint64_t(u) < thrQ ? bit : 0u;
-                    const uint32_t dep = ~(eR | (own ^ up)) & eL & (own ^ dn) & okP;
-                    const uint32_t det = eR & (own ^ up) & ~(eL | (own ^ dn)) & okQ;
-                    flip = dep | det;
-                    count_if_nonzero(ndep, dep);
-                    count_if_nonzero(ndet, det);
+            for (int k = 0; k < 16; ++k) {
+                if (GENERAL && (k & 3) == 0)
+                    Uw = draw(seed, sweep, TAG_ACCEPT, tile_id, uint32_t(4 * m + (k >> 2)));
+                if (k == 8) xw = A.y;
+                if (k == 10) yw = A.w;
+                const uint32_t xd = __umulhi(xw, 16u);  // top 4 bits
+                const uint32_t yd = __umulhi(yw, 8u);   // top 3 bits
+                xw *= 16u;
+                yw *= 8u;
+                const uint32_t u = GENERAL ? sel4(Uw, k & 3) : 0u;
+                uint32_t fdep = 0, fdet = 0;
+                if (FULL || active) {
+                    if (setw & (2u << (2 * k))) {
+                        if (setw & (1u << (2 * k)))
+                            kpz_attempt_word<1, 1, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                        else
+                            kpz_attempt_word<0, 1, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                    } else {
+                        if (setw & (1u << (2 * k)))
+                            kpz_attempt_word<1, 0, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                        else
+                            kpz_attempt_word<0, 0, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                    }
                 }
-                *reinterpret_cast<uint32_t*>(pw) = own ^ flip;
+                count_if_nonzero(ndep, fdep);
+                if (GENERAL) count_if_nonzero(ndet, fdet);
+                __syncthreads();
             }
-            __syncthreads();
         }
     }
 }
 
 template <bool GENERAL, bool FULL>
-__global__ void __launch_bounds__(256, 6) kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
+#ifndef LFG_KPZ_MIN_BLOCKS
+#define LFG_KPZ_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(256, LFG_KPZ_MIN_BLOCKS) kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int L = a.L, Lm = L - 1, wpr = L >> 5, wmask = wpr - 1;
     const int Wt = a.bx >> 5, Ty = a.by >> 4;
@@ -131,12 +170,13 @@ __global__ void __launch_bounds__(256, 6) kpz_dtr_phase_kernel(const __grid_cons
     const int b = X0 & 31;
     const int w0 = ((X0 - 32 + L) & Lm) >> 5;
 
-    // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin away.
+    // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin
+    // away (slot s of row R <- global bits [X0 + 32 s, X0 + 32 s + 32)).
     for (int R = warp - 1; R <= a.by; R += nwarps) {
-        const uint32_t* __restrict__ row = f + size_t((Y0 + R) & Lm) * wpr;
+        const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
         for (int k = lane; k < Wt + 2; k += 32) {
-            const uint32_t lo = row[(w0 + k) & wmask];
-            const uint32_t hi = row[(w0 + k + 1) & wmask];
+            const uint32_t lo = __ldg(row + ((w0 + k) & wmask));
+            const uint32_t hi = __ldg(row + ((w0 + k + 1) & wmask));
             sm[sm_slot(R, k - 1)] = __funnelshift_r(lo, hi, b);
         }
     }
@@ -151,7 +191,7 @@ __global__ void __launch_bounds__(256, 6) kpz_dtr_phase_kernel(const __grid_cons
 
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     for (int R = warp; R < a.by; R += nwarps) {
-        uint32_t* __restrict__ row = f + size_t((Y0 + R) & Lm) * wpr;
+        uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
         for (int k = lane; k <= Wt; k += 32) {
             if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
             row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);

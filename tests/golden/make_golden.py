@@ -44,7 +44,7 @@ KPZ_DTR_CASES = [
     (256, 64, 128, 0.95, 0.05, 12, 5, 2),
     (512, 256, 128, 1.0, 0.0, 1, 0, 2),
     (1024, 512, 128, 1.0, 0.0, 1, 0, 1),
-    (1024, 512, 256, 0.95, 0.05, 5, 100, 1),
+    (1024, 512, 64, 0.95, 0.05, 5, 100, 1),
     (2048, 1024, 128, 1.0, 0.0, 1, 0, 1),
     (2048, 1024, 128, 0.25, 0.75, 9, 0, 1),
 ]
