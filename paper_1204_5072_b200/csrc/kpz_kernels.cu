@@ -27,9 +27,11 @@ namespace lfg {
 
 // ============================================================ DTr phase kernel
 // One CTA = one active device block (bx x by sites) of one replica.
-// Threads: one warp per tile row (by/16 warps), lane = tile column (bx/32
-// lanes active).  Shared-memory layout (32-bit words, 256-byte lines):
-//   line 0, words 0..31     : the block's 512 inner-set draws (2 bits each)
+// Threads: 32 lanes x (by/16/NT) warps; lane = tile column (bx/32 lanes
+// active), warp w owns tile rows w + n*(by/16/NT), n < NT (NT tiles per lane,
+// so the per-round dispatch, barrier and loop are shared by NT independent
+// attempts).  Shared-memory layout (32-bit words, 256-byte lines):
+//   line 0, words 0..31     : spare (set draws live in uniform registers)
 //   line R+8, word s        : staged spins of block row R (R = -1 .. by),
 //                             s = 0..Wt-1 tile words, s = Wt the right halo
 //                             word (H_R); the left halo word (H_L) of row R
@@ -37,7 +39,7 @@ namespace lfg {
 // With a 64-word line stride every tile column owns one bank for all its
 // rows, so the per-round gathers (own/up/down words) are conflict-free, and
 // the neighbour-word gather is a lane rotation that lands the block's edge
-// lanes exactly on H_L / H_R (bank 31 / bank Wt).
+// lanes exactly on H_L (bank 31) / H_R (bank Wt).
 __device__ __forceinline__ int sm_slot(int R, int s) {
     return s < 0 ? (R + 7) * 64 + 63 : (R + 8) * 64 + s;
 }
@@ -57,18 +59,20 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
-// One single-hit attempt of the tile's active domain (HX, HY) in round k.
-//   own/up/dn : spin words of anchor row j, j+1, j-1 (same tile column)
+// One single-hit attempt of a tile's active domain (HX, HY).
+//   addr      : byte offset of the anchor row's tile word (row j) in the
+//               active half-tile row block (HY adds 8 rows = 2048 bytes)
+//   own/up/dn : spin words of rows j, j+1, j-1 (same tile column, same bank)
 //   nb        : the neighbouring tile word on the crossing side (left for the
 //               hx=0 half, right for hx=1); funnel shifts bring f(i-1) and
 //               f(i+1) into bit position i for all 32 columns at once.
 //   deposit   : f_R==f_S & f_U==f_S & f_L!=f_S & f_D!=f_S  (LUT 0x81 & 0x18)
-// The anchor bit selects the one column that is actually attempted.
+//   detach    : f_R!=f_S & f_U!=f_S & f_L==f_S & f_D==f_S  (LUT 0x18 & 0x81)
+// The one-hot anchor bit selects the column actually attempted.
 template <int HX, int HY, bool GENERAL>
-__device__ __forceinline__ void kpz_attempt_word(char* smb, uint32_t lane_base, uint32_t xd, uint32_t yd,
-                                                 uint32_t u, uint64_t thrP, uint64_t thrQ, uint32_t& fdep,
-                                                 uint32_t& fdet) {
-    char* pw = smb + (yd * 256u + lane_base) + (HY << 11);
+__device__ __forceinline__ void kpz_attempt_word(char* smb, uint32_t addr, uint32_t xd, uint32_t u, uint64_t thrP,
+                                                 uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
+    char* pw = smb + addr + (HY << 11);
     const uint32_t own = *reinterpret_cast<const uint32_t*>(pw);
     const uint32_t up = *reinterpret_cast<const uint32_t*>(pw + 256);
     const uint32_t dn = *reinterpret_cast<const uint32_t*>(pw - 256);
@@ -77,32 +81,43 @@ __device__ __forceinline__ void kpz_attempt_word(char* smb, uint32_t lane_base, 
     const uint32_t Lw = __funnelshift_l(nb, own, 1);  // bit i = f(i-1)
     const uint32_t bit = (HX ? 0x10000u : 1u) << xd;
     if (!GENERAL) {
-        fdep = lop3<0x80>(lop3<0x81>(own, Rw, up),    // f_R == f_S && f_U == f_S
-                          lop3<0x18>(own, Lw, dn),    // f_L != f_S && f_D != f_S
-                          bit);
-        *reinterpret_cast<uint32_t*>(pw) = own ^ fdep;
+        const uint32_t flip = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), bit);
+        *reinterpret_cast<uint32_t*>(pw) = own ^ flip;
+        count_if_nonzero(ndep, flip);
     } else {
         const uint32_t okP = uint64_t(u) < thrP ? bit : 0u;
         const uint32_t okQ = uint64_t(u) < thrQ ? bit : 0u;
-        fdep = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), okP);
-        fdet = lop3<0x80>(lop3<0x18>(own, Rw, up), lop3<0x81>(own, Lw, dn), okQ);
-        *reinterpret_cast<uint32_t*>(pw) = own ^ (fdep | fdet);
+        const uint32_t dep = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), okP);
+        const uint32_t det = lop3<0x80>(lop3<0x18>(own, Rw, up), lop3<0x81>(own, Lw, dn), okQ);
+        *reinterpret_cast<uint32_t*>(pw) = own ^ (dep | det);
+        count_if_nonzero(ndep, dep);
+        count_if_nonzero(ndet, det);
     }
 }
 
+template <int HX, int HY, bool GENERAL, int NT>
+__device__ __forceinline__ void kpz_attempt_tiles(char* smb, const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
+                                                  const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
+                                                  uint32_t& ndep, uint32_t& ndet) {
+#pragma unroll
+    for (int n = 0; n < NT; ++n) kpz_attempt_word<HX, HY, GENERAL>(smb, addr[n], xd[n], u[n], thrP, thrQ, ndep, ndet);
+}
+
 // Inner single-hit rounds of one block activation.  The inner set of each
-// round is block-uniform (drawn from Philox(seed, sweep, block) into uniform
-// registers once per 64 rounds), so a uniform branch selects one of four
+// round is block-uniform (Philox(seed, sweep, block) in uniform registers,
+// redrawn every 64 rounds), so a uniform branch selects one of four
 // specialised bodies whose row offset, neighbour direction and bit offset are
 // immediates.  Anchor of round k of a 16-round batch (A = Philox(tile,
-// batch)), fields consumed from the top of each word with IMAD.HI/IMAD.SHL
-// (FMA pipe -- the ALU pipe is this kernel's binding unit):
+// batch)), fields taken from the top of each word:
 //   xd = bits [28-4(k&7), +4) of A[k>>3];  yd = bits [29-3k, +3) of A.z (k<10),
 //   [29-3(k-10), +3) of A.w.
-template <bool GENERAL, bool FULL>
-__device__ __forceinline__ void kpz_block_rounds(char* smb, uint32_t lane_base, bool active, uint64_t seed,
-                                                 uint64_t sweep, uint32_t block_id, uint32_t tile_id,
-                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
+// lane_base has bits 8..10 clear, so the anchor row offset yd*256 is merged
+// with a single LOP3.
+template <bool GENERAL, bool FULL, int NT>
+__device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lane_base)[NT], bool active,
+                                                 uint64_t seed, uint64_t sweep, uint32_t block_id,
+                                                 const uint32_t (&tile_id)[NT], uint64_t thrP, uint64_t thrQ,
+                                                 uint32_t& ndep, uint32_t& ndet) {
 #pragma unroll 1
     for (int m4 = 0; m4 < kRounds / 64; ++m4) {
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
@@ -110,47 +125,62 @@ __device__ __forceinline__ void kpz_block_rounds(char* smb, uint32_t lane_base, 
         for (int j = 0; j < 4; ++j) {
             const uint32_t setw = sel4(V, j);
             const int m = 4 * m4 + j;
-            const U4 A = draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(m));
-            uint32_t xw = A.x, yw = A.z;
-            U4 Uw = {0, 0, 0, 0};
+            U4 A[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) A[n] = draw(seed, sweep, TAG_ANCHOR, tile_id[n], uint32_t(m));
+            U4 Uw[NT];
+            uint32_t xw[NT];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) xw[n] = A[n].x;
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
-                if (GENERAL && (k & 3) == 0)
-                    Uw = draw(seed, sweep, TAG_ACCEPT, tile_id, uint32_t(4 * m + (k >> 2)));
-                if (k == 8) xw = A.y;
-                if (k == 10) yw = A.w;
-                const uint32_t xd = __umulhi(xw, 16u);  // top 4 bits
-                const uint32_t yd = __umulhi(yw, 8u);   // top 3 bits
-                xw *= 16u;
-                yw *= 8u;
-                const uint32_t u = GENERAL ? sel4(Uw, k & 3) : 0u;
-                uint32_t fdep = 0, fdet = 0;
+                uint32_t addr[NT], xd[NT], u[NT];
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    if (GENERAL && (k & 3) == 0)
+                        Uw[n] = draw(seed, sweep, TAG_ACCEPT, tile_id[n], uint32_t(4 * m + (k >> 2)));
+                    if (k == 8) xw[n] = A[n].y;
+                    // FMA-pipe field extraction (the ALU pipe binds this kernel):
+                    // xd = top 4 bits, then advance; the row field is moved to
+                    // bits 8..10 by a power-of-two multiply (hi or lo half) and
+                    // the LOP3 mask drops the neighbouring random bits.
+                    xd[n] = __umulhi(xw[n], 16u);
+                    xw[n] *= 16u;
+                    const uint32_t yw = k < 10 ? A[n].z : A[n].w;
+                    const int ysh = 21 - 3 * (k < 10 ? k : k - 10);  // field -> bits 8..10
+                    const uint32_t yb = ysh > 0 ? __umulhi(yw, 1u << (32 - ysh)) : yw * (1u << -ysh);
+                    addr[n] = lop3<0xF8>(lane_base[n], yb, 0x700u);  // lane_base | (yb & 0x700)
+                    u[n] = GENERAL ? sel4(Uw[n], k & 3) : 0u;
+                }
                 if (FULL || active) {
                     if (setw & (2u << (2 * k))) {
                         if (setw & (1u << (2 * k)))
-                            kpz_attempt_word<1, 1, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                            kpz_attempt_tiles<1, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
                         else
-                            kpz_attempt_word<0, 1, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                            kpz_attempt_tiles<0, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
                     } else {
                         if (setw & (1u << (2 * k)))
-                            kpz_attempt_word<1, 0, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                            kpz_attempt_tiles<1, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
                         else
-                            kpz_attempt_word<0, 0, GENERAL>(smb, lane_base, xd, yd, u, thrP, thrQ, fdep, fdet);
+                            kpz_attempt_tiles<0, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
                     }
                 }
-                count_if_nonzero(ndep, fdep);
-                if (GENERAL) count_if_nonzero(ndet, fdet);
                 __syncthreads();
             }
         }
     }
 }
 
-template <bool GENERAL, bool FULL>
-#ifndef LFG_KPZ_MIN_BLOCKS
-#define LFG_KPZ_MIN_BLOCKS 5
+#ifndef LFG_KPZ_NT
+#define LFG_KPZ_NT 2  // tiles per lane for block_y >= 32
 #endif
-__global__ void __launch_bounds__(256, LFG_KPZ_MIN_BLOCKS) kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
+#ifndef LFG_KPZ_MIN_BLOCKS
+#define LFG_KPZ_MIN_BLOCKS 6
+#endif
+
+template <bool GENERAL, bool FULL, int kNT>
+__global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
+    kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int L = a.L, Lm = L - 1, wpr = L >> 5, wmask = wpr - 1;
     const int Wt = a.bx >> 5, Ty = a.by >> 4;
@@ -172,29 +202,59 @@ __global__ void __launch_bounds__(256, LFG_KPZ_MIN_BLOCKS) kpz_dtr_phase_kernel(
 
     // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin
     // away (slot s of row R <- global bits [X0 + 32 s, X0 + 32 s + 32)).
-    for (int R = warp - 1; R <= a.by; R += nwarps) {
-        const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
-        for (int k = lane; k < Wt + 2; k += 32) {
-            const uint32_t lo = __ldg(row + ((w0 + k) & wmask));
-            const uint32_t hi = __ldg(row + ((w0 + k + 1) & wmask));
-            sm[sm_slot(R, k - 1)] = __funnelshift_r(lo, hi, b);
+    if (FULL) {  // Wt == 32: lane k loads word w0+k, neighbours come by shuffle
+        for (int R = warp - 1; R <= a.by; R += nwarps) {
+            const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            const uint32_t v0 = __ldg(row + ((w0 + lane) & wmask));
+            const uint32_t v1 = lane < 3 ? __ldg(row + ((w0 + 32 + lane) & wmask)) : 0u;
+            const uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, v0, 1);
+            const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, v1, 0);
+            const uint32_t n1 = __shfl_down_sync(0xFFFFFFFFu, v1, 1);
+            sm[sm_slot(R, lane - 1)] = __funnelshift_r(v0, lane == 31 ? t0 : n0, b);
+            if (lane < 2) sm[(R + 8) * 64 + 31 + lane] = __funnelshift_r(v1, n1, b);
+        }
+    } else {
+        for (int R = warp - 1; R <= a.by; R += nwarps) {
+            const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            for (int k = lane; k < Wt + 2; k += 32) {
+                const uint32_t lo = __ldg(row + ((w0 + k) & wmask));
+                const uint32_t hi = __ldg(row + ((w0 + k + 1) & wmask));
+                sm[sm_slot(R, k - 1)] = __funnelshift_r(lo, hi, b);
+            }
         }
     }
     __syncthreads();
 
-    const int tx = lane, ty = warp;
-    const uint32_t tile_id = uint32_t(byi * Ty + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
-    const uint32_t lane_base = uint32_t((16 * ty + 8) * 256 + 4 * tx);
+    const int tx = lane;
+    const int rows_per_n = Ty / kNT;
+    uint32_t lane_base[kNT], tile_id[kNT];
+#pragma unroll
+    for (int n = 0; n < kNT; ++n) {
+        const int ty = warp + n * rows_per_n;
+        tile_id[n] = uint32_t(byi * Ty + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
+        lane_base[n] = uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
+    }
     uint32_t ndep = 0, ndet = 0;
-    kpz_block_rounds<GENERAL, FULL>(reinterpret_cast<char*>(sm), lane_base, tx < Wt, seed, sweep, block_id,
-                                    tile_id, a.thrP, a.thrQ, ndep, ndet);
+    kpz_block_rounds<GENERAL, FULL, kNT>(reinterpret_cast<char*>(sm), lane_base, tx < Wt, seed, sweep, block_id,
+                                         tile_id, a.thrP, a.thrQ, ndep, ndet);
 
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
-    for (int R = warp; R < a.by; R += nwarps) {
-        uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
-        for (int k = lane; k <= Wt; k += 32) {
-            if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
-            row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
+    if (FULL) {
+        for (int R = warp; R < a.by; R += nwarps) {
+            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            const uint32_t cur = sm[(R + 8) * 64 + lane];             // slot lane
+            const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, cur, 1);  // slot lane-1
+            const uint32_t lo = lane == 0 ? sm[sm_slot(R, -1)] : prv;
+            row[(w0 + 1 + lane) & wmask] = __funnelshift_l(lo, cur, b);
+            if (lane == 31 && b != 0) row[(w0 + 33) & wmask] = __funnelshift_l(cur, sm[(R + 8) * 64 + 32], b);
+        }
+    } else {
+        for (int R = warp; R < a.by; R += nwarps) {
+            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            for (int k = lane; k <= Wt; k += 32) {
+                if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
+                row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
+            }
         }
     }
     // Counters: deposits, detaches per replica.
@@ -208,40 +268,53 @@ __global__ void __launch_bounds__(256, LFG_KPZ_MIN_BLOCKS) kpz_dtr_phase_kernel(
 
 size_t kpz_phase_smem_bytes(int by) { return size_t(by + 9) * 256; }
 
+template <int NT>
+static void launch_nt(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
+    const dim3 block(unsigned(32 * (b.by / 16 / NT)));
+    const bool full = b.bx == 1024;
+    if (b.general) {
+        if (full) kpz_dtr_phase_kernel<true, true, NT><<<grid, block, smem, st>>>(b);
+        else kpz_dtr_phase_kernel<true, false, NT><<<grid, block, smem, st>>>(b);
+    } else {
+        if (full) kpz_dtr_phase_kernel<false, true, NT><<<grid, block, smem, st>>>(b);
+        else kpz_dtr_phase_kernel<false, false, NT><<<grid, block, smem, st>>>(b);
+    }
+}
+
 cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st) {
-    const dim3 block(unsigned(32 * (a.by / 16)));
     const size_t smem = kpz_phase_smem_bytes(a.by);
-    const bool full = a.bx == 1024;
     for (int r0 = 0; r0 < replicas; r0 += kMaxRepPerLaunch) {
         KpzPhaseArgs b = a;
         b.rep0 = r0;
         const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
         for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
         const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.L / a.by / 2), unsigned(nr));
-        if (a.general) {
-            if (full) kpz_dtr_phase_kernel<true, true><<<grid, block, smem, st>>>(b);
-            else kpz_dtr_phase_kernel<true, false><<<grid, block, smem, st>>>(b);
-        } else {
-            if (full) kpz_dtr_phase_kernel<false, true><<<grid, block, smem, st>>>(b);
-            else kpz_dtr_phase_kernel<false, false><<<grid, block, smem, st>>>(b);
-        }
+        if (a.by >= 16 * LFG_KPZ_NT) launch_nt<LFG_KPZ_NT>(b, grid, smem, st);
+        else launch_nt<1>(b, grid, smem, st);
     }
     return cudaGetLastError();
 }
 
-cudaError_t kpz_phase_kernel_attrs() {
-    const int smem = int(kpz_phase_smem_bytes(128));
-    cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true>,
+template <int NT>
+static cudaError_t attrs_nt(int smem) {
+    cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem);
+    return e;
+}
+
+cudaError_t kpz_phase_kernel_attrs() {
+    const int smem = int(kpz_phase_smem_bytes(128));
+    cudaError_t e = attrs_nt<1>(smem);
+    if (e == cudaSuccess && LFG_KPZ_NT != 1) e = attrs_nt<LFG_KPZ_NT>(smem);
     return e;
 }
 
