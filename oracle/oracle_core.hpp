@@ -141,12 +141,12 @@ void kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& a
                             uint32_t* a4 = anc + size_t(ty * twx + tx) * 4;
                             if ((r & 15) == 0) draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(r >> 4), a4);
                             // Anchor of round r (k = r & 15 within its 16-round batch), fields
-                            // consumed from the TOP of each Philox word:
-                            //   xd = bits [28-4(k&7), +4) of word k>>3 (words 0,1)
-                            //   yd = bits [29-3k, +3) of word 2 (k < 10), [29-3(k-10), +3) of word 3
-                            const int k = r & 15;
-                            const int32_t xd = int32_t((a4[k >> 3] >> (28 - 4 * (k & 7))) & 15u);
-                            const int32_t yd = int32_t(k < 10 ? (a4[2] >> (29 - 3 * k)) & 7u : (a4[3] >> (29 - 3 * (k - 10))) & 7u);
+                            // consumed from the TOP of each Philox word (h = k >> 3, k' = k & 7):
+                            //   xd = bits [28-4k', +4) of word h      (words 0, 1)
+                            //   yd = bits [29-3k', +3) of word 2 + h  (words 2, 3; low 8 bits unused)
+                            const int k = r & 15, h = k >> 3, kk = k & 7;
+                            const int32_t xd = int32_t((a4[h] >> (28 - 4 * kk)) & 15u);
+                            const int32_t yd = int32_t((a4[2 + h] >> (29 - 3 * kk)) & 7u);
                             const int32_t i = (d.ox + kTileW * gx + kDomW * hx + xd) & mask;
                             const int32_t j = (d.oy + kTileH * gy + kDomH * hy + yd) & mask;
                             attempt(i, j, tile_id, r);

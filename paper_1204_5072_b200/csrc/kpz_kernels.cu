@@ -59,60 +59,64 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
-// One single-hit attempt of a tile's active domain (HX, HY).
-//   addr      : byte offset of the anchor row's tile word (row j) in the
-//               active half-tile row block (HY adds 8 rows = 2048 bytes)
+// One single-hit round of the NT tiles a lane owns, active domain (HX, HY).
+//   addr      : byte offset of each anchor row's tile word (row j); HY adds 8
+//               rows (2048 bytes)
 //   own/up/dn : spin words of rows j, j+1, j-1 (same tile column, same bank)
 //   nb        : the neighbouring tile word on the crossing side (left for the
 //               hx=0 half, right for hx=1); funnel shifts bring f(i-1) and
 //               f(i+1) into bit position i for all 32 columns at once.
 //   deposit   : f_R==f_S & f_U==f_S & f_L!=f_S & f_D!=f_S  (LUT 0x81 & 0x18)
 //   detach    : f_R!=f_S & f_U!=f_S & f_L==f_S & f_D==f_S  (LUT 0x18 & 0x81)
-// The one-hot anchor bit selects the column actually attempted.
-template <int HX, int HY, bool GENERAL>
-__device__ __forceinline__ void kpz_attempt_word(char* smb, uint32_t addr, uint32_t xd, uint32_t u, uint64_t thrP,
-                                                 uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
-    char* pw = smb + addr + (HY << 11);
-    const uint32_t own = *reinterpret_cast<const uint32_t*>(pw);
-    const uint32_t up = *reinterpret_cast<const uint32_t*>(pw + 256);
-    const uint32_t dn = *reinterpret_cast<const uint32_t*>(pw - 256);
-    const uint32_t nb = *reinterpret_cast<const uint32_t*>(pw + (HX ? 4 : -4));
-    const uint32_t Rw = __funnelshift_r(own, nb, 1);  // bit i = f(i+1)
-    const uint32_t Lw = __funnelshift_l(nb, own, 1);  // bit i = f(i-1)
-    const uint32_t bit = (HX ? 0x10000u : 1u) << xd;
-    if (!GENERAL) {
-        const uint32_t flip = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), bit);
-        *reinterpret_cast<uint32_t*>(pw) = own ^ flip;
-        count_if_nonzero(ndep, flip);
-    } else {
-        const uint32_t okP = uint64_t(u) < thrP ? bit : 0u;
-        const uint32_t okQ = uint64_t(u) < thrQ ? bit : 0u;
-        const uint32_t dep = lop3<0x80>(lop3<0x81>(own, Rw, up), lop3<0x18>(own, Lw, dn), okP);
-        const uint32_t det = lop3<0x80>(lop3<0x18>(own, Rw, up), lop3<0x81>(own, Lw, dn), okQ);
-        *reinterpret_cast<uint32_t*>(pw) = own ^ (dep | det);
-        count_if_nonzero(ndep, dep);
-        count_if_nonzero(ndet, det);
-    }
-}
-
+// The one-hot anchor bit selects the column actually attempted.  All loads
+// of all tiles are issued before any store (the tiles are disjoint rows), so
+// the NT dependency chains overlap.
 template <int HX, int HY, bool GENERAL, int NT>
 __device__ __forceinline__ void kpz_attempt_tiles(char* smb, const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
                                                   uint32_t& ndep, uint32_t& ndet) {
+    uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
 #pragma unroll
-    for (int n = 0; n < NT; ++n) kpz_attempt_word<HX, HY, GENERAL>(smb, addr[n], xd[n], u[n], thrP, thrQ, ndep, ndet);
+    for (int n = 0; n < NT; ++n) {
+        const char* pw = smb + addr[n] + (HY << 11);
+        own[n] = *reinterpret_cast<const uint32_t*>(pw);
+        up[n] = *reinterpret_cast<const uint32_t*>(pw + 256);
+        dn[n] = *reinterpret_cast<const uint32_t*>(pw - 256);
+        nb[n] = *reinterpret_cast<const uint32_t*>(pw + (HX ? 4 : -4));
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const uint32_t Rw = __funnelshift_r(own[n], nb[n], 1);  // bit i = f(i+1)
+        const uint32_t Lw = __funnelshift_l(nb[n], own[n], 1);  // bit i = f(i-1)
+        const uint32_t bit = (HX ? 0x10000u : 1u) << xd[n];
+        if (!GENERAL) {
+            const uint32_t flip = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), bit);
+            res[n] = own[n] ^ flip;
+            count_if_nonzero(ndep, flip);
+        } else {
+            const uint32_t okP = uint64_t(u[n]) < thrP ? bit : 0u;
+            const uint32_t okQ = uint64_t(u[n]) < thrQ ? bit : 0u;
+            const uint32_t dep = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), okP);
+            const uint32_t det = lop3<0x80>(lop3<0x18>(own[n], Rw, up[n]), lop3<0x81>(own[n], Lw, dn[n]), okQ);
+            res[n] = own[n] ^ (dep | det);
+            count_if_nonzero(ndep, dep);
+            count_if_nonzero(ndet, det);
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) *reinterpret_cast<uint32_t*>(smb + addr[n] + (HY << 11)) = res[n];
 }
 
 // Inner single-hit rounds of one block activation.  The inner set of each
 // round is block-uniform (Philox(seed, sweep, block) in uniform registers,
 // redrawn every 64 rounds), so a uniform branch selects one of four
 // specialised bodies whose row offset, neighbour direction and bit offset are
-// immediates.  Anchor of round k of a 16-round batch (A = Philox(tile,
-// batch)), fields taken from the top of each word:
-//   xd = bits [28-4(k&7), +4) of A[k>>3];  yd = bits [29-3k, +3) of A.z (k<10),
-//   [29-3(k-10), +3) of A.w.
-// lane_base has bits 8..10 clear, so the anchor row offset yd*256 is merged
-// with a single LOP3.
+// immediates.  Anchor fields of round k of a 16-round batch (A = Philox(tile,
+// batch), h = k >> 3) are consumed from the top of A[h] (xd, 4 bits) and
+// A[2+h] (yd, 3 bits) with IMAD.HI/IMAD.SHL on the FMA pipe -- the ALU pipe
+// binds this kernel -- which also makes the loop body position-independent,
+// so only 4 rounds are unrolled (small I-cache footprint).  lane_base has
+// bits 8..10 clear, so the row offset yd*256 merges with one LOP3.
 template <bool GENERAL, bool FULL, int NT>
 __device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lane_base)[NT], bool active,
                                                  uint64_t seed, uint64_t sweep, uint32_t block_id,
@@ -123,49 +127,55 @@ __device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lan
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) {
-            const uint32_t setw = sel4(V, j);
+            uint32_t setw = sel4(V, j);
             const int m = 4 * m4 + j;
             U4 A[NT];
 #pragma unroll
             for (int n = 0; n < NT; ++n) A[n] = draw(seed, sweep, TAG_ANCHOR, tile_id[n], uint32_t(m));
-            U4 Uw[NT];
-            uint32_t xw[NT];
-#pragma unroll
-            for (int n = 0; n < NT; ++n) xw[n] = A[n].x;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                uint32_t addr[NT], xd[NT], u[NT];
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                uint32_t xw[NT], yw[NT];
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
-                    if (GENERAL && (k & 3) == 0)
-                        Uw[n] = draw(seed, sweep, TAG_ACCEPT, tile_id[n], uint32_t(4 * m + (k >> 2)));
-                    if (k == 8) xw[n] = A[n].y;
-                    // FMA-pipe field extraction (the ALU pipe binds this kernel):
-                    // xd = top 4 bits, then advance; the row field is moved to
-                    // bits 8..10 by a power-of-two multiply (hi or lo half) and
-                    // the LOP3 mask drops the neighbouring random bits.
-                    xd[n] = __umulhi(xw[n], 16u);
-                    xw[n] *= 16u;
-                    const uint32_t yw = k < 10 ? A[n].z : A[n].w;
-                    const int ysh = 21 - 3 * (k < 10 ? k : k - 10);  // field -> bits 8..10
-                    const uint32_t yb = ysh > 0 ? __umulhi(yw, 1u << (32 - ysh)) : yw * (1u << -ysh);
-                    addr[n] = lop3<0xF8>(lane_base[n], yb, 0x700u);  // lane_base | (yb & 0x700)
-                    u[n] = GENERAL ? sel4(Uw[n], k & 3) : 0u;
+                    xw[n] = h ? A[n].y : A[n].x;
+                    yw[n] = h ? A[n].w : A[n].z;
                 }
-                if (FULL || active) {
-                    if (setw & (2u << (2 * k))) {
-                        if (setw & (1u << (2 * k)))
-                            kpz_attempt_tiles<1, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
-                        else
-                            kpz_attempt_tiles<0, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
-                    } else {
-                        if (setw & (1u << (2 * k)))
-                            kpz_attempt_tiles<1, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
-                        else
-                            kpz_attempt_tiles<0, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+#pragma unroll 1
+                for (int q = 0; q < 2; ++q) {
+                    U4 Uw[NT];
+                    if (GENERAL) {
+#pragma unroll
+                        for (int n = 0; n < NT; ++n)
+                            Uw[n] = draw(seed, sweep, TAG_ACCEPT, tile_id[n], uint32_t(4 * m + 2 * h + q));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint32_t addr[NT], xd[NT], u[NT];
+#pragma unroll
+                        for (int n = 0; n < NT; ++n) {
+                            xd[n] = __umulhi(xw[n], 16u);                         // top 4 bits
+                            addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u), 0x700u);  // | top3 << 8
+                            xw[n] *= 16u;
+                            yw[n] *= 8u;
+                            u[n] = GENERAL ? sel4(Uw[n], k) : 0u;
+                        }
+                        if (FULL || active) {
+                            if (setw & 2u) {
+                                if (setw & 1u)
+                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                else
+                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                            } else {
+                                if (setw & 1u)
+                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                else
+                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                            }
+                        }
+                        setw >>= 2;
+                        __syncthreads();
                     }
                 }
-                __syncthreads();
             }
         }
     }
