@@ -52,6 +52,18 @@ __device__ __forceinline__ void count_if_nonzero(uint32_t& n, uint32_t v) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(n) : "r"(v));
 }
 
+// 32-bit shared-window addressing (avoids re-deriving the generic->shared
+// window base every round).  volatile keeps program order w.r.t. barriers.
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
 template <int LUT>
 __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
@@ -72,17 +84,17 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 // of all tiles are issued before any store (the tiles are disjoint rows), so
 // the NT dependency chains overlap.
 template <int HX, int HY, bool GENERAL, int NT>
-__device__ __forceinline__ void kpz_attempt_tiles(char* smb, const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
+__device__ __forceinline__ void kpz_attempt_tiles(uint32_t smb, const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
                                                   uint32_t& ndep, uint32_t& ndet) {
     uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
-        const char* pw = smb + addr[n] + (HY << 11);
-        own[n] = *reinterpret_cast<const uint32_t*>(pw);
-        up[n] = *reinterpret_cast<const uint32_t*>(pw + 256);
-        dn[n] = *reinterpret_cast<const uint32_t*>(pw - 256);
-        nb[n] = *reinterpret_cast<const uint32_t*>(pw + (HX ? 4 : -4));
+        const uint32_t pw = smb + addr[n] + (HY << 11);
+        own[n] = lds32(pw);
+        nb[n] = lds32(pw + (HX ? 4 : -4));
+        up[n] = lds32(pw + 256);
+        dn[n] = lds32(pw - 256);
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -104,7 +116,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(char* smb, const uint32_t (&ad
         }
     }
 #pragma unroll
-    for (int n = 0; n < NT; ++n) *reinterpret_cast<uint32_t*>(smb + addr[n] + (HY << 11)) = res[n];
+    for (int n = 0; n < NT; ++n) sts32(smb + addr[n] + (HY << 11), res[n]);
 }
 
 // Inner single-hit rounds of one block activation.  The inner set of each
@@ -118,7 +130,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(char* smb, const uint32_t (&ad
 // so only 4 rounds are unrolled (small I-cache footprint).  lane_base has
 // bits 8..10 clear, so the row offset yd*256 merges with one LOP3.
 template <bool GENERAL, bool FULL, int NT>
-__device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lane_base)[NT], bool active,
+__device__ __forceinline__ void kpz_block_rounds(uint32_t smb, const uint32_t (&lane_base)[NT], bool active,
                                                  uint64_t seed, uint64_t sweep, uint32_t block_id,
                                                  const uint32_t (&tile_id)[NT], uint64_t thrP, uint64_t thrQ,
                                                  uint32_t& ndep, uint32_t& ndet) {
@@ -153,10 +165,10 @@ __device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lan
                         uint32_t addr[NT], xd[NT], u[NT];
 #pragma unroll
                         for (int n = 0; n < NT; ++n) {
-                            xd[n] = __umulhi(xw[n], 16u);                         // top 4 bits
-                            addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u), 0x700u);  // | top3 << 8
+                            xd[n] = __umulhi(xw[n], 16u);  // top 4 bits, then advance
                             xw[n] *= 16u;
-                            yw[n] *= 8u;
+                            // row field k of this quarter -> bits 8..10 (bits above masked by the LOP3)
+                            addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u << (3 * k)), 0x700u);
                             u[n] = GENERAL ? sel4(Uw[n], k) : 0u;
                         }
                         if (FULL || active) {
@@ -175,6 +187,8 @@ __device__ __forceinline__ void kpz_block_rounds(char* smb, const uint32_t (&lan
                         setw >>= 2;
                         __syncthreads();
                     }
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) yw[n] <<= 12;  // next 4 row fields
                 }
             }
         }
@@ -213,15 +227,27 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
     // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin
     // away (slot s of row R <- global bits [X0 + 32 s, X0 + 32 s + 32)).
     if (FULL) {  // Wt == 32: lane k loads word w0+k, neighbours come by shuffle
-        for (int R = warp - 1; R <= a.by; R += nwarps) {
-            const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
-            const uint32_t v0 = __ldg(row + ((w0 + lane) & wmask));
-            const uint32_t v1 = lane < 3 ? __ldg(row + ((w0 + 32 + lane) & wmask)) : 0u;
-            const uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, v0, 1);
-            const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, v1, 0);
-            const uint32_t n1 = __shfl_down_sync(0xFFFFFFFFu, v1, 1);
-            sm[sm_slot(R, lane - 1)] = __funnelshift_r(v0, lane == 31 ? t0 : n0, b);
-            if (lane < 2) sm[(R + 8) * 64 + 31 + lane] = __funnelshift_r(v1, n1, b);
+        constexpr int RB = 8;  // rows in flight per warp
+        for (int R0 = warp - 1; R0 <= a.by; R0 += RB * nwarps) {
+            uint32_t v0[RB], v1[RB];
+#pragma unroll
+            for (int t = 0; t < RB; ++t) {
+                const int R = R0 + t * nwarps;
+                const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+                v0[t] = R <= a.by ? __ldg(row + ((w0 + lane) & wmask)) : 0u;
+                v1[t] = (R <= a.by && lane < 3) ? __ldg(row + ((w0 + 32 + lane) & wmask)) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < RB; ++t) {
+                const int R = R0 + t * nwarps;
+                const uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, v0[t], 1);
+                const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, v1[t], 0);
+                const uint32_t n1 = __shfl_down_sync(0xFFFFFFFFu, v1[t], 1);
+                if (R <= a.by) {
+                    sm[sm_slot(R, lane - 1)] = __funnelshift_r(v0[t], lane == 31 ? t0 : n0, b);
+                    if (lane < 2) sm[(R + 8) * 64 + 31 + lane] = __funnelshift_r(v1[t], n1, b);
+                }
+            }
         }
     } else {
         for (int R = warp - 1; R <= a.by; R += nwarps) {
@@ -245,7 +271,7 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
         lane_base[n] = uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
     }
     uint32_t ndep = 0, ndet = 0;
-    kpz_block_rounds<GENERAL, FULL, kNT>(reinterpret_cast<char*>(sm), lane_base, tx < Wt, seed, sweep, block_id,
+    kpz_block_rounds<GENERAL, FULL, kNT>(uint32_t(__cvta_generic_to_shared(sm)), lane_base, tx < Wt, seed, sweep, block_id,
                                          tile_id, a.thrP, a.thrQ, ndep, ndet);
 
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
