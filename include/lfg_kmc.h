@@ -1,0 +1,63 @@
+/* lfg_kmc.h -- C ABI of the KMC path of liblfg.so (see lfg.h for conventions).
+ *
+ * Replaces the reference's binary-alloy API (kmc.hpp, lattice.hpp:104-154):
+ * OccupancyLattice + make_random_alloy + kmc_mcs_sequential +
+ * open_bonds_per_particle + count_b, with the sequential sweep replaced by
+ * the two-layer DT sweep (device blocks of `block`^3 sites in eight block
+ * sets, inner single-hit rounds over 4^3 domains).
+ */
+#ifndef LFG_KMC_H
+#define LFG_KMC_H
+
+#include "lfg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ======================================================================= KMC */
+typedef struct lfg_kmc lfg_kmc;
+
+typedef struct lfg_kmc_plan {
+    int32_t block; /* device block edge in sc sites (0 = auto) */
+} lfg_kmc_plan;
+
+/* OccupancyLattice(L) + KmcParams{eps, active_mode}.validate() (kmc.hpp:18-27). */
+LFG_API int lfg_kmc_create(lfg_kmc** h, int32_t L, double eps, int32_t both_active, uint64_t seed,
+                   const lfg_kmc_plan* plan, int32_t device);
+LFG_API int lfg_kmc_destroy(lfg_kmc* h);
+LFG_API int lfg_kmc_get_plan(const lfg_kmc* h, lfg_kmc_plan* out);
+/* words(): nwords = L^3/64 (lattice.hpp:125-126). */
+LFG_API int lfg_kmc_upload(lfg_kmc* h, const uint64_t* words, size_t nwords);
+LFG_API int lfg_kmc_download(lfg_kmc* h, uint64_t* words, size_t nwords);
+/* make_random_alloy (lattice.cpp:117-132) with the device counter RNG:
+ * Bernoulli(c) per valid site, statistically (not bit-) equal to the
+ * reference's serial stream. */
+LFG_API int lfg_kmc_init_random_alloy(lfg_kmc* h, double c, uint64_t seed);
+/* kmc_mcs_sequential (kmc.cpp:5-18) replaced by n_mcs two-layer DT sweeps. */
+LFG_API int lfg_kmc_sweep(lfg_kmc* h, int64_t n_mcs, lfg_counters* out);
+LFG_API int lfg_kmc_sweep_async(lfg_kmc* h, int64_t n_mcs);
+/* Enqueue one device-layer phase (0..7) of sweep `sweep` (profiling / sharded driver). */
+LFG_API int lfg_kmc_phase(lfg_kmc* h, uint64_t sweep, int32_t phase);
+/* Cumulative counters since create / reset (synchronises); deposits = exchanges. */
+LFG_API int lfg_kmc_counters(lfg_kmc* h, lfg_counters* out);
+LFG_API int lfg_kmc_reset_counters(lfg_kmc* h);
+/* open_bonds_per_particle (kmc.cpp:20-40) as exact sums; LFG_EDOMAIN if no B. */
+LFG_API int lfg_kmc_open_bond_sums(lfg_kmc* h, int64_t* particles, int64_t* open_bonds);
+LFG_API int lfg_kmc_open_bonds_per_particle(lfg_kmc* h, double* out);
+/* count_b (lattice.cpp:97-101). */
+LFG_API int lfg_kmc_count_b(lfg_kmc* h, int64_t* out);
+LFG_API int lfg_kmc_set_params(lfg_kmc* h, double eps, int32_t both_active);
+LFG_API int lfg_kmc_set_sweep_index(lfg_kmc* h, uint64_t sweep);
+LFG_API int lfg_kmc_get_sweep_index(const lfg_kmc* h, uint64_t* sweep);
+LFG_API int lfg_kmc_set_seed(lfg_kmc* h, uint64_t seed);
+LFG_API int lfg_kmc_set_stream(lfg_kmc* h, void* cuda_stream);
+LFG_API int lfg_kmc_synchronize(lfg_kmc* h);
+/* Device pointer of the occupancy words ([L][L][L/32] uint32) for interop. */
+LFG_API int lfg_kmc_device_words(lfg_kmc* h, void** dev_ptr, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFG_KMC_H */

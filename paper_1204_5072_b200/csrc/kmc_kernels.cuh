@@ -1,0 +1,31 @@
+// kmc_kernels.cuh -- launchers for the 3-D fcc binary-alloy KMC kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace lfg {
+
+struct KmcPhaseArgs {
+    uint32_t* w;                   // occupancy bits, sc layout [L][L][L/32] (z, y, x-words)
+    unsigned long long* counters;  // [1] exchanges
+    int32_t L, bk;                 // lattice edge, device block edge
+    uint64_t seed, sweep;
+    int32_t phase;                 // 0..7 position in the sweep's block-set order
+    int32_t both;                  // ActiveMode::both
+    uint32_t thr_lo[13];           // low 32 bits of ceil(exp(-d eps) 2^32), d = 0..12
+    uint32_t thr_hi[13];           // bit 32 (threshold == 2^32)
+};
+
+int kmc_blocks_per_cta(int bk);
+size_t kmc_phase_smem_bytes(int bk);
+cudaError_t kmc_phase_kernel_attrs();
+cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st);
+cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, uint32_t thr_lo, uint32_t thr_hi, uint64_t seed,
+                                  cudaStream_t st);
+cudaError_t kmc_launch_open_bonds(const uint32_t* w, int L, unsigned long long* out2, cudaStream_t st);
+cudaError_t kmc_launch_count_b(const uint32_t* w, int L, unsigned long long* out, cudaStream_t st);
+
+}  // namespace lfg
