@@ -120,6 +120,36 @@ LFG_API int lfg_kpz_synchronize(lfg_kpz* h);
  * interop (torch.distributed halo exchange on the sharded path). */
 LFG_API int lfg_kpz_device_spins(lfg_kpz* h, int32_t replica, void** dev_ptr, size_t* bytes);
 
+/* ---- strip-sharded path (multi-GPU) ----------------------
+ * The caller (one process per GPU) owns a device ring buffer of
+ * `row_capacity` spin rows (power of two; global row y lives at slot
+ * y & (row_capacity-1); each row is L/32 uint32 words) holding its strip
+ * plus ghost rows, and moves rows between ranks (NCCL send/recv).  These
+ * calls only enqueue on the handle's stream.  A handle from
+ * lfg_kpz_create_strip has no resident lattice of its own. */
+LFG_API int lfg_kpz_create_strip(lfg_kpz** h, int32_t L, double p, double q, uint64_t seed,
+                                 const lfg_kpz_plan* plan, int32_t device);
+/* Sweep-level draws of the DTr schedule: out = {ox, oy, set of phase 0..3}. */
+LFG_API int lfg_kpz_sweep_origin(int32_t L, const lfg_kpz_plan* plan, uint64_t seed, uint64_t sweep,
+                                 int32_t out[6]);
+/* One DT phase restricted to block rows [block_row_begin, +block_row_count)
+ * of the sweep's shifted frame (begin and count even). */
+LFG_API int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t block_row_begin,
+                                int32_t block_row_count, uint64_t sweep, int32_t phase);
+/* Fill global rows [row_begin, +row_count) (mod L): pattern 0 = make_flat_slopes,
+ * 1 = all slopes -1 (SlopeField constructor). */
+LFG_API int lfg_kpz_strip_fill(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t row_begin, int32_t row_count,
+                               int32_t pattern);
+/* W^2 pieces (kpz.cpp:62-81 split by rows): H0 = row-0 heights (int32[L], needs global row 0);
+ * per segment of seg_rows rows of [row_begin, +row_count): P1/D int32[nseg][L], P2 += sum p^2 (uint64). */
+LFG_API int lfg_kpz_strip_row0_heights(lfg_kpz* h, const void* rows, int32_t row_capacity, void* H0);
+LFG_API int lfg_kpz_strip_width_partials(lfg_kpz* h, const void* rows, int32_t row_capacity, int32_t row_begin,
+                                         int32_t row_count, int32_t seg_rows, void* P1, void* D, void* P2);
+/* Combine segments given in global row order (seg_len int32[nseg], device):
+ * sum h and sum h^2 - sum p^2 (add the all-reduced P2 to get sum h^2). */
+LFG_API int lfg_kpz_width_combine(lfg_kpz* h, const void* H0, const void* P1, const void* D, const void* seg_len,
+                                  int32_t nseg, int64_t* sum, int64_t* sum2_without_p2);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,7 +47,9 @@ struct lfg_kpz {
     int32_t* H0 = nullptr;                  // [L]
     int32_t* P1 = nullptr;                  // [G][L]
     int32_t* Dd = nullptr;                  // [G][L]
+    int32_t* seglen = nullptr;              // [G]
     unsigned long long* wout = nullptr;     // [3]
+    bool strip_only = false;                // created by lfg_kpz_create_strip: no resident lattice
     int32_t* hbuf = nullptr;                // [L][L] heights (small L)
     unsigned long long* hpin = nullptr;     // pinned readback [max(3, 2R)]
 
@@ -88,7 +90,12 @@ void check_handle(const lfg_kpz* h) {
     if (!h) throw Error(LFG_EINVAL, "null lfg_kpz handle");
 }
 
+void check_resident(const lfg_kpz* h) {
+    if (h->strip_only) throw Error(LFG_EINVAL, "handle was created with lfg_kpz_create_strip (no resident lattice)");
+}
+
 void check_replica(const lfg_kpz* h, int32_t r) {
+    check_resident(h);
     if (r < 0 || r >= h->R) throw Error(LFG_EINVAL, "replica index out of range: " + std::to_string(r));
 }
 
@@ -103,6 +110,11 @@ void ensure_width_scratch(lfg_kpz* h) {
     if (!h->P1) h->P1 = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
     if (!h->Dd) h->Dd = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
     if (!h->wout) h->wout = dmalloc<unsigned long long>(3, "alloc width scratch");
+    if (!h->seglen) {
+        h->seglen = dmalloc<int32_t>(size_t(G), "alloc width scratch");
+        std::vector<int32_t> v(size_t(G), S);
+        cuda_check(cudaMemcpy(h->seglen, v.data(), 4 * size_t(G), cudaMemcpyHostToDevice), "seglen");
+    }
 }
 
 void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel execution"); }
@@ -117,6 +129,9 @@ void enqueue_sweeps(lfg_kpz* h, int64_t n) {
     a.thrP = threshold32(h->p);
     a.thrQ = threshold32(h->q);
     a.general = !(h->p == 1.0 && h->q == 0.0);
+    a.row_mask = h->L - 1;
+    a.brow0 = 0;
+    a.nbrow = h->L / h->by;
     for (int64_t s = 0; s < n; ++s) {
         a.sweep = h->sweep + uint64_t(s);
         for (int k = 0; k < 4; ++k) {
@@ -229,6 +244,7 @@ int lfg_kpz_destroy(lfg_kpz* h) {
         dfree(h->P1);
         dfree(h->Dd);
         dfree(h->wout);
+        dfree(h->seglen);
         dfree(h->hbuf);
         if (h->hpin) cudaFreeHost(h->hpin);
         if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -249,6 +265,7 @@ int lfg_kpz_get_plan(const lfg_kpz* h, lfg_kpz_plan* out) {
 int lfg_kpz_init_flat(lfg_kpz* h) {
     return guarded([&] {
         check_handle(h);
+        check_resident(h);
         DeviceGuard g(h->device);
         cuda_check(kpz_launch_init_flat(h->f, h->L, h->R, h->stream), "init_flat");
         sync(h);
@@ -305,6 +322,7 @@ int lfg_kpz_download(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size
 int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out) {
     return guarded([&] {
         check_handle(h);
+        check_resident(h);
         if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
         DeviceGuard g(h->device);
         read_counters(h);
@@ -321,6 +339,7 @@ int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out) {
 int lfg_kpz_sweep_async(lfg_kpz* h, int64_t n_mcs) {
     return guarded([&] {
         check_handle(h);
+        check_resident(h);
         if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
         DeviceGuard g(h->device);
         enqueue_sweeps(h, n_mcs);
@@ -330,6 +349,7 @@ int lfg_kpz_sweep_async(lfg_kpz* h, int64_t n_mcs) {
 int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase) {
     return guarded([&] {
         check_handle(h);
+        check_resident(h);
         if (phase < 0 || phase > 3) throw Error(LFG_EINVAL, "phase must be in 0..3");
         DeviceGuard g(h->device);
         KpzPhaseArgs a{};
@@ -341,6 +361,9 @@ int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase) {
         a.thrP = threshold32(h->p);
         a.thrQ = threshold32(h->q);
         a.general = !(h->p == 1.0 && h->q == 0.0);
+        a.row_mask = h->L - 1;
+        a.brow0 = 0;
+        a.nbrow = h->L / h->by;
         a.sweep = sweep;
         a.phase = phase;
         cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
@@ -350,7 +373,7 @@ int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase) {
 int lfg_kpz_counters(lfg_kpz* h, int32_t replica, lfg_counters* out) {
     return guarded([&] {
         check_handle(h);
-        check_replica(h, replica);
+        if (replica < 0 || replica >= h->R) throw Error(LFG_EINVAL, "replica index out of range");
         DeviceGuard g(h->device);
         read_counters(h);
         *out = make_counters(h->attempts[size_t(replica)], h->hcnt[2 * replica], h->hcnt[2 * replica + 1]);
@@ -375,7 +398,8 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         DeviceGuard g(h->device);
         ensure_width_scratch(h);
         cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
-        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->wout, h->stream), "width scan");
+        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->seglen, h->wout, h->stream),
+                   "width scan");
         cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         *sum = int64_t(h->hpin[0]);
@@ -469,6 +493,148 @@ int lfg_kpz_device_spins(lfg_kpz* h, int32_t replica, void** ptr, size_t* bytes)
         check_replica(h, replica);
         *ptr = h->rep(replica);
         *bytes = h->words_per_replica() * 4;
+    });
+}
+
+// ------------------------------------------------------------------ strip-sharded path
+int lfg_kpz_create_strip(lfg_kpz** out, int32_t L, double p, double q, uint64_t seed, const lfg_kpz_plan* plan,
+                         int32_t device) {
+    return guarded([&] {
+        if (!out) throw Error(LFG_EINVAL, "null output handle");
+        *out = nullptr;
+        validate_size(L);
+        validate_params(p, q);
+        auto* h = new lfg_kpz();
+        try {
+            h->L = L;
+            h->p = p;
+            h->q = q;
+            h->R = 1;
+            h->device = device;
+            h->strip_only = true;
+            resolve_plan(h, plan);
+            h->seeds.assign(1, seed);
+            h->hcnt.assign(2, 0);
+            h->attempts.assign(1, 0);
+            DeviceGuard g(device);
+            cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            h->own_stream = true;
+            cuda_check(kpz_phase_kernel_attrs(), "kernel attributes");
+            h->dcnt = dmalloc<unsigned long long>(2, "alloc counters");
+            cuda_check(cudaMallocHost(&h->hpin, sizeof(unsigned long long) * 3), "alloc pinned");
+            cuda_check(cudaMemsetAsync(h->dcnt, 0, 16, h->stream), "memset");
+            sync(h);
+        } catch (...) {
+            lfg_kpz_destroy(h);
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int lfg_kpz_sweep_origin(int32_t L, const lfg_kpz_plan* plan, uint64_t seed, uint64_t sweep, int32_t out6[6]) {
+    return guarded([&] {
+        lfg_kpz tmp;
+        tmp.L = L;
+        validate_size(L);
+        resolve_plan(&tmp, plan);
+        const KpzSweep sw = kpz_sweep_draw(tmp.bx, tmp.by, seed, sweep);
+        out6[0] = sw.ox;
+        out6[1] = sw.oy;
+        for (int k = 0; k < 4; ++k) out6[2 + k] = sw.set(k);
+    });
+}
+
+namespace {
+void check_ring(const lfg_kpz* h, const void* rows, int32_t cap) {
+    if (!rows) throw Error(LFG_EINVAL, "null row buffer");
+    if (cap < 1 || !is_pow2(cap) || cap > h->L)
+        throw Error(LFG_EINVAL, "row_capacity must be a power of two <= L, got " + std::to_string(cap));
+}
+}  // namespace
+
+int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0, int32_t nbrow, uint64_t sweep,
+                        int32_t phase) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, rows, cap);
+        if (phase < 0 || phase > 3) throw Error(LFG_EINVAL, "phase must be in 0..3");
+        if (brow0 < 0 || (brow0 & 1) || nbrow < 2 || (nbrow & 1) || brow0 + nbrow > h->L / h->by)
+            throw Error(LFG_EINVAL, "block-row range must be even-aligned inside [0, L/block_y)");
+        if (cap < h->L && cap < nbrow * h->by + 2)
+            throw Error(LFG_EINVAL, "row_capacity too small for the strip and its ghost rows");
+        DeviceGuard g(h->device);
+        KpzPhaseArgs a{};
+        a.f = static_cast<uint32_t*>(rows);
+        a.counters = h->dcnt;
+        a.L = h->L;
+        a.bx = h->bx;
+        a.by = h->by;
+        a.thrP = threshold32(h->p);
+        a.thrQ = threshold32(h->q);
+        a.general = !(h->p == 1.0 && h->q == 0.0);
+        a.row_mask = cap - 1;
+        a.brow0 = brow0;
+        a.nbrow = nbrow;
+        a.sweep = sweep;
+        a.phase = phase;
+        cuda_check(kpz_launch_phase(a, h->seeds.data(), 1, h->stream), "kpz_dtr_phase launch");
+        h->attempts[0] += int64_t(nbrow) * h->by * h->L / 4;
+    });
+}
+
+int lfg_kpz_strip_fill(lfg_kpz* h, void* rows, int32_t cap, int32_t row_begin, int32_t row_count, int32_t pattern) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, rows, cap);
+        if (row_count < 0 || row_count > cap) throw Error(LFG_EINVAL, "row_count out of range");
+        DeviceGuard g(h->device);
+        cuda_check(kpz_launch_fill_rows(static_cast<uint32_t*>(rows), h->L, cap - 1, row_begin, row_count, pattern,
+                                        h->stream),
+                   "fill rows");
+    });
+}
+
+int lfg_kpz_strip_row0_heights(lfg_kpz* h, const void* rows, int32_t cap, void* H0) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, rows, cap);
+        DeviceGuard g(h->device);
+        cuda_check(kpz_launch_row0_heights(static_cast<const uint32_t*>(rows), h->L, static_cast<int32_t*>(H0),
+                                           h->stream),
+                   "row0 heights");
+    });
+}
+
+int lfg_kpz_strip_width_partials(lfg_kpz* h, const void* rows, int32_t cap, int32_t row_begin, int32_t row_count,
+                                 int32_t seg_rows, void* P1, void* D, void* P2) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, rows, cap);
+        if (seg_rows < 1 || row_count < 1) throw Error(LFG_EINVAL, "empty width segment");
+        DeviceGuard g(h->device);
+        cuda_check(kpz_launch_width_partials(static_cast<const uint32_t*>(rows), h->L, cap - 1, row_begin, row_count,
+                                             seg_rows, static_cast<int32_t*>(P1), static_cast<int32_t*>(D),
+                                             static_cast<unsigned long long*>(P2), h->stream),
+                   "width partials");
+    });
+}
+
+int lfg_kpz_width_combine(lfg_kpz* h, const void* H0, const void* P1, const void* D, const void* seg_len,
+                          int32_t nseg, int64_t* sum, int64_t* sum2_rel) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        if (!h->wout) h->wout = dmalloc<unsigned long long>(3, "alloc width scratch");
+        cuda_check(cudaMemsetAsync(h->wout, 0, 16, h->stream), "memset");
+        cuda_check(kpz_launch_width_combine(static_cast<const int32_t*>(H0), static_cast<const int32_t*>(P1),
+                                            static_cast<const int32_t*>(D), static_cast<const int32_t*>(seg_len),
+                                            h->L, nseg, h->wout, h->stream),
+                   "width combine");
+        cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 16, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        *sum = int64_t(h->hpin[0]);
+        *sum2_rel = int64_t(h->hpin[1]);
     });
 }
 

@@ -212,12 +212,15 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
     const int rep = a.rep0 + int(blockIdx.z);
     const uint64_t seed = a.seeds[blockIdx.z];
     const uint64_t sweep = a.sweep;
-    uint32_t* __restrict__ f = a.f + size_t(rep) * size_t(L) * size_t(wpr);
+    // Rows live at buffer slot (global row & rmask): rmask = L-1 for a whole
+    // lattice, C-1 for a strip shard whose ring buffer holds C >= H + 4 by + 2 rows.
+    const int rmask = Lm & a.row_mask;
+    uint32_t* __restrict__ f = a.f + size_t(rep) * size_t(a.row_mask + 1) * size_t(wpr);
 
     const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, sweep);
     const int set = sw.set(a.phase);
     const int bxi = 2 * int(blockIdx.x) + (set & 1);
-    const int byi = 2 * int(blockIdx.y) + (set >> 1);
+    const int byi = a.brow0 + 2 * int(blockIdx.y) + (set >> 1);  // brow0 even
     const uint32_t block_id = uint32_t(byi) * uint32_t(L / a.bx) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * a.bx) & Lm;
     const int Y0 = (sw.oy + byi * a.by) & Lm;
@@ -233,7 +236,7 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
 #pragma unroll
             for (int t = 0; t < RB; ++t) {
                 const int R = R0 + t * nwarps;
-                const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+                const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
                 v0[t] = R <= a.by ? __ldg(row + ((w0 + lane) & wmask)) : 0u;
                 v1[t] = (R <= a.by && lane < 3) ? __ldg(row + ((w0 + 32 + lane) & wmask)) : 0u;
             }
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
         }
     } else {
         for (int R = warp - 1; R <= a.by; R += nwarps) {
-            const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
             for (int k = lane; k < Wt + 2; k += 32) {
                 const uint32_t lo = __ldg(row + ((w0 + k) & wmask));
                 const uint32_t hi = __ldg(row + ((w0 + k + 1) & wmask));
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     if (FULL) {
         for (int R = warp; R < a.by; R += nwarps) {
-            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
             const uint32_t cur = sm[(R + 8) * 64 + lane];             // slot lane
             const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, cur, 1);  // slot lane-1
             const uint32_t lo = lane == 0 ? sm[sm_slot(R, -1)] : prv;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
         }
     } else {
         for (int R = warp; R < a.by; R += nwarps) {
-            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & Lm) * uint32_t(wpr);
+            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
             for (int k = lane; k <= Wt; k += 32) {
                 if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
                 row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
@@ -324,7 +327,7 @@ cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int r
         b.rep0 = r0;
         const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
         for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
-        const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.L / a.by / 2), unsigned(nr));
+        const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.nbrow / 2), unsigned(nr));
         if (a.by >= 16 * LFG_KPZ_NT) launch_nt<LFG_KPZ_NT>(b, grid, smem, st);
         else launch_nt<1>(b, grid, smem, st);
     }
@@ -498,11 +501,13 @@ cudaError_t kpz_launch_to_slopes(const uint32_t* f, int L, uint32_t* X, uint32_t
 // ============================================================ W^2 scan
 // interface_width(const SlopeField&) (kpz.cpp:62-81): h(i,0) = sum_{k=1..i}
 // s_x(k,0); h(i,j) = h(i,j-1) + s_y(i,j); exact int64 sum and sum of squares.
-// Stage 1: row-0 heights H0[i] (one CTA).  Stage 2: per (row segment g, word
-// column w), relative column heights p (p = 0 at the segment's first row for
-// g = 0, else the first row's s_y) with P1 = sum p (per column), the final p
-// (D), and sum p^2 (global).  Stage 3: per column, walk the segments:
-//   sum h  += S_g H + P1,   sum h^2 += S_g H^2 + 2 H P1,   H += D.
+// Stage 1: row-0 heights H0[i] (one CTA).  Stage 2: the rows are cut into
+// segments (global row ranges, in row order); per (segment, word column):
+// relative column heights p (p = 0 on global row 0, otherwise the first row
+// already adds its s_y), P1 = sum p per column, D = last p per column, and
+// sum p^2 (global).  Stage 3: per column, walk the segments in row order:
+//   sum h += len H + P1,   sum h^2 += len H^2 + 2 H P1,   H += D
+// with H = H0 at row 0.  Segments may come from different strip shards.
 __global__ void kpz_row0_heights_kernel(const uint32_t* __restrict__ f, int L, int32_t* __restrict__ H0) {
     __shared__ int32_t part[1024];
     const int wpr = L >> 5, wmask = wpr - 1;
@@ -536,24 +541,27 @@ __global__ void kpz_row0_heights_kernel(const uint32_t* __restrict__ f, int L, i
     }
 }
 
-__global__ void __launch_bounds__(128) kpz_width_seg_kernel(const uint32_t* __restrict__ f, int L, int S,
+__global__ void __launch_bounds__(128) kpz_width_seg_kernel(const uint32_t* __restrict__ f, int L, int rmask,
+                                                            int row_begin, int row_count, int S,
                                                             int32_t* __restrict__ P1, int32_t* __restrict__ D,
                                                             unsigned long long* __restrict__ sum_p2) {
     const int wpr = L >> 5, Lm = L - 1;
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
     const int g = blockIdx.y;
+    const int jl0 = g * S, n = min(S, row_count - jl0);
     int32_t p[32], s1[32];
 #pragma unroll
     for (int c = 0; c < 32; ++c) { p[c] = 0; s1[c] = 0; }
     long long s2 = 0;
-    if (w < wpr) {
-        const int j0 = g * S;
-        uint32_t prev = f[size_t((j0 - 1) & Lm) * wpr + w];
-        for (int j = j0; j < j0 + S; ++j) {
-            const uint32_t F = f[size_t(j) * wpr + w];
-            const uint32_t up = ~(F ^ prev);  // sigma_y(.,j) bits
+    if (w < wpr && n > 0) {
+        const int jg0 = (row_begin + jl0) & Lm;
+        uint32_t prev = f[size_t(((jg0 - 1) & Lm) & rmask) * wpr + w];
+        for (int jl = 0; jl < n; ++jl) {
+            const int jg = (jg0 + jl) & Lm;
+            const uint32_t F = f[size_t(jg & rmask) * wpr + w];
+            const uint32_t up = ~(F ^ prev);  // sigma_y(., jg) bits
             prev = F;
-            const bool add = j > 0;
+            const bool add = jg != 0;
             int32_t rowsq = 0;
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
@@ -569,22 +577,22 @@ __global__ void __launch_bounds__(128) kpz_width_seg_kernel(const uint32_t* __re
             D[size_t(g) * L + 32 * w + c] = p[c];
         }
     }
-    // s2 >= 0 always; reduce within the warp then one atomic.
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_down_sync(0xFFFFFFFFu, s2, o);
     if ((threadIdx.x & 31) == 0 && s2) atomicAdd(sum_p2, (unsigned long long)s2);
 }
 
 __global__ void kpz_width_combine_kernel(const int32_t* __restrict__ H0, const int32_t* __restrict__ P1,
-                                         const int32_t* __restrict__ D, int L, int S, int G,
-                                         unsigned long long* __restrict__ out /* sum, sum2 as int64 */) {
+                                         const int32_t* __restrict__ D, const int32_t* __restrict__ seg_len,
+                                         int L, int G, unsigned long long* __restrict__ out /* sum, sum2 */) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     long long sh = 0, sh2 = 0;
     if (c < L) {
         long long H = H0[c];
         for (int g = 0; g < G; ++g) {
             const long long q1 = P1[size_t(g) * L + c];
-            sh += (long long)S * H + q1;
-            sh2 += (long long)S * H * H + 2 * H * q1;
+            const long long n = seg_len[g];
+            sh += n * H + q1;
+            sh2 += n * H * H + 2 * H * q1;
             H += D[size_t(g) * L + c];
         }
     }
@@ -600,15 +608,55 @@ __global__ void kpz_width_combine_kernel(const int32_t* __restrict__ H0, const i
 
 int kpz_width_segment_rows(int L) { return L >= 4096 ? 2048 : (L >= 256 ? 128 : L); }
 
-cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D,
+cudaError_t kpz_launch_row0_heights(const uint32_t* row0, int L, int32_t* H0, cudaStream_t st) {
+    kpz_row0_heights_kernel<<<1, 1024, 0, st>>>(row0, L, H0);
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_width_partials(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int S,
+                                      int32_t* P1, int32_t* D, unsigned long long* sum_p2, cudaStream_t st) {
+    const int wpr = L >> 5;
+    const int G = (row_count + S - 1) / S;
+    const dim3 g1(unsigned((wpr + 127) / 128), unsigned(G));
+    kpz_width_seg_kernel<<<g1, 128, 0, st>>>(f, L, rmask, row_begin, row_count, S, P1, D, sum_p2);
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_width_combine(const int32_t* H0, const int32_t* P1, const int32_t* D, const int32_t* seg_len,
+                                     int L, int G, unsigned long long* out2, cudaStream_t st) {
+    kpz_width_combine_kernel<<<(L + 255) / 256, 256, 0, st>>>(H0, P1, D, seg_len, L, G, out2);
+    return cudaGetLastError();
+}
+
+cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D, int32_t* seg_len,
                              unsigned long long* out3, cudaStream_t st) {
     const int S = kpz_width_segment_rows(L);
     const int G = L / S;
-    const int wpr = L >> 5;
-    kpz_row0_heights_kernel<<<1, 1024, 0, st>>>(f, L, H0);
-    const dim3 g1(unsigned((wpr + 127) / 128), unsigned(G));
-    kpz_width_seg_kernel<<<g1, 128, 0, st>>>(f, L, S, P1, D, out3 + 2);
-    kpz_width_combine_kernel<<<(L + 255) / 256, 256, 0, st>>>(H0, P1, D, L, S, G, out3);
+    cudaError_t e = kpz_launch_row0_heights(f, L, H0, st);
+    if (e == cudaSuccess) e = kpz_launch_width_partials(f, L, L - 1, 0, L, S, P1, D, out3 + 2, st);
+    if (e == cudaSuccess) e = kpz_launch_width_combine(H0, P1, D, seg_len, L, G, out3, st);
+    return e;
+}
+
+// Fill rows [row_begin, row_begin + row_count) (global, mod L) of a ring buffer
+// with a row-periodic spin pattern (pattern word = pat[global row & 3]).
+__global__ void kpz_fill_rows_kernel(uint32_t* f, int L, int rmask, int row_begin, int row_count, uint4 pat) {
+    const int wpr = L >> 5, Lm = L - 1;
+    const size_t n = size_t(row_count) * wpr;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n; k += size_t(gridDim.x) * blockDim.x) {
+        const int jg = (row_begin + int(k / size_t(wpr))) & Lm;
+        const int q = jg & 3;
+        f[size_t(jg & rmask) * wpr + k % size_t(wpr)] = q == 0 ? pat.x : (q == 1 ? pat.y : (q == 2 ? pat.z : pat.w));
+    }
+}
+
+cudaError_t kpz_launch_fill_rows(uint32_t* f, int L, int rmask, int row_begin, int row_count, int pattern,
+                                 cudaStream_t st) {
+    const uint4 pat = pattern == 0 ? make_uint4(0x66666666u, 0x99999999u, 0x99999999u, 0x66666666u)
+                                   : make_uint4(0xAAAAAAAAu, 0x55555555u, 0xAAAAAAAAu, 0x55555555u);
+    const size_t n = size_t(row_count) * (L >> 5);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    kpz_fill_rows_kernel<<<blocks, 256, 0, st>>>(f, L, rmask, row_begin, row_count, pat);
     return cudaGetLastError();
 }
 

@@ -21,6 +21,8 @@ struct KpzPhaseArgs {
     uint64_t thrP, thrQ;            // ceil(p 2^32), ceil(q 2^32)
     bool general;                   // false: p == 1, q == 0 fast path
     int32_t rep0;                   // first replica of this launch (set by the launcher)
+    int32_t row_mask;               // buffer row slot = global row & row_mask (L-1: whole lattice)
+    int32_t brow0, nbrow;           // block rows [brow0, brow0 + nbrow) of the shifted frame (strips)
     uint64_t seeds[kMaxRepPerLaunch];
 };
 
@@ -34,8 +36,15 @@ cudaError_t kpz_launch_from_slopes(const uint32_t* X, const uint32_t* Y, int L, 
 cudaError_t kpz_launch_to_slopes(const uint32_t* f, int L, uint32_t* X, uint32_t* Y, const uint32_t* Xcmp,
                                  const uint32_t* Ycmp, unsigned long long* mismatch, cudaStream_t st);
 int kpz_width_segment_rows(int L);
-cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D,
+cudaError_t kpz_launch_width(const uint32_t* f, int L, int32_t* H0, int32_t* P1, int32_t* D, int32_t* seg_len,
                              unsigned long long* out3, cudaStream_t st);
+cudaError_t kpz_launch_row0_heights(const uint32_t* row0, int L, int32_t* H0, cudaStream_t st);
+cudaError_t kpz_launch_width_partials(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int S,
+                                      int32_t* P1, int32_t* D, unsigned long long* sum_p2, cudaStream_t st);
+cudaError_t kpz_launch_width_combine(const int32_t* H0, const int32_t* P1, const int32_t* D, const int32_t* seg_len,
+                                     int L, int G, unsigned long long* out2, cudaStream_t st);
+cudaError_t kpz_launch_fill_rows(uint32_t* f, int L, int rmask, int row_begin, int row_count, int pattern,
+                                 cudaStream_t st);
 cudaError_t kpz_launch_heights(const uint32_t* f, int L, int32_t* H0, int32_t* h, cudaStream_t st);
 
 }  // namespace lfg

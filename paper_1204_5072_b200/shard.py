@@ -1,0 +1,410 @@
+"""Strip-sharded KPZ DTr sweep across GPUs.
+
+Partition.  With `world` ranks, H = L/world rows per rank, H a multiple of
+2*block_y.  In sweep s (origin oy_s), rank g owns the rows
+[oy_s + g H, oy_s + (g+1) H) (mod L) of the lattice -- exactly the block rows
+[g H/by, (g+1) H/by) of the sweep's shifted frame -- so every device block of
+every phase lives on one rank and the per-rank kernel is the single-GPU
+kernel restricted to those block rows (lfg_kpz_strip_phase).
+
+Storage.  Each rank holds a device ring buffer of C rows (power of two
+>= H + 4 by + 2; C = L when world == 1): global row y sits at slot y & (C-1),
+so the strip, its two ghost rows and the rows in flight during an ownership
+roll never collide and nothing is ever shifted in memory.
+
+Exchanges (the only collective traffic; all NCCL send/recv between ring
+neighbours, one L/32-word row = 16 KiB at L = 2^17):
+  * per sweep, the ownership roll: the origin moves by d = oy_s - oy_{s-1}
+    in (-2 by, 2 by); |d| rows move to the neighbour on one side and |d|
+    arrive from the other;
+  * per phase, one ghost row: a phase of block-row parity sy reads exactly
+    one row outside the strip -- the first row of rank g+1 (sy = 1) or the
+    last row of rank g-1 (sy = 0) -- and no phase writes outside the strip.
+The RNG is keyed on global tile/block ids of the shifted frame, so the
+sharded trajectory is bit-identical to the single-GPU one for any world size
+(tests/test_shard_gpu.py, tests/test_shard_cpu.py).
+
+Execution back-ends (`comm`):
+  * DistComm: torch.distributed point-to-point (NCCL over NVLink on B200,
+    gloo on CPU for the world_size-2 tests);
+  * LocalComm: all shards in one process (e.g. k shards on one GPU), rows
+    copied directly -- used to prove bit-identity with a single device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _native
+
+
+def next_pow2(v: int) -> int:
+    p = 1
+    while p < v:
+        p <<= 1
+    return p
+
+
+# ----------------------------------------------------------------------------- plan
+@dataclass(frozen=True)
+class StripPlan:
+    L: int
+    world: int
+    bx: int
+    by: int
+
+    def __post_init__(self):
+        if self.L % self.world:
+            raise ValueError("world must divide L")
+        if self.world > 1 and self.H % (2 * self.by):
+            raise ValueError(f"strip height L/world = {self.H} must be a multiple of 2*block_y = {2 * self.by}")
+
+    @property
+    def H(self) -> int:
+        return self.L // self.world
+
+    @property
+    def cap(self) -> int:
+        return self.L if self.world == 1 else min(self.L, next_pow2(self.H + 4 * self.by + 2))
+
+    @property
+    def wpr(self) -> int:
+        return self.L // 32
+
+    def start(self, oy: int, rank: int) -> int:
+        return (oy + rank * self.H) % self.L
+
+    def block_rows(self, rank: int):
+        return rank * self.H // self.by, self.H // self.by
+
+    def roll(self, oy_old: int, oy_new: int, rank: int):
+        """Row moves when the origin goes from oy_old to oy_new:
+        list of (kind, peer, row_begin, count)."""
+        if self.world == 1 or oy_old == oy_new:
+            return []
+        d = oy_new - oy_old
+        s = self.start(oy_old, rank)
+        up, dn = (rank + 1) % self.world, (rank - 1) % self.world
+        if d > 0:
+            return [("send", dn, s, d), ("recv", up, s + self.H, d)]
+        return [("send", up, s + self.H + d, -d), ("recv", dn, s + d, -d)]
+
+    def ghost(self, oy: int, rank: int, sy: int):
+        """The one ghost row a phase of block-row parity sy reads, refreshed."""
+        if self.world == 1:
+            return []
+        s = self.start(oy, rank)
+        up, dn = (rank + 1) % self.world, (rank - 1) % self.world
+        if sy == 1:  # top block row active: needs row s+H (first row of rank+1)
+            return [("send", dn, s, 1), ("recv", up, s + self.H, 1)]
+        return [("send", up, s + self.H - 1, 1), ("recv", dn, s - 1, 1)]  # bottom: last row of rank-1
+
+    def pieces(self, row_begin: int, count: int):
+        """Split global rows [row_begin, +count) mod L into contiguous slot ranges
+        of the ring buffer: list of (slot_begin, n)."""
+        out = []
+        y = row_begin % self.L
+        left = count
+        while left > 0:
+            slot = y % self.cap
+            n = min(left, self.cap - slot, self.L - y)
+            out.append((slot, n))
+            y = (y + n) % self.L
+            left -= n
+        return out
+
+    def row_pieces_global(self, row_begin: int, count: int):
+        """Split global rows into pieces that do not wrap past row L-1: (start, n)."""
+        out = []
+        y = row_begin % self.L
+        left = count
+        while left > 0:
+            n = min(left, self.L - y)
+            out.append((y, n))
+            y = (y + n) % self.L
+            left -= n
+        return out
+
+
+# ----------------------------------------------------------------------------- engines
+class CudaStripEngine:
+    """One rank's strip on a CUDA device: ring buffer (torch uint32 rows) +
+    a strip handle of liblfg.so (lfg_kpz_create_strip)."""
+
+    def __init__(self, plan: StripPlan, p: float, q: float, seed: int, device: int = 0):
+        import torch
+
+        self.plan = plan
+        self.device = device
+        self.torch = torch
+        self.buf = torch.zeros((plan.cap, plan.wpr), dtype=torch.int32, device=f"cuda:{device}")
+        lib = _native.lib()
+        h = C.c_void_p()
+        kp = _native.KpzPlan(plan.bx, plan.by)
+        _native.check(lib.lfg_kpz_create_strip(C.byref(h), plan.L, float(p), float(q), int(seed), C.byref(kp),
+                                               device))
+        self.h = h
+        self.stream = torch.cuda.Stream(device=device)
+        _native.check(lib.lfg_kpz_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
+
+    def close(self):
+        if self.h is not None:
+            _native.lib().lfg_kpz_destroy(self.h)
+            self.h = None
+
+    def rows(self, slot: int, n: int):
+        return self.buf[slot:slot + n]
+
+    def sync(self):
+        self.stream.synchronize()
+
+    def fill(self, row_begin: int, count: int, pattern: int):
+        _native.check(_native.lib().lfg_kpz_strip_fill(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
+                                                       row_begin, count, pattern))
+
+    def phase(self, sweep: int, phase: int, brow0: int, nbrow: int):
+        _native.check(_native.lib().lfg_kpz_strip_phase(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
+                                                        brow0, nbrow, int(sweep), phase))
+
+    def counters(self):
+        c = _native.Counters()
+        _native.check(_native.lib().lfg_kpz_counters(self.h, 0, C.byref(c)))
+        return c
+
+    def width_partials(self, pieces, S):
+        """[(start, n)] -> (P1 [nseg, L] int32, D [nseg, L] int32, seg (start, len) list, P2 int)."""
+        torch = self.torch
+        L = self.plan.L
+        segs = []
+        for (a, n) in pieces:
+            for k in range(0, n, S):
+                segs.append((a + k, min(S, n - k)))
+        P1 = torch.zeros((len(segs), L), dtype=torch.int32, device=self.buf.device)
+        D = torch.zeros_like(P1)
+        P2 = torch.zeros(1, dtype=torch.int64, device=self.buf.device)
+        lib = _native.lib()
+        for gi, (a, n) in enumerate(segs):
+            _native.check(lib.lfg_kpz_strip_width_partials(
+                self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap, a, n, n,
+                C.c_void_p(P1[gi].data_ptr()), C.c_void_p(D[gi].data_ptr()), C.c_void_p(P2.data_ptr())))
+        return P1, D, segs, P2
+
+    def row0_heights(self):
+        H0 = self.torch.zeros(self.plan.L, dtype=self.torch.int32, device=self.buf.device)
+        _native.check(_native.lib().lfg_kpz_strip_row0_heights(self.h, C.c_void_p(self.buf.data_ptr()),
+                                                               self.plan.cap, C.c_void_p(H0.data_ptr())))
+        return H0
+
+    def combine(self, H0, P1, D, seglen):
+        s, s2 = C.c_int64(), C.c_int64()
+        _native.check(_native.lib().lfg_kpz_width_combine(
+            self.h, C.c_void_p(H0.data_ptr()), C.c_void_p(P1.data_ptr()), C.c_void_p(D.data_ptr()),
+            C.c_void_p(seglen.data_ptr()), int(seglen.numel()), C.byref(s), C.byref(s2)))
+        return int(s.value), int(s2.value)
+
+
+def sweep_origin(plan: StripPlan, seed: int, sweep: int):
+    out = (C.c_int32 * 6)()
+    kp = _native.KpzPlan(plan.bx, plan.by)
+    _native.check(_native.lib().lfg_kpz_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep), out))
+    return int(out[0]), int(out[1]), [int(out[2 + k]) for k in range(4)]
+
+
+# ----------------------------------------------------------------------------- comms
+class LocalComm:
+    """All shards in one process: ops are executed as direct row copies."""
+
+    def __init__(self, engines):
+        self.engines = engines
+        self.world = len(engines)
+
+    def exchange(self, ops_per_rank):
+        # a send of rows [b, b+n) from rank r lands in the same global rows of `peer`
+        for r, ops in enumerate(ops_per_rank):
+            for kind, peer, b, n in ops:
+                if kind != "send":
+                    continue
+                src, dst = self.engines[r], self.engines[peer]
+                src.sync()
+                for (slot, m) in src.plan.pieces(b, n):
+                    dst.rows(slot, m).copy_(src.rows(slot, m))
+                dst.sync()
+
+
+class DistComm:
+    """torch.distributed point-to-point between ring neighbours (one shard per process)."""
+
+    def __init__(self, engine, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.engine = engine
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def exchange(self, ops):
+        dist = self.dist
+        e = self.engine
+        e.sync()
+        p2p = []
+        for kind, peer, b, n in ops:
+            for (slot, m) in e.plan.pieces(b, n):
+                t = e.rows(slot, m)
+                p2p.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer, self.group))
+        if p2p:
+            for w in dist.batch_isend_irecv(p2p):
+                w.wait()
+        if hasattr(e, "torch") and e.buf.is_cuda:
+            e.torch.cuda.current_stream(e.buf.device).synchronize()
+
+
+# ----------------------------------------------------------------------------- driver
+class ShardedKpz:
+    """Strip-sharded lattice.  `engines` are this process's shards (all of them
+    for LocalComm, exactly one for DistComm); `ranks` their global ranks."""
+
+    def __init__(self, plan: StripPlan, seed: int, engines, ranks, comm):
+        self.plan = plan
+        self.seed = seed
+        self.engines = list(engines)
+        self.ranks = list(ranks)
+        self.comm = comm
+        self.sweep_index = 0
+        self.oy = None  # origin the current row ownership refers to
+
+    # ---- initial state -------------------------------------------------------
+    def make_flat_slopes(self, sweep_index: int = 0):
+        """Each rank fills its window for the first sweep's origin plus both ghosts
+        (no communication)."""
+        self.sweep_index = sweep_index
+        _, oy, _ = sweep_origin(self.plan, self.seed, sweep_index)
+        for e, r in zip(self.engines, self.ranks):
+            e.fill(self.plan.start(oy, r) - 1, self.plan.H + 2, 0)
+        for e in self.engines:
+            e.sync()
+        self.oy = oy
+
+    # ---- sweeps --------------------------------------------------------------
+    def _exchange(self, fn):
+        if isinstance(self.comm, LocalComm):
+            self.comm.exchange([fn(r) for r in self.ranks])
+        else:
+            self.comm.exchange(fn(self.ranks[0]))
+
+    def sweep(self, n: int = 1):
+        pl = self.plan
+        for _ in range(n):
+            s = self.sweep_index
+            _, oy, sets = sweep_origin(pl, self.seed, s)
+            if oy != self.oy:
+                old = self.oy
+                self._exchange(lambda r: pl.roll(old, oy, r))
+                self.oy = oy
+            for k in range(4):
+                sy = sets[k] >> 1
+                self._exchange(lambda r: pl.ghost(oy, r, sy))
+                for e, r in zip(self.engines, self.ranks):
+                    b0, nb = pl.block_rows(r)
+                    e.phase(s, k, b0, nb)
+            self.sweep_index += 1
+        for e in self.engines:
+            e.sync()
+
+    def counters_local(self):
+        tot = [0, 0]
+        for e in self.engines:
+            c = e.counters()
+            tot[0] += c.deposits
+            tot[1] += c.detaches
+        return tot
+
+    # ---- readout -------------------------------------------------------------
+    def owned_pieces(self, rank: int):
+        return self.plan.row_pieces_global(self.plan.start(self.oy, rank), self.plan.H)
+
+    def gather_rows(self):
+        """Full lattice of spin rows as one CPU int32 tensor [L, L/32].  With
+        DistComm every rank contributes its owned rows (all_reduce of disjoint
+        row sets); with LocalComm the shards are read directly."""
+        import torch
+
+        L, wpr = self.plan.L, self.plan.wpr
+        out = torch.zeros((L, wpr), dtype=torch.int32)
+        for e, r in zip(self.engines, self.ranks):
+            e.sync()
+            for (a, n) in self.owned_pieces(r):
+                y = a
+                for (slot, m) in self.plan.pieces(a, n):
+                    out[y:y + m] = e.rows(slot, m).cpu()
+                    y += m
+        if isinstance(self.comm, DistComm):
+            dist = self.comm.dist
+            dev = self.engines[0].buf.device
+            t = out.to(dev)
+            # rows are disjoint across ranks: XOR-free sum of int32 words is exact
+            # only without overflow, so reduce as int64 halves
+            lo = (t & 0xFFFF).to(torch.int64)
+            hi = ((t >> 16) & 0xFFFF).to(torch.int64)
+            dist.all_reduce(lo, group=self.comm.group)
+            dist.all_reduce(hi, group=self.comm.group)
+            out = ((hi << 16) | lo).to(torch.int32).cpu()
+        return out
+
+    def width_sums(self):
+        """interface_width sums (kpz.cpp:62-81) of the sharded lattice: exact int64
+        (sum h, sum h^2), h(0,0) = 0.  Segments of all ranks are combined in
+        global row order; H0 comes from the rank that owns row 0."""
+        import torch
+
+        pl = self.plan
+        S = 2048 if pl.L >= 4096 else max(1, min(pl.L, 128))
+        local = []
+        H0 = None
+        P2 = 0
+        for e, r in zip(self.engines, self.ranks):
+            pieces = self.owned_pieces(r)
+            P1, D, segs, p2 = e.width_partials(pieces, S)
+            e.sync()
+            P2 += int(p2.item())
+            local.append((P1, D, segs))
+            if any(a == 0 for (a, _) in pieces):
+                H0 = e.row0_heights()
+                e.sync()
+        e0 = self.engines[0]
+        dev = e0.buf.device
+        if isinstance(self.comm, DistComm):
+            dist = self.comm.dist
+            grp = self.comm.group
+            segs_all = [None] * self.comm.world
+            dist.all_gather_object(segs_all, [s for (_, _, segs) in local for s in segs], group=grp)
+            P1l = torch.cat([p for (p, _, _) in local]).to(dev)
+            Dl = torch.cat([d for (_, d, _) in local]).to(dev)
+            nmax = max(len(x) for x in segs_all)
+            pad = lambda t: torch.cat([t, torch.zeros((nmax - t.shape[0], pl.L), dtype=t.dtype, device=dev)])  # noqa: E731
+            P1g = [torch.zeros((nmax, pl.L), dtype=torch.int32, device=dev) for _ in range(self.comm.world)]
+            Dg = [torch.zeros_like(P1g[0]) for _ in range(self.comm.world)]
+            dist.all_gather(P1g, pad(P1l), group=grp)
+            dist.all_gather(Dg, pad(Dl), group=grp)
+            h0 = H0 if H0 is not None else torch.zeros(pl.L, dtype=torch.int32, device=dev)
+            dist.all_reduce(h0, group=grp)
+            H0 = h0
+            p2 = torch.tensor([P2], dtype=torch.int64, device=dev)
+            dist.all_reduce(p2, group=grp)
+            P2 = int(p2.item())
+            entries = [(segs_all[r][i], P1g[r][i], Dg[r][i]) for r in range(self.comm.world)
+                       for i in range(len(segs_all[r]))]
+        else:
+            entries = [(segs[i], P1[i].to(dev), D[i].to(dev)) for (P1, D, segs) in local for i in range(len(segs))]
+        entries.sort(key=lambda t: t[0][0])
+        P1c = torch.stack([t[1] for t in entries]).contiguous()
+        Dc = torch.stack([t[2] for t in entries]).contiguous()
+        seglen = torch.tensor([t[0][1] for t in entries], dtype=torch.int32, device=dev)
+        s, s2 = e0.combine(H0.to(dev).contiguous(), P1c, Dc, seglen)
+        return s, s2 + P2
+
+    def interface_width(self) -> float:
+        s, s2 = self.width_sums()
+        n = float(self.plan.L * self.plan.L)  # kpz.cpp:78-80
+        mean = s / n
+        return s2 / n - mean * mean
