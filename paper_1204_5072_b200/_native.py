@@ -118,6 +118,14 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_set_stream", P, P)
     _sig(L, "lfg_kpz_synchronize", P)
     _sig(L, "lfg_kpz_device_spins", P, I32, C.POINTER(P), C.POINTER(SZ))
+    # strip-sharded path
+    _sig(L, "lfg_kpz_create_strip", C.POINTER(P), I32, D, D, U64, C.POINTER(KpzPlan), I32)
+    _sig(L, "lfg_kpz_sweep_origin", I32, C.POINTER(KpzPlan), U64, U64, C.POINTER(I32))
+    _sig(L, "lfg_kpz_strip_phase", P, P, I32, I32, I32, U64, I32)
+    _sig(L, "lfg_kpz_strip_fill", P, P, I32, I32, I32, I32)
+    _sig(L, "lfg_kpz_strip_row0_heights", P, P, I32, P)
+    _sig(L, "lfg_kpz_strip_width_partials", P, P, I32, I32, I32, I32, P, P, P)
+    _sig(L, "lfg_kpz_width_combine", P, P, P, P, P, I32, C.POINTER(I64), C.POINTER(I64))
     _bind_kmc(L)
     _lib = L
     return L

@@ -206,7 +206,8 @@ class CudaStripEngine:
 def sweep_origin(plan: StripPlan, seed: int, sweep: int):
     out = (C.c_int32 * 6)()
     kp = _native.KpzPlan(plan.bx, plan.by)
-    _native.check(_native.lib().lfg_kpz_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep), out))
+    _native.check(_native.lib().lfg_kpz_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep),
+                                                     C.cast(out, C.POINTER(C.c_int32))))
     return int(out[0]), int(out[1]), [int(out[2 + k]) for k in range(4)]
 
 

@@ -85,3 +85,14 @@ def test_header_compiles_as_c():
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-c", "-I", os.path.join(ROOT, "include"), tmp,
                         "-o", "/tmp/lfg_hdr_test.o"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_sweep_origin_matches_oracle(native, oracle):
+    # host-side DTr draws of the C ABI (used by the sharded driver) == oracle restatement
+    from paper_1204_5072_b200.shard import StripPlan, sweep_origin
+
+    for (L, bx, by) in ((2048, 1024, 128), (256, 64, 32), (1 << 16, 1024, 128)):
+        pl = StripPlan(L, 1, bx, by)
+        for s in range(20):
+            ox, oy, sets = sweep_origin(pl, 12345, s)
+            assert [ox, oy, *sets] == oracle.kpz_sweep_draw(L, bx, by, 12345, s).tolist()
