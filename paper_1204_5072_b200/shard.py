@@ -359,6 +359,10 @@ class ShardedKpz:
         import torch
 
         pl = self.plan
+        # each piece's first segment reads the row below it (s_y of its first
+        # row): bring both ghost rows up to date first
+        for sy in (0, 1):
+            self._exchange(lambda r: pl.ghost(self.oy, r, sy))
         S = 2048 if pl.L >= 4096 else max(1, min(pl.L, 128))
         local = []
         H0 = None
