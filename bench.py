@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kmc", action="store_true")
     return ap.parse_args()
 
 
@@ -140,47 +141,63 @@ def flat_words(L):
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def reference_sample(L, p, q, seconds, threads):
-    """Time the reference's own kpz_sweep_sequential loop body (oracle/_ref =
-    the unmodified reference sources) on `threads` host threads, one
-    independent replica each (the reference has no parallel sweep)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-    import pyoracle
+class ReferenceReplicas:
+    """`threads` independent reference lattices (oracle/_ref = the unmodified
+    reference sources; the reference has no parallel sweep), each a persistent
+    lf::SlopeField so timed samples exclude host copies (SPEC.md:454)."""
 
-    ref = pyoracle.try_ref()
-    kind = "reference"
-    if ref is None:
-        raise RuntimeError("oracle/_ref/liblfref.so missing: build it where /root/reference exists")
-    x0, y0 = flat_words(L)
-    fields = [ref.kpz_field(L, x0, y0) for _ in range(threads)]
-    del x0, y0
-    # calibrate on one thread (warms the replica's pages and caches)
-    n_cal = 1 << 22
-    t = time.perf_counter()
-    fields[0].attempts(p, q, "lcg64", 1, n_cal)
-    rate1 = n_cal / (time.perf_counter() - t)
-    n = max(n_cal, int(rate1 * seconds))
-    results = [None] * threads
+    def __init__(self, L, p, q, threads):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
 
-    def work(r):
+        self.ref = pyoracle.try_ref()
+        if self.ref is None:
+            raise RuntimeError("oracle/_ref/liblfref.so missing: build it where /root/reference exists")
+        self.L, self.p, self.q, self.threads = L, p, q, threads
+        x0, y0 = flat_words(L)
+        self.fields = [self.ref.kpz_field(L, x0, y0) for _ in range(threads)]
+        self.state = [1 + r for r in range(threads)]
+        self.rate1 = None
+
+    def calibrate(self, n=1 << 21):
+        t = time.perf_counter()
+        _, self.state[0] = self.fields[0].attempts(self.p, self.q, "lcg64", self.state[0], n)
+        self.rate1 = n / (time.perf_counter() - t)
+        return self.rate1
+
+    def sample(self, seconds):
+        if self.rate1 is None:
+            self.calibrate()
+        n = max(1 << 20, int(self.rate1 * seconds))
+
+        def work(r):
+            _, self.state[r] = self.fields[r].attempts(self.p, self.q, "lcg64", self.state[r], n)
+
+        ths = [threading.Thread(target=work, args=(r,)) for r in range(self.threads)]
         t0 = time.perf_counter()
-        fields[r].attempts(p, q, "lcg64", 1 + r, n)
-        results[r] = time.perf_counter() - t0
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        wall = time.perf_counter() - t0
+        return self.threads * n / (wall * 1e9), n, wall
 
-    ths = [threading.Thread(target=work, args=(r,)) for r in range(threads)]
-    t0 = time.perf_counter()
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    wall = time.perf_counter() - t0
-    for fl in fields:
-        fl.close()
-    agg = threads * n / (wall * 1e9)
-    return {"value": agg, "unit": "attempts/ns", "cores": threads, "kind": kind,
-            "sample": f"{n} attempts of kpz_sweep_sequential's loop (kpz.cpp:12-16) per thread on a flat "
-                      f"L={L} lattice (1 GiB/replica), {threads} independent replicas, wall {wall:.1f}s"}
+    def close(self):
+        for f in self.fields:
+            f.close()
+
+    def describe(self, n, wall):
+        return (f"{n} attempts of kpz_sweep_sequential's loop (kpz.cpp:12-16) per thread on a flat L={self.L} "
+                f"lattice (1 GiB/replica), {self.threads} independent replicas, wall {wall:.1f}s")
+
+
+def reference_sample(L, p, q, seconds, threads):
+    rr = ReferenceReplicas(L, p, q, threads)
+    try:
+        v, n, wall = rr.sample(seconds)
+        return {"value": v, "unit": "attempts/ns", "cores": threads, "kind": "reference", "sample": rr.describe(n, wall)}
+    finally:
+        rr.close()
 
 
 def cpu_threads_for(L):
@@ -201,23 +218,53 @@ def run_reference(args):
     if rank != 0:
         return
     threads = cpu_threads_for(args.L)
-    per_step = []
-    cb = None
+    rr = ReferenceReplicas(args.L, args.p, args.q, threads)
+    rr.calibrate()
+    step_s = max(1.0, min(4.0, 150.0 / max(1, args.warmup + args.steps)))
+    vals = []
+    n = wall = 0
     for s in range(args.warmup + args.steps):
-        r = reference_sample(args.L, args.p, args.q, max(2.0, args.cpu_seconds / 4), threads)
+        v, n, wall = rr.sample(step_s)
         if s >= args.warmup:
-            per_step.append(r["value"])
-            cb = r
-    v = statistics.median(per_step)
+            vals.append(v)
+    rr.close()
+    v = statistics.median(vals)
     ncpu, model = host_info()
     line = {"metric": METRIC, "value": v, "unit": "attempts/ns", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic (flat start)",
-            "config": {"workload": f"KPZ octahedron, L={args.L}, p={args.p}, q={args.q}, flat start",
+            "config": {"workload": f"KPZ octahedron, L={args.L}, p={args.p}, q={args.q}, flat start; reference "
+                                   f"random-sequential sweep (lf::kpz_sweep_sequential), bounded sample per step",
                        "cpu_model": model, "nproc": ncpu},
-            "cpu_baseline": {**cb, "value": v},
+            "cpu_baseline": {"value": v, "unit": "attempts/ns", "cores": threads, "kind": "reference",
+                             "sample": rr.describe(n, wall)},
             "e2e": {"value": v, "unit": "attempts/ns", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
+    """BASELINE configs[3]: 3-D fcc binary alloy, 256^3 sc, c = 0.5, eps = 1.5,
+    both species active; one step = one MCS (L^3/2 attempts)."""
+    out = {}
+    for both in (True, False):
+        k = lfg.KmcLattice(L, 1.5, both, 7)
+        k.set_stream(stream.cuda_stream)
+        k.make_random_alloy(0.5, 3)
+        k.sweep_async(warmup)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        k.sweep_async(steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        out["both" if both else "b_only"] = {"value": (L ** 3 // 2) * steps / (ms * 1e6), "unit": "attempts/ns",
+                                             "ms_per_mcs": ms / steps, "open_bonds": k.open_bonds_per_particle()}
+        k.close()
+    out["config"] = f"KMC fcc binary alloy {L}^3 sc, c=0.5, eps=1.5, DT blocks 32^3 (BASELINE.json configs[3])"
+    out["note"] = ("L2-resident (2 MiB); only L^3/4096 tiles are active per single-hit round, so the 256^3 "
+                   "case is latency-bound by construction")
+    return out
 
 
 def run_b200(args):
@@ -226,17 +273,19 @@ def run_b200(args):
     import paper_1204_5072_b200 as lfg
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # several ranks may share one GPU (gloo tests)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LFG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     L = args.L
     stream = torch.cuda.current_stream()
-    k = lfg.KpzLattice(L, args.p, args.q, args.seed + rank, device=local)
-    k.set_stream(stream.cuda_stream)
-    k.make_flat_slopes()
     attempts_per_step = L * L
 
     def barrier():
@@ -244,17 +293,36 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up
-    k.sweep_async(args.warmup)
+    peak, peak_kind = measured_peaks()
+    if world == 1:
+        k = lfg.KpzLattice(L, args.p, args.q, args.seed, device=local)
+        k.set_stream(stream.cuda_stream)
+        k.make_flat_slopes()
+        plan = k.plan
+        run = lambda n: k.sweep_async(n)  # noqa: E731
+        mode = "1 GPU"
+    else:
+        from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, ShardedKpz, StripPlan
+
+        bx, by = min(1024, L // 2), min(128, L // 2)
+        plan = (bx, by)
+        pl = StripPlan(L, world, bx, by)
+        eng = CudaStripEngine(pl, args.p, args.q, args.seed, local)
+        sk = ShardedKpz(pl, args.seed, [eng], [rank], DistComm(eng))
+        sk.make_flat_slopes()
+        stream = eng.stream
+        run = sk.sweep
+        mode = f"strip-sharded x{world} (rows rolled per sweep, one ghost row per phase, {dist.get_backend()})"
+
+    run(args.warmup)
     barrier()
-    # timed region
     clocks = ClockSampler(local)
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
-    k.sweep_async(args.steps)
+    run(args.steps)
     e1.record(stream)
     barrier()
     clk = clocks.stop()
@@ -263,46 +331,44 @@ def run_b200(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * attempts_per_step * args.steps / (ms * 1e6)  # attempts/ns, whole job
-    c = k.counters()
+    value = attempts_per_step * args.steps / (ms * 1e6)  # attempts/ns, whole job (fixed L: strong scaling)
 
-    # dominant kernel: per-launch event timing of the phase kernel on the same stream
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
-    s0 = k.sweep_index
-    for i, (a, b) in enumerate(ev):
-        a.record(stream)
-        k.phase(s0 + i // 4, i % 4)
-        b.record(stream)
-    k.sweep_index = s0 + 2
-    torch.cuda.synchronize()
-    launch_ms = [a.elapsed_time(b) for a, b in ev]
-    avg_launch_ms = statistics.mean(launch_ms)
-    peak, peak_kind = measured_peaks()
-    bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / 4
-    achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            traffic = json.load(f).get("kpz_dtr_phase", {}).get("dram_bytes_per_launch")
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_kind,
-                "kernel": "kpz_dtr_phase_kernel", "avg_launch_ms": avg_launch_ms,
-                "alg_bytes_per_launch": bytes_per_launch,
-                "note": "algorithmic bytes = 0.5 B/attempt (two 1-bit slope planes read+written once per "
-                        "MCS, SURVEY.md §8(d)); the device stores 1 spin bit per site, so actual HBM "
-                        "traffic is about half of that; the kernel is issue/SMEM bound, not HBM bound"}
+    # dominant kernel: event-timed phase launches on the launching stream
+    roofline = None
+    if world == 1:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
+        s0 = k.sweep_index
+        for i, (a, b) in enumerate(ev):
+            a.record(stream)
+            k.phase(s0 + i // 4, i % 4)
+            b.record(stream)
+        k.sweep_index = s0 + 2
+        torch.cuda.synchronize()
+        avg_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / 4
+        achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+                traffic = json.load(f).get("kpz_dtr_phase", {}).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "peak_source": peak_kind, "kernel": "kpz_dtr_phase_kernel",
+                    "avg_launch_ms": avg_launch_ms, "alg_bytes_per_launch": bytes_per_launch,
+                    "binding_unit": "SM issue / ALU pipe (profiles/r01_kpz_ncu.txt: issue 73%, ALU 58%, DRAM 3%)",
+                    "note": "algorithmic bytes = 0.5 B/attempt (two 1-bit slope planes read+written once per MCS, "
+                            "SURVEY.md §8(d)); the device keeps 1 spin bit per site; the faithful single-hit "
+                            "DTr kernel is issue-bound, not HBM-bound (DESIGN.md §4.1)"}
 
-    # end-to-end through the public API with host buffers (rank-local)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and world == 1:
         import numpy as np
 
         x0, y0 = flat_words(L)
         hx = torch.from_numpy(x0.view(np.int64)).pin_memory()
         hy = torch.from_numpy(y0.view(np.int64)).pin_memory()
-        ke = lfg.KpzLattice(L, args.p, args.q, args.seed + 1000 + rank, device=local)
+        ke = lfg.KpzLattice(L, args.p, args.q, args.seed + 1000, device=local)
         ke.upload_ptr(hx.data_ptr(), hy.data_ptr())
         ke.sweep(1)
         ke.download_ptr(hx.data_ptr(), hy.data_ptr())
@@ -315,16 +381,33 @@ def run_b200(args):
             ke.download_ptr(hx.data_ptr(), hy.data_ptr())     # device -> host SlopeField
         barrier()
         dt = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([dt], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
-        e2e = {"value": world * attempts_per_step * args.e2e_steps / (dt * 1e9), "unit": "attempts/ns",
+        e2e = {"value": attempts_per_step * args.e2e_steps / (dt * 1e9), "unit": "attempts/ns",
                "h2d_bytes_per_step": 2 * L * L // 8, "d2h_bytes_per_step": 2 * L * L // 8 + 24 + 32,
                "steps": args.e2e_steps,
                "step": "lfg_kpz_upload(host SlopeField planes, pinned) + lfg_kpz_sweep(1 MCS) + "
                        "lfg_kpz_interface_width + lfg_kpz_download", "w2_last": w2}
         ke.close()
+    elif not args.no_e2e:
+        # sharded: each rank moves its strip (spin rows) host<->device around one MCS + distributed W^2
+        hbuf = torch.empty_like(eng.buf, device="cpu").pin_memory()
+        hbuf.copy_(eng.buf)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            eng.buf.copy_(hbuf, non_blocking=True)
+            sk.sweep(1)
+            w2 = sk.interface_width()
+            hbuf.copy_(eng.buf)
+        barrier()
+        dt = time.perf_counter() - t0
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        nbytes = eng.buf.numel() * 4 * world
+        e2e = {"value": attempts_per_step * args.e2e_steps / (dt * 1e9), "unit": "attempts/ns",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 16, "steps": args.e2e_steps,
+               "step": "per rank: strip ring buffer host->device, 1 MCS, distributed W^2, device->host",
+               "w2_last": w2}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -333,21 +416,26 @@ def run_b200(args):
         except Exception as ex:  # reported, not fatal
             cpu = {"value": None, "unit": "attempts/ns", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+    kmc = None
+    if rank == 0 and world == 1 and not args.no_kmc:
+        kmc = kmc_measure(lfg, torch, stream, steps=20, warmup=3)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "attempts/ns", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (flat start)",
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (flat start)",
                 "config": {"workload": f"KPZ octahedron DTr, L={L}x{L}, p={args.p}, q={args.q}, flat start, "
                                        f"1 MCS per step (BASELINE.json configs[1])",
-                           "plan": {"block_x": k.plan[0], "block_y": k.plan[1], "domain": "16x8"},
-                           "parallelism": f"replica-per-GPU x{world}" if world > 1 else "1 GPU",
-                           "l2": "lattice 512 MiB >> 126 MB L2: no flush needed",
-                           "successes_per_step": c.successes / max(1, c.attempts // attempts_per_step)},
+                           "plan": {"block_x": plan[0], "block_y": plan[1], "domain": "16x8"},
+                           "parallelism": mode,
+                           "l2": "lattice 512 MiB >> 126 MB L2: no flush needed"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": 4 * args.steps}
+                "gpu_launches": 4 * args.steps, "kmc": kmc}
         print(json.dumps(line), flush=True)
-    k.close()
+    if world == 1:
+        k.close()
+    else:
+        eng.close()
     if dist is not None:
         dist.destroy_process_group()
 

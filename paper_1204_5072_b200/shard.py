@@ -243,19 +243,30 @@ class DistComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves CPU tensors only: device rows are staged through host
+        # memory (used to exercise the distributed path with several ranks on
+        # one GPU); NCCL sends device rows directly over NVLink.
+        self.stage = dist.get_backend(group) == "gloo" and getattr(engine.buf, "is_cuda", False)
 
     def exchange(self, ops):
         dist = self.dist
         e = self.engine
         e.sync()
-        p2p = []
+        p2p, unstage = [], []
         for kind, peer, b, n in ops:
             for (slot, m) in e.plan.pieces(b, n):
                 t = e.rows(slot, m)
+                if self.stage:
+                    h = t.cpu() if kind == "send" else t.new_empty(t.shape, device="cpu")
+                    if kind == "recv":
+                        unstage.append((t, h))
+                    t = h
                 p2p.append(dist.P2POp(dist.isend if kind == "send" else dist.irecv, t, peer, self.group))
         if p2p:
             for w in dist.batch_isend_irecv(p2p):
                 w.wait()
+        for t, h in unstage:
+            t.copy_(h)
         if hasattr(e, "torch") and e.buf.is_cuda:
             e.torch.cuda.current_stream(e.buf.device).synchronize()
 
@@ -341,7 +352,7 @@ class ShardedKpz:
                     y += m
         if isinstance(self.comm, DistComm):
             dist = self.comm.dist
-            dev = self.engines[0].buf.device
+            dev = "cpu" if self.comm.stage else self.engines[0].buf.device
             t = out.to(dev)
             # rows are disjoint across ranks: XOR-free sum of int32 words is exact
             # only without overflow, so reduce as int64 halves
@@ -381,6 +392,9 @@ class ShardedKpz:
         if isinstance(self.comm, DistComm):
             dist = self.comm.dist
             grp = self.comm.group
+            if self.comm.stage:
+                dev = torch.device("cpu")
+                H0 = H0.cpu() if H0 is not None else None
             segs_all = [None] * self.comm.world
             dist.all_gather_object(segs_all, [s for (_, _, segs) in local for s in segs], group=grp)
             P1l = torch.cat([p for (p, _, _) in local]).to(dev)
@@ -402,10 +416,11 @@ class ShardedKpz:
         else:
             entries = [(segs[i], P1[i].to(dev), D[i].to(dev)) for (P1, D, segs) in local for i in range(len(segs))]
         entries.sort(key=lambda t: t[0][0])
-        P1c = torch.stack([t[1] for t in entries]).contiguous()
-        Dc = torch.stack([t[2] for t in entries]).contiguous()
-        seglen = torch.tensor([t[0][1] for t in entries], dtype=torch.int32, device=dev)
-        s, s2 = e0.combine(H0.to(dev).contiguous(), P1c, Dc, seglen)
+        cdev = e0.buf.device
+        P1c = torch.stack([t[1] for t in entries]).to(cdev).contiguous()
+        Dc = torch.stack([t[2] for t in entries]).to(cdev).contiguous()
+        seglen = torch.tensor([t[0][1] for t in entries], dtype=torch.int32, device=cdev)
+        s, s2 = e0.combine(H0.to(cdev).contiguous(), P1c, Dc, seglen)
         return s, s2 + P2
 
     def interface_width(self) -> float:

@@ -4,7 +4,7 @@
 #   stages: comma list of test,smoke,bench,launches,ncu (default: all)
 set -u
 TAG=${1:-r01}
-STAGES=${2:-test,smoke,bench,launches,ncu}
+STAGES=${2:-test,smoke,bench,dist,launches,ncu}
 OUT=gpurun_out/$TAG
 mkdir -p "$OUT"
 has() { [[ ",$STAGES," == *",$1,"* ]]; }
@@ -27,6 +27,12 @@ fi
 if has bench; then
   timeout 900 python bench.py --steps 20 --warmup 3 > "$OUT/bench.json" 2> "$OUT/bench.err"
   echo "bench exit $?" >> "$OUT/bench.err"
+fi
+if has dist; then
+  LFG_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+      --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 2 --L 4096 --steps 3 --warmup 1 \
+      --no-kmc --no-cpu-baseline > "$OUT/dist2_gloo.json" 2> "$OUT/dist2_gloo.err"
+  echo "dist exit $?" >> "$OUT/dist2_gloo.err"
 fi
 if has launches; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv \
