@@ -27,11 +27,11 @@ namespace lfg {
 
 // ============================================================ DTr phase kernel
 // One CTA = one active device block (bx x by sites) of one replica.
-// Threads: 32 lanes x (by/16/NT) warps; lane = tile column (bx/32 lanes
-// active), warp w owns tile rows w + n*(by/16/NT), n < NT (NT tiles per lane,
+// Threads: 32 lanes x NW warps, NW = by / (16 NT); lane = tile column (bx/32
+// lanes active), warp w owns tile rows w + n*NW, n < NT (NT tiles per lane,
 // so the per-round dispatch, barrier and loop are shared by NT independent
-// attempts).  Shared-memory layout (32-bit words, 256-byte lines):
-//   line 0, words 0..31     : spare (set draws live in uniform registers)
+// attempts).  Shared-memory layout (32-bit words, 256-byte lines, line 0 at
+// a 2 KB-aligned shared-window address A):
 //   line R+8, word s        : staged spins of block row R (R = -1 .. by),
 //                             s = 0..Wt-1 tile words, s = Wt the right halo
 //                             word (H_R); the left halo word (H_L) of row R
@@ -39,7 +39,11 @@ namespace lfg {
 // With a 64-word line stride every tile column owns one bank for all its
 // rows, so the per-round gathers (own/up/down words) are conflict-free, and
 // the neighbour-word gather is a lane rotation that lands the block's edge
-// lanes exactly on H_L (bank 31) / H_R (bank Wt).
+// lanes exactly on H_L (bank 31) / H_R (bank Wt).  Lines 0..5 are never
+// touched, so A may sit up to 1.5 KB below the dynamic-smem base; the 2 KB
+// alignment makes "tile row base | anchor row * 256" a single LOP3 and keeps
+// every anchor address in one ordinary register (no per-round re-derivation
+// of the shared window base).
 __device__ __forceinline__ int sm_slot(int R, int s) {
     return s < 0 ? (R + 7) * 64 + 63 : (R + 8) * 64 + s;
 }
@@ -52,8 +56,7 @@ __device__ __forceinline__ void count_if_nonzero(uint32_t& n, uint32_t v) {
     asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(n) : "r"(v));
 }
 
-// 32-bit shared-window addressing (avoids re-deriving the generic->shared
-// window base every round).  volatile keeps program order w.r.t. barriers.
+// 32-bit shared-window addressing.  volatile keeps program order w.r.t. barriers.
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -71,9 +74,73 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
     return d;
 }
 
+// ---- TMA bulk copies (cp.async.bulk, global -> shared, mbarrier completion)
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity0(uint32_t mbar) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], 0;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(mbar)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+// FMA-pipe integer ops (IMAD.HI / IMAD / IMAD.SHL), kept as such so that the
+// ALU pipe (LOP3/SHF, half rate per SMSP) only carries the pattern logic.
+__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t mullo_u32(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+#ifndef LFG_KPZ_HALFSHIFT
+#define LFG_KPZ_HALFSHIFT 0
+#endif
+#ifndef LFG_KPZ_LUT
+#define LFG_KPZ_LUT 0
+#endif
+#ifndef LFG_KPZ_IMADDR
+#define LFG_KPZ_IMADDR 0
+#endif
+#ifndef LFG_KPZ_SWITCH
+#define LFG_KPZ_SWITCH 0
+#endif
+
+template <bool MW>
+__device__ __forceinline__ void round_barrier() {
+    if (MW) __syncthreads();
+    else __syncwarp();
+}
+
 // One single-hit round of the NT tiles a lane owns, active domain (HX, HY).
-//   addr      : byte offset of each anchor row's tile word (row j); HY adds 8
-//               rows (2048 bytes)
+//   addr      : shared address of each anchor row's tile word (row j of the
+//               tile's top half); HY adds 8 rows (2048 bytes, an immediate)
 //   own/up/dn : spin words of rows j, j+1, j-1 (same tile column, same bank)
 //   nb        : the neighbouring tile word on the crossing side (left for the
 //               hx=0 half, right for hx=1); funnel shifts bring f(i-1) and
@@ -84,23 +151,40 @@ __device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
 // of all tiles are issued before any store (the tiles are disjoint rows), so
 // the NT dependency chains overlap.
 template <int HX, int HY, bool GENERAL, int NT>
-__device__ __forceinline__ void kpz_attempt_tiles(uint32_t smb, const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
+__device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
                                                   uint32_t& ndep, uint32_t& ndet) {
     uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
+#if LFG_KPZ_LUT
+    uint32_t bitw[NT];
+#endif
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
-        const uint32_t pw = smb + addr[n] + (HY << 11);
+        const uint32_t pw = addr[n] + (HY << 11);
         own[n] = lds32(pw);
-        nb[n] = lds32(pw + (HX ? 4 : -4));
+        nb[n] = lds32(HX ? pw + 4u : pw - 4u);
         up[n] = lds32(pw + 256);
         dn[n] = lds32(pw - 256);
+#if LFG_KPZ_LUT
+        bitw[n] = lds32(xd[n] + (HX << 6));  // xd holds the LUT address of 1 << xd
+#endif
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
+#if LFG_KPZ_HALFSHIFT
+        // Only the active half's 16 bits matter: the shift towards the inside of
+        // the word needs no neighbour bit and runs on the FMA pipe.
+        const uint32_t Rw = HX ? __funnelshift_r(own[n], nb[n], 1) : mulhi_u32(own[n], 0x80000000u);
+        const uint32_t Lw = HX ? mullo_u32(own[n], 2u) : __funnelshift_l(nb[n], own[n], 1);
+#else
         const uint32_t Rw = __funnelshift_r(own[n], nb[n], 1);  // bit i = f(i+1)
         const uint32_t Lw = __funnelshift_l(nb[n], own[n], 1);  // bit i = f(i-1)
+#endif
+#if LFG_KPZ_LUT
+        const uint32_t bit = bitw[n];
+#else
         const uint32_t bit = (HX ? 0x10000u : 1u) << xd[n];
+#endif
         if (!GENERAL) {
             const uint32_t flip = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), bit);
             res[n] = own[n] ^ flip;
@@ -116,7 +200,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(uint32_t smb, const uint32_t (
         }
     }
 #pragma unroll
-    for (int n = 0; n < NT; ++n) sts32(smb + addr[n] + (HY << 11), res[n]);
+    for (int n = 0; n < NT; ++n) sts32(addr[n] + (HY << 11), res[n]);
 }
 
 // Inner single-hit rounds of one block activation.  The inner set of each
@@ -129,11 +213,11 @@ __device__ __forceinline__ void kpz_attempt_tiles(uint32_t smb, const uint32_t (
 // binds this kernel -- which also makes the loop body position-independent,
 // so only 4 rounds are unrolled (small I-cache footprint).  lane_base has
 // bits 8..10 clear, so the row offset yd*256 merges with one LOP3.
-template <bool GENERAL, bool FULL, int NT>
-__device__ __forceinline__ void kpz_block_rounds(uint32_t smb, const uint32_t (&lane_base)[NT], bool active,
-                                                 uint64_t seed, uint64_t sweep, uint32_t block_id,
-                                                 const uint32_t (&tile_id)[NT], uint64_t thrP, uint64_t thrQ,
-                                                 uint32_t& ndep, uint32_t& ndet) {
+template <bool GENERAL, bool FULL, int NT, bool MW>
+__device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT], bool active, uint64_t seed,
+                                                 uint64_t sweep, uint32_t block_id, const uint32_t (&tile_id)[NT],
+                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet,
+                                                 uint32_t lut) {
 #pragma unroll 1
     for (int m4 = 0; m4 < kRounds / 64; ++m4) {
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
@@ -165,30 +249,51 @@ __device__ __forceinline__ void kpz_block_rounds(uint32_t smb, const uint32_t (&
                         uint32_t addr[NT], xd[NT], u[NT];
 #pragma unroll
                         for (int n = 0; n < NT; ++n) {
+#if LFG_KPZ_LUT
+                            xd[n] = mad_u32(mulhi_u32(xw[n], 16u), 4u, lut);  // LUT address of 1 << field
+#else
                             xd[n] = __umulhi(xw[n], 16u);  // top 4 bits, then advance
-                            xw[n] *= 16u;
+#endif
+                            xw[n] = mullo_u32(xw[n], 16u);
+#if LFG_KPZ_IMADDR
+                            // row field at the top of yw: address = field * 256 + base (FMA pipe)
+                            addr[n] = mad_u32(mulhi_u32(yw[n], 8u), 256u, lane_base[n]);
+                            yw[n] = mullo_u32(yw[n], 8u);
+#else
                             // row field k of this quarter -> bits 8..10 (bits above masked by the LOP3)
                             addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u << (3 * k)), 0x700u);
+#endif
                             u[n] = GENERAL ? sel4(Uw[n], k) : 0u;
                         }
                         if (FULL || active) {
+#if LFG_KPZ_SWITCH
+                            switch (setw & 3u) {
+                                case 0: kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
+                                case 1: kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
+                                case 2: kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
+                                default: kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
+                            }
+#else
                             if (setw & 2u) {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
                                 else
-                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
                             } else {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
                                 else
-                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(smb, addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
                             }
+#endif
                         }
                         setw >>= 2;
-                        __syncthreads();
+                        round_barrier<MW>();
                     }
+#if !LFG_KPZ_IMADDR
 #pragma unroll
                     for (int n = 0; n < NT; ++n) yw[n] <<= 12;  // next 4 row fields
+#endif
                 }
             }
         }
@@ -196,18 +301,22 @@ __device__ __forceinline__ void kpz_block_rounds(uint32_t smb, const uint32_t (&
 }
 
 #ifndef LFG_KPZ_NT
-#define LFG_KPZ_NT 2  // tiles per lane for block_y >= 32
-#endif
-#ifndef LFG_KPZ_MIN_BLOCKS
-#define LFG_KPZ_MIN_BLOCKS 6
+#define LFG_KPZ_NT 2  // max tiles per lane (by >= 16 NT); measured best on B200 (NT=4: fewer warps, slower)
 #endif
 
-template <bool GENERAL, bool FULL, int kNT>
-__global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
+// Dynamic shared memory: lines 6 .. by+8 relative to the 2 KB-aligned origin
+// A = ceil_2048(base - 1536), which lies at most 511 bytes above base - 1536.
+size_t kpz_phase_smem_bytes(int by) { return size_t(by + 9) * 256 + 512; }
+
+template <bool GENERAL, bool FULL, int kNT, bool MW>
+__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
     kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
-    extern __shared__ __align__(16) uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm_raw[];
+    const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
+    const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;  // shared address of line 0
+    uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);  // generic pointer to line 0 (lines < 6 unused)
     const int L = a.L, Lm = L - 1, wpr = L >> 5, wmask = wpr - 1;
-    const int Wt = a.bx >> 5, Ty = a.by >> 4;
+    const int Wt = a.bx >> 5;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     const int rep = a.rep0 + int(blockIdx.z);
     const uint64_t seed = a.seeds[blockIdx.z];
@@ -229,28 +338,41 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
 
     // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin
     // away (slot s of row R <- global bits [X0 + 32 s, X0 + 32 s + 32)).
-    if (FULL) {  // Wt == 32: lane k loads word w0+k, neighbours come by shuffle
-        constexpr int RB = 8;  // rows in flight per warp
-        for (int R0 = warp - 1; R0 <= a.by; R0 += RB * nwarps) {
-            uint32_t v0[RB], v1[RB];
-#pragma unroll
-            for (int t = 0; t < RB; ++t) {
-                const int R = R0 + t * nwarps;
-                const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
-                v0[t] = R <= a.by ? __ldg(row + ((w0 + lane) & wmask)) : 0u;
-                v1[t] = (R <= a.by && lane < 3) ? __ldg(row + ((w0 + 32 + lane) & wmask)) : 0u;
+    if (FULL) {
+        // Wt == 32 (so L >= 2048 and a row has >= 64 words).  Raw words
+        // [a0, a0 + 40) (a0 = w0 rounded down to 16 bytes) of every staged row
+        // land at words 0..39 of the row's own line by cp.async.bulk (split in
+        // two where the block wraps around x = L), all rows in flight at once
+        // against one mbarrier; each warp then funnel-shifts its rows in place
+        // (all reads of a row before any of its writes; slot -1 goes to word 63
+        // of the previous line, which no raw copy touches).
+        const uint32_t mbar = smA + 6 * 256;  // line 6, word 0 (lines < 7 hold no row data)
+        const int a0 = w0 & ~3, m = w0 & 3;
+        const int n1 = min(40, wpr - a0);  // words before the x wrap (a multiple of 4)
+        const uint32_t rows = uint32_t(a.by + 2);
+        if (threadIdx.x == 0) {
+            mbar_init(mbar, 1);
+            mbar_arrive_expect_tx(mbar, rows * 160u);
+        }
+        __syncthreads();
+        for (int R = int(threadIdx.x) - 1; R <= a.by; R += int(blockDim.x)) {
+            const uint32_t* row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
+            const uint32_t dst = smA + uint32_t(R + 8) * 256u;
+            bulk_g2s(dst, row + a0, uint32_t(n1) * 4u, mbar);
+            if (n1 < 40) bulk_g2s(dst + uint32_t(n1) * 4u, row, uint32_t(40 - n1) * 4u, mbar);
+        }
+        mbar_wait_parity0(mbar);
+        for (int R = warp - 1; R <= a.by; R += nwarps) {
+            const uint32_t* line = sm + (R + 8) * 64;
+            const uint32_t lo = line[m + lane + 1], hi = line[m + lane + 2];
+            uint32_t elo = 0, ehi = 0;  // lane 0: slot -1, lane 1: slot 32
+            if (lane < 2) {
+                elo = line[m + 33 * lane];
+                ehi = line[m + 33 * lane + 1];
             }
-#pragma unroll
-            for (int t = 0; t < RB; ++t) {
-                const int R = R0 + t * nwarps;
-                const uint32_t n0 = __shfl_down_sync(0xFFFFFFFFu, v0[t], 1);
-                const uint32_t t0 = __shfl_sync(0xFFFFFFFFu, v1[t], 0);
-                const uint32_t n1 = __shfl_down_sync(0xFFFFFFFFu, v1[t], 1);
-                if (R <= a.by) {
-                    sm[sm_slot(R, lane - 1)] = __funnelshift_r(v0[t], lane == 31 ? t0 : n0, b);
-                    if (lane < 2) sm[(R + 8) * 64 + 31 + lane] = __funnelshift_r(v1[t], n1, b);
-                }
-            }
+            __syncwarp();
+            sm[(R + 8) * 64 + lane] = __funnelshift_r(lo, hi, b);
+            if (lane < 2) sm[lane ? (R + 8) * 64 + 32 : (R + 7) * 64 + 63] = __funnelshift_r(elo, ehi, b);
         }
     } else {
         for (int R = warp - 1; R <= a.by; R += nwarps) {
@@ -262,21 +384,22 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
             }
         }
     }
+    // One-hot LUT (line 6, words 16..47, one bank per entry): lut[i] = 1 << i.
+    const uint32_t lut = smA + 6u * 256u + 64u;
+    if (LFG_KPZ_LUT && threadIdx.x < 32) sm[6 * 64 + 16 + threadIdx.x] = 1u << threadIdx.x;
     __syncthreads();
 
     const int tx = lane;
-    const int rows_per_n = Ty / kNT;
     uint32_t lane_base[kNT], tile_id[kNT];
 #pragma unroll
     for (int n = 0; n < kNT; ++n) {
-        const int ty = warp + n * rows_per_n;
-        tile_id[n] = uint32_t(byi * Ty + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
-        lane_base[n] = uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
+        const int ty = warp + n * nwarps;
+        tile_id[n] = uint32_t(byi * (a.by >> 4) + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
+        lane_base[n] = smA + uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
     }
     uint32_t ndep = 0, ndet = 0;
-    kpz_block_rounds<GENERAL, FULL, kNT>(uint32_t(__cvta_generic_to_shared(sm)), lane_base, tx < Wt, seed, sweep, block_id,
-                                         tile_id, a.thrP, a.thrQ, ndep, ndet);
-
+    kpz_block_rounds<GENERAL, FULL, kNT, MW>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP, a.thrQ,
+                                             ndep, ndet, lut);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     if (FULL) {
         for (int R = warp; R < a.by; R += nwarps) {
@@ -305,55 +428,70 @@ __global__ void __launch_bounds__(256 / kNT, LFG_KPZ_MIN_BLOCKS)
     }
 }
 
-size_t kpz_phase_smem_bytes(int by) { return size_t(by + 9) * 256; }
+// Tiles per lane for a block height: the largest NT <= LFG_KPZ_NT with by >= 16 NT.
+static int kpz_nt_for(int by) {
+    int nt = LFG_KPZ_NT;
+    while (nt > 1 && by < 16 * nt) nt >>= 1;
+    return nt;
+}
 
-template <int NT>
-static void launch_nt(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
+template <int NT, bool MW>
+static void launch_cfg(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
     const dim3 block(unsigned(32 * (b.by / 16 / NT)));
     const bool full = b.bx == 1024;
     if (b.general) {
-        if (full) kpz_dtr_phase_kernel<true, true, NT><<<grid, block, smem, st>>>(b);
-        else kpz_dtr_phase_kernel<true, false, NT><<<grid, block, smem, st>>>(b);
+        if (full) kpz_dtr_phase_kernel<true, true, NT, MW><<<grid, block, smem, st>>>(b);
+        else kpz_dtr_phase_kernel<true, false, NT, MW><<<grid, block, smem, st>>>(b);
     } else {
-        if (full) kpz_dtr_phase_kernel<false, true, NT><<<grid, block, smem, st>>>(b);
-        else kpz_dtr_phase_kernel<false, false, NT><<<grid, block, smem, st>>>(b);
+        if (full) kpz_dtr_phase_kernel<false, true, NT, MW><<<grid, block, smem, st>>>(b);
+        else kpz_dtr_phase_kernel<false, false, NT, MW><<<grid, block, smem, st>>>(b);
     }
+}
+
+template <int NT>
+static void launch_nt(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
+    if (b.by > 16 * NT) launch_cfg<NT, true>(b, grid, smem, st);
+    else launch_cfg<NT, false>(b, grid, smem, st);
 }
 
 cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st) {
     const size_t smem = kpz_phase_smem_bytes(a.by);
+    const int nt = kpz_nt_for(a.by);
     for (int r0 = 0; r0 < replicas; r0 += kMaxRepPerLaunch) {
         KpzPhaseArgs b = a;
         b.rep0 = r0;
         const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
         for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
         const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.nbrow / 2), unsigned(nr));
-        if (a.by >= 16 * LFG_KPZ_NT) launch_nt<LFG_KPZ_NT>(b, grid, smem, st);
+        if (nt >= 4) launch_nt<(LFG_KPZ_NT >= 4 ? 4 : 1)>(b, grid, smem, st);
+        else if (nt == 2) launch_nt<2>(b, grid, smem, st);
         else launch_nt<1>(b, grid, smem, st);
     }
     return cudaGetLastError();
 }
 
+template <int NT, bool MW>
+static cudaError_t attrs_cfg(int smem) {
+    const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT, MW>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT, MW>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT, MW>, at, smem);
+    return e;
+}
+
 template <int NT>
 static cudaError_t attrs_nt(int smem) {
-    cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem);
+    cudaError_t e = attrs_cfg<NT, true>(smem);
+    if (e == cudaSuccess) e = attrs_cfg<NT, false>(smem);
     return e;
 }
 
 cudaError_t kpz_phase_kernel_attrs() {
     const int smem = int(kpz_phase_smem_bytes(128));
     cudaError_t e = attrs_nt<1>(smem);
-    if (e == cudaSuccess && LFG_KPZ_NT != 1) e = attrs_nt<LFG_KPZ_NT>(smem);
+    if (e == cudaSuccess) e = attrs_nt<2>(smem);
+    if (e == cudaSuccess && LFG_KPZ_NT >= 4) e = attrs_nt<4>(smem);
     return e;
 }
 
