@@ -261,7 +261,7 @@ def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
         out["both" if both else "b_only"] = {"value": (L ** 3 // 2) * steps / (ms * 1e6), "unit": "attempts/ns",
                                              "ms_per_mcs": ms / steps, "open_bonds": k.open_bonds_per_particle()}
         k.close()
-    out["config"] = f"KMC fcc binary alloy {L}^3 sc, c=0.5, eps=1.5, DT blocks 32^3 (BASELINE.json configs[3])"
+    out["config"] = f"KMC fcc binary alloy {L}^3 sc, c=0.5, eps=1.5, DT blocks 16^3 (BASELINE.json configs[3])"
     out["note"] = ("L2-resident (2 MiB); only L^3/4096 tiles are active per single-hit round, so the 256^3 "
                    "case is latency-bound by construction")
     return out

@@ -103,7 +103,7 @@ int lfg_kmc_create(lfg_kmc** out, int32_t L, double eps, int32_t both_active, ui
             throw Error(LFG_EINVAL, "DtPlan: the KMC two-layer DT needs L >= 32 (two 16-site blocks per axis), got " +
                                         std::to_string(L));
         validate_eps(eps);
-        int32_t bk = plan && plan->block ? plan->block : (L >= 64 ? 32 : 16);
+        int32_t bk = plan && plan->block ? plan->block : 16;  // 16^3 blocks: SURVEY §7.1 (+0.03 %, z=+0.3)
         if (!(bk == 16 || bk == 32) || L % (2 * bk))
             throw Error(LFG_EINVAL, "DtPlan: block must be 16 or 32 with L % (2*block) == 0, got " +
                                         std::to_string(bk));

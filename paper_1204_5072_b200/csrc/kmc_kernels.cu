@@ -39,14 +39,18 @@ struct KmcRows {
 
 __device__ __forceinline__ int bit_at(unsigned long long row, int lx) { return int((row >> (lx + 16)) & 1ull); }
 
-// Number of B among the 12 fcc neighbours of (lx, ly, lz).
+// Number of B among the 12 fcc neighbours of (lx, ly, lz): four rows at
+// Manhattan distance 1 in (y, z) contribute bits lx-1 and lx+1, the four
+// diagonal rows bit lx.  All eight row loads depend only on the site, so the
+// two counts of an attempt (B site and A partner) issue together with the
+// occupancy loads -- one shared-memory latency per round.
 __device__ __forceinline__ int nb_count(const KmcRows& R, int lx, int ly, int lz) {
     const unsigned long long m2 = 5ull << (lx + 15);  // bits lx-1, lx+1
-    int n = __popcll(R.at(ly - 1, lz) & m2) + __popcll(R.at(ly + 1, lz) & m2) + __popcll(R.at(ly, lz - 1) & m2) +
-            __popcll(R.at(ly, lz + 1) & m2);
-    n += bit_at(R.at(ly - 1, lz - 1), lx) + bit_at(R.at(ly - 1, lz + 1), lx) + bit_at(R.at(ly + 1, lz - 1), lx) +
-         bit_at(R.at(ly + 1, lz + 1), lx);
-    return n;
+    const unsigned long long m1 = 1ull << (lx + 16);
+    return __popcll(R.at(ly - 1, lz) & m2) + __popcll(R.at(ly + 1, lz) & m2) + __popcll(R.at(ly, lz - 1) & m2) +
+           __popcll(R.at(ly, lz + 1) & m2) + __popcll(R.at(ly - 1, lz - 1) & m1) +
+           __popcll(R.at(ly - 1, lz + 1) & m1) + __popcll(R.at(ly + 1, lz - 1) & m1) +
+           __popcll(R.at(ly + 1, lz + 1) & m1);
 }
 
 __device__ __forceinline__ void global_flip(uint32_t* w, int L, int gx, int gy, int gz) {
@@ -54,9 +58,29 @@ __device__ __forceinline__ void global_flip(uint32_t* w, int L, int gx, int gy, 
     atomicXor(w + (idx >> 5), 1u << (idx & 31));
 }
 
-template <bool BOTH>
+// kFccOffsets (lattice.hpp:147-151) in closed form: group g = dir >> 2 picks
+// the two non-zero axes ((x,y), (x,z), (y,z)); bit 1 of dir negates the first,
+// bit 0 the second.  Register arithmetic instead of a divergent constant-bank
+// lookup (12 distinct addresses per warp would serialise).
+__device__ __forceinline__ void fcc_offset(int dir, int& dx, int& dy, int& dz) {
+    const int g = dir >> 2;
+    const int s1 = 1 - (dir & 2), s2 = 1 - 2 * (dir & 1);
+    dx = g == 2 ? 0 : s1;
+    dy = g == 0 ? s2 : (g == 2 ? s1 : 0);
+    dz = g == 0 ? 0 : s2;
+}
+
+// One CTA holds `bpc` device blocks of tpb = (bk/8)^3 threads (one thread per
+// 8^3 tile).  When a block fits in a warp (bk = 16: 8 threads, four blocks per
+// warp) the per-round barrier is __syncwarp; for bk = 32 one block is one CTA.
+// Per round the Philox words of the NEXT round are computed first (they do
+// not depend on the lattice), so the RNG chain overlaps the attempt's
+// shared-memory latency, and every shared load of the attempt (site,
+// partner, 2 x 8 neighbour rows) is issued before the first use.
+template <bool BOTH, bool WARP_SYNC>
 __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
     extern __shared__ __align__(16) unsigned long long smk[];
+    __shared__ unsigned long long s_thr[13];
     const int L = a.L, Lm = L - 1, bk = a.bk, E = bk + 4, rows = E * E;
     const int tb = bk / 8, tpb = tb * tb * tb;
     const int sub = int(threadIdx.x) / tpb, t = int(threadIdx.x) % tpb;
@@ -71,6 +95,7 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * bk) & Lm, Y0 = (sw.oy + byi * bk) & Lm, Z0 = (sw.oz + bzi * bk) & Lm;
     const KmcRows R{smk + size_t(sub) * rows, E};
+    if (threadIdx.x < 13) s_thr[threadIdx.x] = (uint64_t(a.thr_hi[threadIdx.x]) << 32) | a.thr_lo[threadIdx.x];
 
     // Stage the block plus a 2-site halo.
     const int wpr = L >> 5, wm = wpr - 1;
@@ -87,47 +112,165 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     const int tx = t % tb, ty = (t / tb) % tb, tz = t / (tb * tb);
     const uint32_t tl = uint32_t(L / 8);
     const uint32_t tile_id = (uint32_t(bzi * tb + tz) * tl + uint32_t(byi * tb + ty)) * tl + uint32_t(bxi * tb + tx);
+    const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;  // parity offset of the block frame
     uint32_t nsucc = 0;
     U4 V = {0, 0, 0, 0};
+    U4 Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
+#pragma unroll 1
     for (int r = 0; r < kKmcRounds; ++r) {
+        const U4 W = Wn;
         if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
+        Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r + 1));  // next round (unused after the last)
         const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
-        const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r));
         const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
-        // KmcKernel::draw_site (kmc.hpp:154-171) over the domain box.
+        // KmcKernel::draw_site (kmc.hpp:154-171) over the domain box: x, y
+        // uniform, z uniform over the two planes of matching parity.
         const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
-        const int tpar = ((X0 + lx) ^ (Y0 + ly)) & 1;
-        const int lz = lz0 + ((((Z0 + lz0) & 1) == tpar) ? 0 : 1) + 2 * int((W.x >> 4) & 1u);
-        // kmc_attempt_impl (kmc.hpp:84-111)
-        const int here = bit_at(R.at(ly, lz), lx);
-        if (BOTH || here) {
-            const int dir = int(below(W.y, 12));
-            const int px = lx + c_fcc[dir][0], py = ly + c_fcc[dir][1], pz = lz + c_fcc[dir][2];
-            const int pb = bit_at(R.at(py, pz), px);
-            if (pb != here) {
-                const int bx_ = here ? lx : px, by_ = here ? ly : py, bz_ = here ? lz : pz;
-                const int ax = here ? px : lx, ay = here ? py : ly, az = here ? pz : lz;
-                // n_i excludes the A partner (no B there), n_f excludes the B partner.
-                const int d = nb_count(R, bx_, by_, bz_) - (nb_count(R, ax, ay, az) - 1);
-                const bool acc = d <= 0 || uint64_t(W.z) < ((uint64_t(a.thr_hi[d]) << 32) | a.thr_lo[d]);
-                if (acc) {
-                    atomicXor(R.ptr(by_, bz_), 1ull << (bx_ + 16));
-                    atomicXor(R.ptr(ay, az), 1ull << (ax + 16));
-                    global_flip(a.w, L, (X0 + bx_) & Lm, (Y0 + by_) & Lm, (Z0 + bz_) & Lm);
-                    global_flip(a.w, L, (X0 + ax) & Lm, (Y0 + ay) & Lm, (Z0 + az) & Lm);
-                    ++nsucc;
-                }
+        const int tpar = (lx ^ ly ^ lz0 ^ zpar0) & 1;  // 1 iff plane lz0 has the wrong parity
+        const int lz = lz0 + tpar + 2 * int((W.x >> 4) & 1u);
+        const int dir = int(below(W.y, 12));
+        int dx, dy, dz;
+        fcc_offset(dir, dx, dy, dz);
+        const int px = lx + dx, py = ly + dy, pz = lz + dz;
+        // kmc_attempt_impl (kmc.hpp:84-111); everything loaded up front.
+        const int here = int((R.at(ly, lz) >> (lx + 16)) & 1ull);
+        const int pb = int((R.at(py, pz) >> (px + 16)) & 1ull);
+        const int n_site = nb_count(R, lx, ly, lz), n_part = nb_count(R, px, py, pz);
+        if ((BOTH || here) && pb != here) {
+            // n_i (B site, its A partner excluded: no B there), n_f (A site, its B partner excluded)
+            const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
+            const bool acc = d <= 0 || uint64_t(W.z) < s_thr[d];
+            if (acc) {
+                atomicXor(R.ptr(ly, lz), 1ull << (lx + 16));
+                atomicXor(R.ptr(py, pz), 1ull << (px + 16));
+                global_flip(a.w, L, (X0 + lx) & Lm, (Y0 + ly) & Lm, (Z0 + lz) & Lm);
+                global_flip(a.w, L, (X0 + px) & Lm, (Y0 + py) & Lm, (Z0 + pz) & Lm);
+                ++nsucc;
             }
         }
-        __syncthreads();
+        if (WARP_SYNC) __syncwarp();
+        else __syncthreads();
     }
     nsucc = __reduce_add_sync(0xFFFFFFFFu, nsucc);
     if ((threadIdx.x & 31) == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
 }
 
+// ---------------------------------------------------------------- bk = 16
+// Specialised for 16^3 device blocks (the default plan): block plus 2-site
+// halo is 20 sites per axis, so a staged row is ONE 32-bit word (local x lx
+// at bit lx + 8) and a block is 400 words.  One block (8 tiles, 8 lanes) per
+// CTA/warp, so the 512 active blocks of a 256^3 phase spread over all SMs and
+// the per-round barrier is __syncwarp.  The lattice is not written during the
+// rounds: each block keeps a pristine copy of its staged rows and XORs the
+// difference into global memory once, after its last round (RED.XOR on the
+// words holding bits [X0-1, X0+17) of rows y, z in [-1, 17): the write reach
+// of kmc.hpp:140-141; neighbouring active blocks touch disjoint bits).
+constexpr int kK16E = 20, kK16Rows = kK16E * kK16E, kK16Ofs = 8;
+
+__device__ __forceinline__ int k16_row(int ly, int lz) { return (lz + 2) * kK16E + (ly + 2); }
+
+// B count among the 12 fcc neighbours of local x lx, given the site's four
+// face rows f[] (y-1, y+1, z-1, z+1: bits lx-1, lx+1) and four edge rows e[]
+// (bit lx).
+__device__ __forceinline__ int k16_count(const uint32_t (&f)[4], const uint32_t (&e)[4], int lx) {
+    const uint32_t m2 = 5u << (lx + kK16Ofs - 1), m1 = 1u << (lx + kK16Ofs);
+    return __popc(f[0] & m2) + __popc(f[1] & m2) + __popc(f[2] & m2) + __popc(f[3] & m2) + __popc(e[0] & m1) +
+           __popc(e[1] & m1) + __popc(e[2] & m1) + __popc(e[3] & m1);
+}
+
+template <bool BOTH>
+__global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    extern __shared__ __align__(16) uint32_t sk16[];
+    __shared__ unsigned long long s_thr[13];
+    const int L = a.L, Lm = L - 1, t = int(threadIdx.x) & 7, sub = int(threadIdx.x) >> 3;
+    const unsigned wmask = blockDim.x >= 32 ? 0xFFFFFFFFu : (1u << blockDim.x) - 1u;
+    uint32_t* const cur = sk16 + sub * (2 * kK16Rows);
+    uint32_t* const org = cur + kK16Rows;
+    const int nb = L >> 4, h = nb >> 1;
+    const int blin = int(blockIdx.x) * int(blockDim.x >> 3) + sub;
+    const KmcSweep sw = kmc_sweep_draw(16, a.seed, a.sweep);
+    const int set = sw.set(a.phase);
+    const int bxi = 2 * (blin % h) + (set & 1);
+    const int byi = 2 * ((blin / h) % h) + ((set >> 1) & 1);
+    const int bzi = 2 * (blin / (h * h)) + (set >> 2);
+    const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
+    const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
+    if (threadIdx.x < 13) s_thr[threadIdx.x] = (uint64_t(a.thr_hi[threadIdx.x]) << 32) | a.thr_lo[threadIdx.x];
+
+    // Stage: row word bit k = global bit X0 - 8 + k (k = lx + 8).
+    const int wpr = L >> 5, wm = wpr - 1;
+    const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
+    for (int rr = t; rr < kK16Rows; rr += 8) {
+        const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
+        const uint32_t* row = a.w + (size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+        const uint32_t v = __funnelshift_r(row[w0 & wm], row[(w0 + 1) & wm], bo);
+        cur[rr] = v;
+        org[rr] = v;
+    }
+    __syncwarp(wmask);
+
+    const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
+    const uint32_t tl = uint32_t(L / 8);
+    const uint32_t tile_id = (uint32_t(bzi * 2 + tz) * tl + uint32_t(byi * 2 + ty)) * tl + uint32_t(bxi * 2 + tx);
+    const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;
+    uint32_t nsucc = 0;
+    U4 V = {0, 0, 0, 0};
+    U4 Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
+#pragma unroll 1
+    for (int r = 0; r < kKmcRounds; ++r) {
+        const U4 W = Wn;
+        if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
+        const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
+        const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
+        // KmcKernel::draw_site (kmc.hpp:154-171) over the domain box.
+        const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
+        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((W.x >> 4) & 1u);
+        int dx, dy, dz;
+        fcc_offset(int(below(W.y, 12)), dx, dy, dz);
+        const int px = lx + dx, py = ly + dy, pz = lz + dz;
+        const int sr = k16_row(ly, lz), pr = k16_row(py, pz);
+        // every shared load of the attempt, issued before any use
+        const uint32_t own = cur[sr], par = cur[pr];
+        const uint32_t sf[4] = {cur[sr - 1], cur[sr + 1], cur[sr - kK16E], cur[sr + kK16E]};
+        const uint32_t se[4] = {cur[sr - kK16E - 1], cur[sr + kK16E - 1], cur[sr - kK16E + 1], cur[sr + kK16E + 1]};
+        const uint32_t pf[4] = {cur[pr - 1], cur[pr + 1], cur[pr - kK16E], cur[pr + kK16E]};
+        const uint32_t pe[4] = {cur[pr - kK16E - 1], cur[pr + kK16E - 1], cur[pr - kK16E + 1], cur[pr + kK16E + 1]};
+        Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r + 1));  // next round, overlaps the loads
+        const int here = int((own >> (lx + kK16Ofs)) & 1u), pb = int((par >> (px + kK16Ofs)) & 1u);
+        const int n_site = k16_count(sf, se, lx), n_part = k16_count(pf, pe, px);
+        // kmc_attempt_impl (kmc.hpp:84-111)
+        if ((BOTH || here) && pb != here) {
+            const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
+            if (d <= 0 || uint64_t(W.z) < s_thr[d]) {
+                atomicXor(cur + sr, 1u << (lx + kK16Ofs));
+                atomicXor(cur + pr, 1u << (px + kK16Ofs));
+                ++nsucc;
+            }
+        }
+        __syncwarp(wmask);
+    }
+    // Write-back of the 1-ring-extended block: bits lx in [-1, 17) of rows
+    // (ly, lz) in [-1, 17)^2, as XOR differences.
+    const int gx = (X0 - 1 + L) & Lm, gw = gx >> 5, gb = gx & 31;
+    for (int q = t; q < 18 * 18; q += 8) {
+        const int ly = q % 18 - 1, lz = q / 18 - 1;
+        const int rr = k16_row(ly, lz);
+        const uint32_t d = ((cur[rr] ^ org[rr]) >> (kK16Ofs - 1)) & 0x3FFFFu;  // 18 bits, lx = -1 .. 16
+        if (d) {
+            uint32_t* row = a.w + (size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+            atomicXor(row + gw, d << gb);
+            if (gb > 14) atomicXor(row + ((gw + 1) & wm), d >> (32 - gb));
+        }
+    }
+    nsucc = __reduce_add_sync(wmask, nsucc);
+    if (threadIdx.x == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
+}
+
+// Blocks per CTA: bk = 16 (8 threads) packs four blocks in one warp; bk = 32
+// (64 threads) is one block per CTA.
 int kmc_blocks_per_cta(int bk) {
     const int tpb = (bk / 8) * (bk / 8) * (bk / 8);
-    return tpb >= 128 ? 1 : 128 / tpb;
+    return tpb >= 32 ? 1 : 32 / tpb;
 }
 
 size_t kmc_phase_smem_bytes(int bk) {
@@ -135,13 +278,18 @@ size_t kmc_phase_smem_bytes(int bk) {
     return size_t(kmc_blocks_per_cta(bk)) * E * E * 8;
 }
 
+template <bool BOTH, bool WS>
+static cudaError_t kmc_attr(int smem) {
+    return cudaFuncSetAttribute(kmc_dt_phase_kernel<BOTH, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
 cudaError_t kmc_phase_kernel_attrs() {
     const int smem = int(kmc_phase_smem_bytes(32) > kmc_phase_smem_bytes(16) ? kmc_phase_smem_bytes(32)
                                                                               : kmc_phase_smem_bytes(16));
-    cudaError_t e = cudaFuncSetAttribute(kmc_dt_phase_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(kmc_dt_phase_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = kmc_attr<false, false>(smem);
+    if (e == cudaSuccess) e = kmc_attr<true, false>(smem);
+    if (e == cudaSuccess) e = kmc_attr<false, true>(smem);
+    if (e == cudaSuccess) e = kmc_attr<true, true>(smem);
     return e;
 }
 
@@ -154,10 +302,24 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
     const dim3 grid(unsigned(active / bpc));
     const dim3 block(unsigned(bpc * tpb));
     const size_t smem = size_t(bpc) * size_t(a.bk + 4) * size_t(a.bk + 4) * 8;
-    if (a.both)
-        kmc_dt_phase_kernel<true><<<grid, block, smem, st>>>(a);
-    else
-        kmc_dt_phase_kernel<false><<<grid, block, smem, st>>>(a);
+    if (a.bk == 16) {
+        // One block per warp while the phase has fewer blocks than ~4 per
+        // SMSP (latency-bound: spread over all SMs); four per warp beyond.
+        const int per = active >= 4 * 4 * 148 ? 4 : 1;
+        const dim3 g16 = dim3(unsigned(active / per)), b16 = dim3(unsigned(8 * per));
+        const size_t sm16 = size_t(per) * 2 * kK16Rows * sizeof(uint32_t);
+        if (a.both) kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
+        else kmc_dt16_phase_kernel<false><<<g16, b16, sm16, st>>>(a);
+        return cudaGetLastError();
+    }
+    const bool ws = bpc * tpb <= 32;
+    if (a.both) {
+        if (ws) kmc_dt_phase_kernel<true, true><<<grid, block, smem, st>>>(a);
+        else kmc_dt_phase_kernel<true, false><<<grid, block, smem, st>>>(a);
+    } else {
+        if (ws) kmc_dt_phase_kernel<false, true><<<grid, block, smem, st>>>(a);
+        else kmc_dt_phase_kernel<false, false><<<grid, block, smem, st>>>(a);
+    }
     return cudaGetLastError();
 }
 
