@@ -56,6 +56,34 @@ LFG_API int lfg_kmc_synchronize(lfg_kmc* h);
 /* Device pointer of the occupancy words ([L][L][L/32] uint32) for interop. */
 LFG_API int lfg_kmc_device_words(lfg_kmc* h, void** dev_ptr, size_t* bytes);
 
+/* ------------------------------------------------------ z-slab shards (C5)
+ * No reference counterpart: the reference is single-process (SURVEY.md §2,
+ * PAPER.md:473-480 describes only an MPI dead-border variant).  One rank holds
+ * the planes of its z-slab in a device ring buffer of `plane_capacity` planes
+ * (a power of two; == L for a whole lattice); global plane z lives at slot
+ * z & (plane_capacity - 1), each plane L*L/32 uint32 words in the
+ * OccupancyLattice order.  The RNG is keyed on global block/tile ids of the
+ * sweep's shifted frame, so any slab decomposition reproduces the
+ * single-lattice trajectory bit for bit.  The host driver
+ * (paper_1204_5072_b200/shard.py, ShardedKmc) moves planes between ranks. */
+/* A handle without a resident lattice (slab phases, readouts, counters). */
+LFG_API int lfg_kmc_create_slab(lfg_kmc** h, int32_t L, double eps, int32_t both_active, uint64_t seed,
+                                const lfg_kmc_plan* plan, int32_t device);
+/* Sweep draw of the shifted frame: out[11] = ox, oy, oz, block-set order[8]. */
+LFG_API int lfg_kmc_sweep_origin(int32_t L, const lfg_kmc_plan* plan, uint64_t seed, uint64_t sweep, int32_t* out);
+/* Phase `phase` of sweep `sweep` restricted to block z-rows
+ * [block_row_begin, +block_rows) (even-aligned) of the shifted frame; reads
+ * planes two beyond the slab, writes one beyond (kmc.hpp:140-141). */
+LFG_API int lfg_kmc_slab_phase(lfg_kmc* h, void* planes, int32_t plane_capacity, int32_t block_row_begin,
+                               int32_t block_rows, uint64_t sweep, int32_t phase);
+/* make_random_alloy on planes [z_begin, +nz) (same sites as lfg_kmc_init_random_alloy). */
+LFG_API int lfg_kmc_slab_init_random_alloy(lfg_kmc* h, void* planes, int32_t plane_capacity, int32_t z_begin,
+                                           int32_t nz, double c, uint64_t seed);
+/* open_bonds_per_particle partial sums over planes [z_begin, +nz) (planes
+ * z_begin-1 and z_begin+nz must be current). */
+LFG_API int lfg_kmc_slab_open_bond_sums(lfg_kmc* h, const void* planes, int32_t plane_capacity, int32_t z_begin,
+                                        int32_t nz, int64_t* particles, int64_t* open_bonds);
+
 #ifdef __cplusplus
 }
 #endif

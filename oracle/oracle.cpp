@@ -455,6 +455,54 @@ int orc_kmc_sweep_dt(int32_t L, uint64_t* w, double eps, int both, uint64_t seed
     return 0;
 }
 
+// One DT phase restricted to block z-rows [bz0, bz0 + nbz) (the z-slab
+// driver's unit of work; tests/test_shard_kmc_cpu.py).
+int orc_kmc_dt_phase_rows(int32_t L, uint64_t* w, double eps, int both, uint64_t seed, uint64_t sweep,
+                          int32_t phase, int32_t bk, int32_t bz0, int32_t nbz, int64_t* counters) {
+    if (!(eps >= 0.0) || phase < 0 || phase > 7) return -1;
+    orc::KmcPlan pl{L, bk};
+    const orc::KmcSweepDraw d = orc::kmc_sweep_draw(pl, seed, sweep);
+    int64_t succ = 0, att = 0;
+    orc::kmc_dt_phase(pl, d, seed, sweep, phase, bz0, bz0 + nbz,
+                      [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
+                          const int32_t site[3] = {x, y, z};
+                          ++att;
+                          succ += kmc_attempt(w, L, site, eps, both, [&] { return orc::below(dir_w, 12); },
+                                              [&] { return acc_w * 0x1p-32; }) == 0;
+                      });
+    counters[0] += att;
+    counters[1] += succ;
+    return 0;
+}
+
+// The KMC sweep draw (origin + block-set order): out[11] = ox, oy, oz, order[8].
+void orc_kmc_sweep_draw(int32_t L, int32_t bk, uint64_t seed, uint64_t sweep, int32_t* out) {
+    const orc::KmcSweepDraw d = orc::kmc_sweep_draw(orc::KmcPlan{L, bk}, seed, sweep);
+    out[0] = d.ox;
+    out[1] = d.oy;
+    out[2] = d.oz;
+    for (int k = 0; k < 8; ++k) out[3 + k] = d.perm[k];
+}
+
+// open_bonds_per_particle (kmc.cpp:20-40) as exact integer sums over planes
+// z in [z0, z0 + nz) (mod L); z0 = 0, nz = L is the reference's readout.
+void orc_kmc_open_bond_sums_planes(int32_t L, const uint64_t* w, int32_t z0, int32_t nz, int64_t* particles,
+                                   int64_t* open) {
+    const int32_t mask = L - 1;
+    int64_t np = 0, no = 0;
+    for (int32_t k = 0; k < nz; ++k) {
+        const int32_t z = (z0 + k) & mask;
+        for (int32_t y = 0; y < L; ++y)
+            for (int32_t x = (y ^ z) & 1; x < L; x += 2) {
+                if (!occ(w, L, x, y, z)) continue;
+                ++np;
+                for (const auto& d : kOff) no += !occ(w, L, (x + d[0]) & mask, (y + d[1]) & mask, (z + d[2]) & mask);
+            }
+    }
+    *particles = np;
+    *open = no;
+}
+
 // open_bonds_per_particle (kmc.cpp:20-40) as exact integer sums.
 void orc_kmc_open_bond_sums(int32_t L, const uint64_t* w, int64_t* particles, int64_t* open) {
     const int32_t mask = L - 1;

@@ -207,19 +207,21 @@ inline KmcSweepDraw kmc_sweep_draw(const KmcPlan& pl, uint64_t seed, uint64_t sw
     return d;
 }
 
-// One KMC DT sweep.  attempt(x, y, z, dir_word, accept_word) performs one
-// exchange attempt at the fcc-valid site (x, y, z).  The site draw follows
-// KmcKernel::draw_site (kmc.hpp:154-171) over the domain box: x and y
-// uniform, z uniform over the parity-matched planes.
+// One phase k (0..7) of a KMC DT sweep, restricted to block z-rows
+// [bz_lo, bz_hi) of the shifted frame (the whole lattice: 0, L/bk -- the
+// z-slab driver runs each rank's rows).  attempt(x, y, z, dir_word,
+// accept_word) performs one exchange attempt at the fcc-valid site (x, y, z).
+// The site draw follows KmcKernel::draw_site (kmc.hpp:154-171) over the
+// domain box: x and y uniform, z uniform over the parity-matched planes.
 template <class Attempt>
-void kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+void kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, uint64_t sweep, int k, int32_t bz_lo,
+                  int32_t bz_hi, Attempt&& attempt) {
     const int32_t L = pl.L, mask = L - 1;
-    const KmcSweepDraw d = kmc_sweep_draw(pl, seed, sweep);
     const int32_t nb = L / pl.bk, tb = pl.bk / kKmcTile, tl = L / kKmcTile;
-    for (int k = 0; k < 8; ++k) {
-        const int set = d.perm[k];
-        const int sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
-        for (int32_t bzi = sz; bzi < nb; bzi += 2)
+    const int set = d.perm[k];
+    const int sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
+    for (int32_t bzi = sz; bzi < nb; bzi += 2) {
+        if (bzi < bz_lo || bzi >= bz_hi) continue;
         for (int32_t byi = sy; byi < nb; byi += 2)
         for (int32_t bxi = sx; bxi < nb; bxi += 2) {
             const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
@@ -248,6 +250,13 @@ void kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& at
             }
         }
     }
+}
+
+// One KMC DT sweep: the eight phases in the sweep's drawn order.
+template <class Attempt>
+void kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+    const KmcSweepDraw d = kmc_sweep_draw(pl, seed, sweep);
+    for (int k = 0; k < 8; ++k) kmc_dt_phase(pl, d, seed, sweep, k, 0, pl.L / pl.bk, attempt);
 }
 
 }  // namespace orc

@@ -69,6 +69,9 @@ class Oracle:
         _sig(lib, "orc_kmc_random_alloy", I, I32, D, I, U64, U32, u64p, C.POINTER(U64))
         _sig(lib, "orc_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
         _sig(lib, "orc_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, i64p)
+        _sig(lib, "orc_kmc_dt_phase_rows", I, I32, u64p, D, I, U64, U64, I32, I32, I32, I32, i64p)
+        _sig(lib, "orc_kmc_sweep_draw", None, I32, I32, U64, U64, i32p)
+        _sig(lib, "orc_kmc_open_bond_sums_planes", None, I32, u64p, I32, I32, C.POINTER(I64), C.POINTER(I64))
         _sig(lib, "orc_kmc_open_bond_sums", None, I32, u64p, C.POINTER(I64), C.POINTER(I64))
         _sig(lib, "orc_kmc_count_b", I64, I32, u64p)
 
@@ -154,6 +157,23 @@ class Oracle:
         c = np.zeros(2, np.int64)
         assert self.lib.orc_kmc_sweep_dt(L, w, eps, int(both), seed, sweep0, nsweeps, bk, c) == 0
         return c
+
+    def kmc_dt_phase_rows(self, L, w, eps, both, seed, sweep, phase, bk, bz0, nbz):
+        """One DT phase on block z-rows [bz0, bz0 + nbz); returns [attempts, successes]."""
+        c = np.zeros(2, np.int64)
+        assert self.lib.orc_kmc_dt_phase_rows(L, w, eps, int(both), seed, sweep, phase, bk, bz0, nbz, c) == 0
+        return c
+
+    def kmc_sweep_draw(self, L, bk, seed, sweep):
+        """(ox, oy, oz, order[8]) of a KMC DT sweep."""
+        out = np.zeros(11, np.int32)
+        self.lib.orc_kmc_sweep_draw(L, bk, seed, sweep, out)
+        return int(out[0]), int(out[1]), int(out[2]), [int(v) for v in out[3:]]
+
+    def kmc_open_bond_sums_planes(self, L, w, z0, nz):
+        a, b = C.c_int64(), C.c_int64()
+        self.lib.orc_kmc_open_bond_sums_planes(L, w, z0, nz, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def kmc_open_bond_sums(self, L, w):
         a, b = C.c_int64(), C.c_int64()

@@ -156,6 +156,12 @@ def _bind_kmc(L) -> None:
     _sig(L, "lfg_kmc_set_stream", P, P)
     _sig(L, "lfg_kmc_synchronize", P)
     _sig(L, "lfg_kmc_device_words", P, C.POINTER(P), C.POINTER(SZ))
+    # z-slab sharded path
+    _sig(L, "lfg_kmc_create_slab", C.POINTER(P), I32, D, I32, U64, C.POINTER(KmcPlan), I32)
+    _sig(L, "lfg_kmc_sweep_origin", I32, C.POINTER(KmcPlan), U64, U64, C.POINTER(I32))
+    _sig(L, "lfg_kmc_slab_phase", P, P, I32, I32, I32, U64, I32)
+    _sig(L, "lfg_kmc_slab_init_random_alloy", P, P, I32, I32, I32, D, U64)
+    _sig(L, "lfg_kmc_slab_open_bond_sums", P, P, I32, I32, I32, C.POINTER(I64), C.POINTER(I64))
 
 
 def check(rc: int) -> None:

@@ -30,6 +30,7 @@ struct lfg_kmc {
     unsigned long long* hpin = nullptr; // pinned [2]
     int64_t attempts = 0;
     uint64_t thr[13] = {};
+    bool slab_only = false;             // created by lfg_kmc_create_slab: no resident lattice
 
     size_t nwords() const { return size_t(L) * L * L / 32; }
 };
@@ -38,6 +39,17 @@ namespace {
 
 void check_handle(const lfg_kmc* h) {
     if (!h) throw Error(LFG_EINVAL, "null lfg_kmc handle");
+}
+
+void check_resident(const lfg_kmc* h) {
+    check_handle(h);
+    if (h->slab_only) throw Error(LFG_EINVAL, "handle was created with lfg_kmc_create_slab (no resident lattice)");
+}
+
+void check_ring(const lfg_kmc* h, const void* planes, int32_t cap) {
+    if (!planes) throw Error(LFG_EINVAL, "null plane buffer");
+    if (cap < 1 || !is_pow2(cap) || cap > h->L)
+        throw Error(LFG_EINVAL, "plane_capacity must be a power of two <= L, got " + std::to_string(cap));
 }
 
 void validate_eps(double eps) {  // KmcParams::validate (kmc.hpp:24-26)
@@ -66,6 +78,9 @@ KmcPhaseArgs base_args(const lfg_kmc* h) {
         a.thr_lo[d] = uint32_t(h->thr[d]);
         a.thr_hi[d] = uint32_t(h->thr[d] >> 32);
     }
+    a.zmask = h->L - 1;
+    a.bz0 = 0;
+    a.nbz = h->L / h->bk;
     return a;
 }
 
@@ -92,46 +107,144 @@ unsigned long long read_u64(lfg_kmc* h, const unsigned long long* d) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+int32_t validate_create(int32_t L, double eps, const lfg_kmc_plan* plan) {
+    if (L < 4 || !is_pow2(L))  // check_size (lattice.cpp:10-16)
+        throw Error(LFG_EINVAL, "OccupancyLattice: size must be a power of two >= 4, got " + std::to_string(L));
+    if (L < 32)
+        throw Error(LFG_EINVAL, "DtPlan: the KMC two-layer DT needs L >= 32 (two 16-site blocks per axis), got " +
+                                    std::to_string(L));
+    validate_eps(eps);
+    const int32_t bk = plan && plan->block ? plan->block : 16;  // 16^3 blocks: SURVEY §7.1 (+0.03 %, z=+0.3)
+    if (!(bk == 16 || bk == 32) || L % (2 * bk))
+        throw Error(LFG_EINVAL, "DtPlan: block must be 16 or 32 with L % (2*block) == 0, got " + std::to_string(bk));
+    return bk;
+}
+
+lfg_kmc* create_handle(int32_t L, double eps, int32_t both_active, uint64_t seed, const lfg_kmc_plan* plan,
+                       int32_t device, bool slab_only) {
+    const int32_t bk = validate_create(L, eps, plan);
+    auto* h = new lfg_kmc();
+    try {
+        h->L = L;
+        h->bk = bk;
+        h->eps = eps;
+        h->both = both_active ? 1 : 0;
+        h->seed = seed;
+        h->device = device;
+        h->slab_only = slab_only;
+        build_thresholds(h);
+        DeviceGuard g(device);
+        cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        h->own_stream = true;
+        cuda_check(kmc_phase_kernel_attrs(), "kernel attributes");
+        if (!slab_only) h->w = dmalloc<uint32_t>(h->nwords(), "alloc lattice");
+        h->dcnt = dmalloc<unsigned long long>(1, "alloc counters");
+        h->dtmp = dmalloc<unsigned long long>(2, "alloc scratch");
+        cuda_check(cudaMallocHost(&h->hpin, 16), "alloc pinned");
+        if (!slab_only)  // all A (lattice.cpp:84-88)
+            cuda_check(cudaMemsetAsync(h->w, 0, h->nwords() * 4, h->stream), "memset");
+        cuda_check(cudaMemsetAsync(h->dcnt, 0, 8, h->stream), "memset");
+        sync(h);
+    } catch (...) {
+        lfg_kmc_destroy(h);
+        throw;
+    }
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
 int lfg_kmc_create(lfg_kmc** out, int32_t L, double eps, int32_t both_active, uint64_t seed,
                    const lfg_kmc_plan* plan, int32_t device) {
     return guarded([&] {
         if (!out) throw Error(LFG_EINVAL, "null output handle");
         *out = nullptr;
-        if (L < 4 || !is_pow2(L))  // check_size (lattice.cpp:10-16)
-            throw Error(LFG_EINVAL, "OccupancyLattice: size must be a power of two >= 4, got " + std::to_string(L));
-        if (L < 32)
-            throw Error(LFG_EINVAL, "DtPlan: the KMC two-layer DT needs L >= 32 (two 16-site blocks per axis), got " +
-                                        std::to_string(L));
-        validate_eps(eps);
-        int32_t bk = plan && plan->block ? plan->block : 16;  // 16^3 blocks: SURVEY §7.1 (+0.03 %, z=+0.3)
-        if (!(bk == 16 || bk == 32) || L % (2 * bk))
-            throw Error(LFG_EINVAL, "DtPlan: block must be 16 or 32 with L % (2*block) == 0, got " +
-                                        std::to_string(bk));
-        auto* h = new lfg_kmc();
-        try {
-            h->L = L;
-            h->bk = bk;
-            h->eps = eps;
-            h->both = both_active ? 1 : 0;
-            h->seed = seed;
-            h->device = device;
-            build_thresholds(h);
-            DeviceGuard g(device);
-            cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-            h->own_stream = true;
-            cuda_check(kmc_phase_kernel_attrs(), "kernel attributes");
-            h->w = dmalloc<uint32_t>(h->nwords(), "alloc lattice");
-            h->dcnt = dmalloc<unsigned long long>(1, "alloc counters");
-            h->dtmp = dmalloc<unsigned long long>(2, "alloc scratch");
-            cuda_check(cudaMallocHost(&h->hpin, 16), "alloc pinned");
-            cuda_check(cudaMemsetAsync(h->w, 0, h->nwords() * 4, h->stream), "memset");  // all A (lattice.cpp:84-88)
-            cuda_check(cudaMemsetAsync(h->dcnt, 0, 8, h->stream), "memset");
-            sync(h);
-        } catch (...) {
-            lfg_kmc_destroy(h);
-            throw;
-        }
-        *out = h;
+        *out = create_handle(L, eps, both_active, seed, plan, device, false);
+    });
+}
+
+int lfg_kmc_create_slab(lfg_kmc** out, int32_t L, double eps, int32_t both_active, uint64_t seed,
+                        const lfg_kmc_plan* plan, int32_t device) {
+    return guarded([&] {
+        if (!out) throw Error(LFG_EINVAL, "null output handle");
+        *out = nullptr;
+        *out = create_handle(L, eps, both_active, seed, plan, device, true);
+    });
+}
+
+int lfg_kmc_sweep_origin(int32_t L, const lfg_kmc_plan* plan, uint64_t seed, uint64_t sweep, int32_t* out) {
+    return guarded([&] {
+        if (!out) throw Error(LFG_EINVAL, "null output");
+        const int32_t bk = validate_create(L, 0.0, plan);
+        const KmcSweep sw = kmc_sweep_draw(bk, seed, sweep);
+        out[0] = sw.ox;
+        out[1] = sw.oy;
+        out[2] = sw.oz;
+        for (int k = 0; k < 8; ++k) out[3 + k] = sw.set(k);
+    });
+}
+
+int lfg_kmc_slab_phase(lfg_kmc* h, void* planes, int32_t cap, int32_t bz0, int32_t nbz, uint64_t sweep,
+                       int32_t phase) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, planes, cap);
+        if (phase < 0 || phase > 7) throw Error(LFG_EINVAL, "phase must be in 0..7");
+        if (bz0 < 0 || (bz0 & 1) || nbz < 2 || (nbz & 1) || bz0 + nbz > h->L / h->bk)
+            throw Error(LFG_EINVAL, "block-row range must be even-aligned inside [0, L/block)");
+        if (cap < h->L && cap < nbz * h->bk + 4)
+            throw Error(LFG_EINVAL, "plane_capacity too small for the slab and its ghost planes");
+        DeviceGuard g(h->device);
+        KmcPhaseArgs a = base_args(h);
+        a.w = static_cast<uint32_t*>(planes);
+        a.zmask = cap - 1;
+        a.bz0 = bz0;
+        a.nbz = nbz;
+        a.sweep = sweep;
+        a.phase = phase;
+        cuda_check(kmc_launch_phase(a, h->stream), "kmc_dt_phase launch");
+        const int64_t hh = h->L / h->bk / 2;
+        h->attempts += hh * hh * (nbz / 2) * int64_t(h->bk) * h->bk * h->bk / 2;
+    });
+}
+
+int lfg_kmc_slab_init_random_alloy(lfg_kmc* h, void* planes, int32_t cap, int32_t z0, int32_t nz, double c,
+                                   uint64_t seed) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, planes, cap);
+        if (!(c >= 0.0 && c <= 1.0))  // lattice.cpp:118-120
+            throw Error(LFG_EINVAL, "make_random_alloy: concentration must be in [0,1]");
+        if (nz < 0 || nz > cap) throw Error(LFG_EINVAL, "plane count out of range");
+        const uint64_t thr = uint64_t(std::llround(c * 4294967296.0));
+        DeviceGuard g(h->device);
+        cuda_check(kmc_launch_init_alloy(static_cast<uint32_t*>(planes), h->L, cap - 1, ((z0 % h->L) + h->L) % h->L,
+                                         nz, uint32_t(thr), uint32_t(thr >> 32), seed, h->stream),
+                   "init");
+    });
+}
+
+int lfg_kmc_slab_open_bond_sums(lfg_kmc* h, const void* planes, int32_t cap, int32_t z0, int32_t nz,
+                                int64_t* particles, int64_t* open_bonds) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, planes, cap);
+        if (nz < 0 || nz > cap) throw Error(LFG_EINVAL, "plane count out of range");
+        DeviceGuard g(h->device);
+        cuda_check(cudaMemsetAsync(h->dtmp, 0, 16, h->stream), "memset");
+        cuda_check(kmc_launch_open_bonds(static_cast<const uint32_t*>(planes), h->L, cap - 1,
+                                         ((z0 % h->L) + h->L) % h->L, nz, h->dtmp, h->stream),
+                   "open bonds");
+        cuda_check(cudaMemcpyAsync(h->hpin, h->dtmp, 16, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        *particles = int64_t(h->hpin[0]);
+        *open_bonds = int64_t(h->hpin[1]);
     });
 }
 
@@ -160,7 +273,7 @@ int lfg_kmc_get_plan(const lfg_kmc* h, lfg_kmc_plan* out) {
 
 int lfg_kmc_upload(lfg_kmc* h, const uint64_t* words, size_t nwords) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         const size_t need = size_t(h->L) * h->L * h->L / 64;
         if (nwords != need || !words) throw Error(LFG_EINVAL, "upload: expected " + std::to_string(need) + " words");
         DeviceGuard g(h->device);
@@ -171,7 +284,7 @@ int lfg_kmc_upload(lfg_kmc* h, const uint64_t* words, size_t nwords) {
 
 int lfg_kmc_download(lfg_kmc* h, uint64_t* words, size_t nwords) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         const size_t need = size_t(h->L) * h->L * h->L / 64;
         if (nwords != need || !words) throw Error(LFG_EINVAL, "download: expected " + std::to_string(need) + " words");
         DeviceGuard g(h->device);
@@ -182,19 +295,21 @@ int lfg_kmc_download(lfg_kmc* h, uint64_t* words, size_t nwords) {
 
 int lfg_kmc_init_random_alloy(lfg_kmc* h, double c, uint64_t seed) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         if (!(c >= 0.0 && c <= 1.0))  // lattice.cpp:118-120
             throw Error(LFG_EINVAL, "make_random_alloy: concentration must be in [0,1]");
         const uint64_t thr = uint64_t(std::llround(c * 4294967296.0));
         DeviceGuard g(h->device);
-        cuda_check(kmc_launch_init_alloy(h->w, h->L, uint32_t(thr), uint32_t(thr >> 32), seed, h->stream), "init");
+        cuda_check(kmc_launch_init_alloy(h->w, h->L, h->L - 1, 0, h->L, uint32_t(thr), uint32_t(thr >> 32), seed,
+                                         h->stream),
+                   "init");
         sync(h);
     });
 }
 
 int lfg_kmc_sweep(lfg_kmc* h, int64_t n_mcs, lfg_counters* out) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
         DeviceGuard g(h->device);
         const unsigned long long before = read_u64(h, h->dcnt);
@@ -211,7 +326,7 @@ int lfg_kmc_sweep(lfg_kmc* h, int64_t n_mcs, lfg_counters* out) {
 
 int lfg_kmc_sweep_async(lfg_kmc* h, int64_t n_mcs) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         if (n_mcs < 0) throw Error(LFG_EINVAL, "sweep: n_mcs must be >= 0");
         DeviceGuard g(h->device);
         enqueue(h, n_mcs);
@@ -220,7 +335,7 @@ int lfg_kmc_sweep_async(lfg_kmc* h, int64_t n_mcs) {
 
 int lfg_kmc_phase(lfg_kmc* h, uint64_t sweep, int32_t phase) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         if (phase < 0 || phase > 7) throw Error(LFG_EINVAL, "phase must be in 0..7");
         DeviceGuard g(h->device);
         KmcPhaseArgs a = base_args(h);
@@ -254,10 +369,10 @@ int lfg_kmc_reset_counters(lfg_kmc* h) {
 
 int lfg_kmc_open_bond_sums(lfg_kmc* h, int64_t* particles, int64_t* open_bonds) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         DeviceGuard g(h->device);
         cuda_check(cudaMemsetAsync(h->dtmp, 0, 16, h->stream), "memset");
-        cuda_check(kmc_launch_open_bonds(h->w, h->L, h->dtmp, h->stream), "open bonds");
+        cuda_check(kmc_launch_open_bonds(h->w, h->L, h->L - 1, 0, h->L, h->dtmp, h->stream), "open bonds");
         cuda_check(cudaMemcpyAsync(h->hpin, h->dtmp, 16, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         *particles = int64_t(h->hpin[0]);
@@ -279,7 +394,7 @@ int lfg_kmc_open_bonds_per_particle(lfg_kmc* h, double* out) {
 
 int lfg_kmc_count_b(lfg_kmc* h, int64_t* out) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         DeviceGuard g(h->device);
         cuda_check(cudaMemsetAsync(h->dtmp, 0, 8, h->stream), "memset");
         cuda_check(kmc_launch_count_b(h->w, h->L, h->dtmp, h->stream), "count_b");
@@ -339,7 +454,7 @@ int lfg_kmc_synchronize(lfg_kmc* h) {
 
 int lfg_kmc_device_words(lfg_kmc* h, void** ptr, size_t* bytes) {
     return guarded([&] {
-        check_handle(h);
+        check_resident(h);
         *ptr = h->w;
         *bytes = h->nwords() * 4;
     });

@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     const int set = sw.set(a.phase);
     const int bxi = 2 * (blin % h) + (set & 1);
     const int byi = 2 * ((blin / h) % h) + ((set >> 1) & 1);
-    const int bzi = 2 * (blin / (h * h)) + (set >> 2);
+    const int bzi = a.bz0 + 2 * (blin / (h * h)) + (set >> 2);  // bz0 even
     const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * bk) & Lm, Y0 = (sw.oy + byi * bk) & Lm, Z0 = (sw.oz + bzi * bk) & Lm;
+    const int zm = Lm & a.zmask;  // plane slot mask
     const KmcRows R{smk + size_t(sub) * rows, E};
     if (threadIdx.x < 13) s_thr[threadIdx.x] = (uint64_t(a.thr_hi[threadIdx.x]) << 32) | a.thr_lo[threadIdx.x];
 
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     const int xs = (X0 - 16 + L) & Lm, w0 = xs >> 5, bo = xs & 31;
     for (int rr = t; rr < rows; rr += tpb) {
         const int ly = rr % E - 2, lz = rr / E - 2;
-        const uint32_t* row = a.w + (size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+        const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
         const uint32_t g0 = row[w0 & wm], g1 = row[(w0 + 1) & wm], g2 = row[(w0 + 2) & wm];
         const uint32_t lo = __funnelshift_r(g0, g1, bo), hi = __funnelshift_r(g1, g2, bo);
         R.r[rr] = (static_cast<unsigned long long>(hi) << 32) | lo;
@@ -143,8 +144,8 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
             if (acc) {
                 atomicXor(R.ptr(ly, lz), 1ull << (lx + 16));
                 atomicXor(R.ptr(py, pz), 1ull << (px + 16));
-                global_flip(a.w, L, (X0 + lx) & Lm, (Y0 + ly) & Lm, (Z0 + lz) & Lm);
-                global_flip(a.w, L, (X0 + px) & Lm, (Y0 + py) & Lm, (Z0 + pz) & Lm);
+                global_flip(a.w, L, (X0 + lx) & Lm, (Y0 + ly) & Lm, (Z0 + lz) & zm);
+                global_flip(a.w, L, (X0 + px) & Lm, (Y0 + py) & Lm, (Z0 + pz) & zm);
                 ++nsucc;
             }
         }
@@ -192,9 +193,10 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     const int set = sw.set(a.phase);
     const int bxi = 2 * (blin % h) + (set & 1);
     const int byi = 2 * ((blin / h) % h) + ((set >> 1) & 1);
-    const int bzi = 2 * (blin / (h * h)) + (set >> 2);
+    const int bzi = a.bz0 + 2 * (blin / (h * h)) + (set >> 2);  // bz0 even
     const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
+    const int zm = Lm & a.zmask;  // plane slot mask
     if (threadIdx.x < 13) s_thr[threadIdx.x] = (uint64_t(a.thr_hi[threadIdx.x]) << 32) | a.thr_lo[threadIdx.x];
 
     // Stage: row word bit k = global bit X0 - 8 + k (k = lx + 8).
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
     for (int rr = t; rr < kK16Rows; rr += 8) {
         const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
-        const uint32_t* row = a.w + (size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+        const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
         const uint32_t v = __funnelshift_r(row[w0 & wm], row[(w0 + 1) & wm], bo);
         cur[rr] = v;
         org[rr] = v;
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         const int rr = k16_row(ly, lz);
         const uint32_t d = ((cur[rr] ^ org[rr]) >> (kK16Ofs - 1)) & 0x3FFFFu;  // 18 bits, lx = -1 .. 16
         if (d) {
-            uint32_t* row = a.w + (size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+            uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
             atomicXor(row + gw, d << gb);
             if (gb > 14) atomicXor(row + ((gw + 1) & wm), d >> (32 - gb));
         }
@@ -296,7 +298,7 @@ cudaError_t kmc_phase_kernel_attrs() {
 cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
     const int tpb = (a.bk / 8) * (a.bk / 8) * (a.bk / 8);
     const int h = a.L / a.bk / 2;
-    const int active = h * h * h;
+    const int active = h * h * (a.nbz / 2);
     int bpc = kmc_blocks_per_cta(a.bk);
     if (bpc > active) bpc = active;
     const dim3 grid(unsigned(active / bpc));
@@ -326,14 +328,19 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
 // make_random_alloy (lattice.cpp:117-132) with the counter RNG: valid site n
 // (n = sc index >> 1) is B iff word (n & 3) of Philox(seed; n >> 2, 0, 0,
 // TAG_KMC_INIT) < threshold, threshold = llround(c 2^32) as in the reference.
-__global__ void kmc_init_alloy_kernel(uint32_t* w, int L, uint32_t thr_lo, uint32_t thr_hi, uint64_t seed) {
-    const size_t nwords = size_t(L) * L * L / 32;
+__global__ void kmc_init_alloy_kernel(uint32_t* w, int L, int zm, int z0, int nz, uint32_t thr_lo, uint32_t thr_hi,
+                                      uint64_t seed) {
+    const int wpr = L >> 5;
+    const size_t plane_words = size_t(L) * wpr;
+    const size_t nwords = size_t(nz) * plane_words;
     const uint64_t thr = (uint64_t(thr_hi) << 32) | thr_lo;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nwords; k += size_t(gridDim.x) * blockDim.x) {
-        const size_t idx0 = k * 32;  // first sc index of the word
-        const size_t row = idx0 / size_t(L);
-        const int y = int(row % size_t(L)), z = int(row / size_t(L));
-        const int xpar = (y ^ z) & 1;  // valid x parity in this row
+        const int z = (z0 + int(k / plane_words)) & (L - 1);  // global plane
+        const size_t in_plane = k % plane_words;
+        const int y = int(in_plane / size_t(wpr));
+        const size_t gword = size_t(z) * plane_words + in_plane;  // global word index
+        const size_t idx0 = gword * 32;                            // first sc index of the word
+        const int xpar = (y ^ z) & 1;                              // valid x parity in this row
         uint32_t v = 0;
         // 16 valid sites per word: n = (idx0 + 2 j + xpar) >> 1 = idx0/2 + j
         const size_t n0 = idx0 >> 1;
@@ -346,15 +353,15 @@ __global__ void kmc_init_alloy_kernel(uint32_t* w, int L, uint32_t thr_lo, uint3
             for (int e = 0; e < 4; ++e)
                 if (uint64_t(rr[e]) < thr) v |= 1u << (2 * (4 * q + e) + xpar);
         }
-        w[k] = v;
+        w[size_t(z & zm) * plane_words + in_plane] = v;
     }
 }
 
-cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, uint32_t thr_lo, uint32_t thr_hi, uint64_t seed,
-                                  cudaStream_t st) {
-    const size_t nwords = size_t(L) * L * L / 32;
+cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, int zmask, int z0, int nz, uint32_t thr_lo, uint32_t thr_hi,
+                                  uint64_t seed, cudaStream_t st) {
+    const size_t nwords = size_t(nz) * L * L / 32;
     const int blocks = int(std::min<size_t>((nwords + 255) / 256, 148 * 16));
-    kmc_init_alloy_kernel<<<blocks, 256, 0, st>>>(w, L, thr_lo, thr_hi, seed);
+    kmc_init_alloy_kernel<<<blocks, 256, 0, st>>>(w, L, (L - 1) & zmask, z0, nz, thr_lo, thr_hi, seed);
     return cudaGetLastError();
 }
 
@@ -362,34 +369,36 @@ cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, uint32_t thr_lo, uint32_t 
 // valid sites, out[1] += sum over those B of A-occupied neighbours.  One
 // thread per 32-bit word; the 12 neighbour directions are aligned to the
 // word with funnel shifts of the three adjacent words of each neighbour row.
-__device__ __forceinline__ uint32_t kmc_row_word(const uint32_t* w, int L, int y, int z, int wi) {
+__device__ __forceinline__ uint32_t kmc_row_word(const uint32_t* w, int L, int zm, int y, int z, int wi) {
     const int Lm = L - 1, wpr = L >> 5;
-    return w[(size_t((z + L) & Lm) * L + size_t((y + L) & Lm)) * wpr + size_t((wi + wpr) & (wpr - 1))];
+    return w[(size_t((z + L) & zm) * L + size_t((y + L) & Lm)) * wpr + size_t((wi + wpr) & (wpr - 1))];
 }
 
 // bits of row (y, z) at x + dx for the 32 x of word wi
-__device__ __forceinline__ uint32_t kmc_shifted(const uint32_t* w, int L, int y, int z, int wi, int dx) {
-    if (dx == 0) return kmc_row_word(w, L, y, z, wi);
-    if (dx > 0) return __funnelshift_r(kmc_row_word(w, L, y, z, wi), kmc_row_word(w, L, y, z, wi + 1), 1);
-    return __funnelshift_l(kmc_row_word(w, L, y, z, wi - 1), kmc_row_word(w, L, y, z, wi), 1);
+__device__ __forceinline__ uint32_t kmc_shifted(const uint32_t* w, int L, int zm, int y, int z, int wi, int dx) {
+    if (dx == 0) return kmc_row_word(w, L, zm, y, z, wi);
+    if (dx > 0) return __funnelshift_r(kmc_row_word(w, L, zm, y, z, wi), kmc_row_word(w, L, zm, y, z, wi + 1), 1);
+    return __funnelshift_l(kmc_row_word(w, L, zm, y, z, wi - 1), kmc_row_word(w, L, zm, y, z, wi), 1);
 }
 
-__global__ void kmc_open_bonds_kernel(const uint32_t* __restrict__ w, int L, unsigned long long* out2) {
-    const size_t nwords = size_t(L) * L * L / 32;
+// Planes [z0, z0 + nz) (their +-1 neighbour planes must be current in the buffer).
+__global__ void kmc_open_bonds_kernel(const uint32_t* __restrict__ w, int L, int zm, int z0, int nz,
+                                      unsigned long long* out2) {
     const int wpr = L >> 5;
+    const size_t nwords = size_t(nz) * L * wpr;
     unsigned long long np = 0, no = 0;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < nwords; k += size_t(gridDim.x) * blockDim.x) {
         const int wi = int(k % size_t(wpr));
         const size_t row = k / size_t(wpr);
-        const int y = int(row % size_t(L)), z = int(row / size_t(L));
+        const int y = int(row % size_t(L)), z = (z0 + int(row / size_t(L))) & (L - 1);
         const uint32_t valid = ((y ^ z) & 1) ? 0xAAAAAAAAu : 0x55555555u;
-        const uint32_t b = w[k] & valid;
+        const uint32_t b = kmc_row_word(w, L, zm, y, z, wi) & valid;
         if (!b) continue;
         np += __popc(b);
         uint32_t open = 0;
 #pragma unroll
         for (int d = 0; d < 12; ++d) {
-            const uint32_t nbits = kmc_shifted(w, L, y + c_fcc[d][1], z + c_fcc[d][2], wi, c_fcc[d][0]);
+            const uint32_t nbits = kmc_shifted(w, L, zm, y + c_fcc[d][1], z + c_fcc[d][2], wi, c_fcc[d][0]);
             open += __popc(b & ~nbits);
         }
         no += open;
@@ -404,10 +413,11 @@ __global__ void kmc_open_bonds_kernel(const uint32_t* __restrict__ w, int L, uns
     }
 }
 
-cudaError_t kmc_launch_open_bonds(const uint32_t* w, int L, unsigned long long* out2, cudaStream_t st) {
-    const size_t nwords = size_t(L) * L * L / 32;
+cudaError_t kmc_launch_open_bonds(const uint32_t* w, int L, int zmask, int z0, int nz, unsigned long long* out2,
+                                  cudaStream_t st) {
+    const size_t nwords = size_t(nz) * L * L / 32;
     const int blocks = int(std::min<size_t>((nwords + 255) / 256, 148 * 16));
-    kmc_open_bonds_kernel<<<blocks, 256, 0, st>>>(w, L, out2);
+    kmc_open_bonds_kernel<<<blocks, 256, 0, st>>>(w, L, (L - 1) & zmask, z0, nz, out2);
     return cudaGetLastError();
 }
 

@@ -17,15 +17,19 @@ struct KmcPhaseArgs {
     int32_t both;                  // ActiveMode::both
     uint32_t thr_lo[13];           // low 32 bits of ceil(exp(-d eps) 2^32), d = 0..12
     uint32_t thr_hi[13];           // bit 32 (threshold == 2^32)
+    int32_t zmask;                 // buffer plane slot = global z & zmask (L-1: whole lattice)
+    int32_t bz0, nbz;              // block z-rows [bz0, bz0 + nbz) of the shifted frame (slabs)
 };
 
 int kmc_blocks_per_cta(int bk);
 size_t kmc_phase_smem_bytes(int bk);
 cudaError_t kmc_phase_kernel_attrs();
 cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st);
-cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, uint32_t thr_lo, uint32_t thr_hi, uint64_t seed,
+// Plane-ranged variants: planes [z0, z0 + nz) (global z, slot z & zmask).
+cudaError_t kmc_launch_init_alloy(uint32_t* w, int L, int zmask, int z0, int nz, uint32_t thr_lo, uint32_t thr_hi,
+                                  uint64_t seed, cudaStream_t st);
+cudaError_t kmc_launch_open_bonds(const uint32_t* w, int L, int zmask, int z0, int nz, unsigned long long* out2,
                                   cudaStream_t st);
-cudaError_t kmc_launch_open_bonds(const uint32_t* w, int L, unsigned long long* out2, cudaStream_t st);
 cudaError_t kmc_launch_count_b(const uint32_t* w, int L, unsigned long long* out, cudaStream_t st);
 
 }  // namespace lfg

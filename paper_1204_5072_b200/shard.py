@@ -428,3 +428,292 @@ class ShardedKpz:
         n = float(self.plan.L * self.plan.L)  # kpz.cpp:78-80
         mean = s / n
         return s2 / n - mean * mean
+
+
+# ============================================================================= KMC z-slabs
+# the 3-D lattice is cut into z-slabs of H = L/world
+# planes, H a multiple of 2*bk, so the block z-rows on either side of a slab
+# boundary are never active in the same phase.  In sweep s (origin oz_s) rank g
+# owns planes [oz_s + g H, oz_s + (g+1) H) (mod L) = block z-rows
+# [g H/bk, (g+1) H/bk) of the shifted frame.  Reach (kmc.hpp:140-141): a phase
+# reads two planes beyond the slab and writes one beyond it, so around each
+# phase of z-parity sz:
+#   * before: the two ghost planes on the active side are refreshed from the
+#     neighbour that owns them;
+#   * after: the one ghost plane the phase may have modified goes back to its
+#     owner (whose own blocks next to it were inactive in that phase).
+# Per sweep the ownership rolls with oz exactly as for the KPZ strips.  Plane
+# traffic per boundary: 2 planes in + 1 plane back per phase (128 KiB each at
+# L = 1024), plus < 2 bk planes per sweep for the roll.
+@dataclass(frozen=True)
+class SlabPlan:
+    L: int
+    world: int
+    bk: int
+
+    def __post_init__(self):
+        if self.L % self.world:
+            raise ValueError("world must divide L")
+        if self.world > 1 and self.H % (2 * self.bk):
+            raise ValueError(f"slab height L/world = {self.H} must be a multiple of 2*block = {2 * self.bk}")
+
+    @property
+    def H(self) -> int:
+        return self.L // self.world
+
+    @property
+    def cap(self) -> int:
+        return self.L if self.world == 1 else min(self.L, next_pow2(self.H + 4 * self.bk + 4))
+
+    @property
+    def wpp(self) -> int:  # uint32 words per plane
+        return self.L * self.L // 32
+
+    def start(self, oz: int, rank: int) -> int:
+        return (oz + rank * self.H) % self.L
+
+    def block_rows(self, rank: int):
+        return rank * self.H // self.bk, self.H // self.bk
+
+    def roll(self, oz_old: int, oz_new: int, rank: int):
+        if self.world == 1 or oz_old == oz_new:
+            return []
+        d = oz_new - oz_old
+        s = self.start(oz_old, rank)
+        up, dn = (rank + 1) % self.world, (rank - 1) % self.world
+        if d > 0:
+            return [("send", dn, s, d), ("recv", up, s + self.H, d)]
+        return [("send", up, s + self.H + d, -d), ("recv", dn, s + d, -d)]
+
+    def ghost(self, oz: int, rank: int, sz: int, depth: int = 2):
+        """Refresh the `depth` planes beyond the slab on side sz (1: above, 0: below)."""
+        if self.world == 1:
+            return []
+        s = self.start(oz, rank)
+        up, dn = (rank + 1) % self.world, (rank - 1) % self.world
+        if sz == 1:
+            return [("send", dn, s, depth), ("recv", up, s + self.H, depth)]
+        return [("send", up, s + self.H - depth, depth), ("recv", dn, s - depth, depth)]
+
+    def writeback(self, oz: int, rank: int, sz: int):
+        """Return the ghost plane a phase of z-parity sz may have written to its owner."""
+        if self.world == 1:
+            return []
+        s = self.start(oz, rank)
+        up, dn = (rank + 1) % self.world, (rank - 1) % self.world
+        if sz == 1:
+            return [("send", up, s + self.H, 1), ("recv", dn, s, 1)]
+        return [("send", dn, s - 1, 1), ("recv", up, s + self.H - 1, 1)]
+
+    def pieces(self, z_begin: int, count: int):
+        """Split global planes [z_begin, +count) mod L into ring-slot ranges (slot, n)."""
+        out = []
+        z = z_begin % self.L
+        left = count
+        while left > 0:
+            slot = z % self.cap
+            n = min(left, self.cap - slot, self.L - z)
+            out.append((slot, n))
+            z = (z + n) % self.L
+            left -= n
+        return out
+
+    def plane_pieces_global(self, z_begin: int, count: int):
+        out = []
+        z = z_begin % self.L
+        left = count
+        while left > 0:
+            n = min(left, self.L - z)
+            out.append((z, n))
+            z = (z + n) % self.L
+            left -= n
+        return out
+
+
+class CudaSlabEngine:
+    """One rank's z-slab on a CUDA device: a ring buffer of planes (torch int32
+    [cap, L*L/32]) + a slab handle of liblfg.so (lfg_kmc_create_slab)."""
+
+    def __init__(self, plan: SlabPlan, eps: float, both: bool, seed: int, device: int = 0):
+        import torch
+
+        self.plan = plan
+        self.torch = torch
+        self.buf = torch.zeros((plan.cap, plan.wpp), dtype=torch.int32, device=f"cuda:{device}")
+        lib = _native.lib()
+        h = C.c_void_p()
+        kp = _native.KmcPlan(plan.bk)
+        _native.check(lib.lfg_kmc_create_slab(C.byref(h), plan.L, float(eps), int(bool(both)), int(seed),
+                                              C.byref(kp), device))
+        self.h = h
+        self.stream = torch.cuda.Stream(device=device)
+        _native.check(lib.lfg_kmc_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
+
+    def close(self):
+        if self.h is not None:
+            _native.lib().lfg_kmc_destroy(self.h)
+            self.h = None
+
+    def rows(self, slot: int, n: int):
+        return self.buf[slot:slot + n]
+
+    def sync(self):
+        self.stream.synchronize()
+
+    def init_random_alloy(self, z_begin: int, count: int, c: float, seed: int):
+        _native.check(_native.lib().lfg_kmc_slab_init_random_alloy(
+            self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap, z_begin, count, float(c), int(seed)))
+
+    def load_planes(self, words_u64, z_begin: int, count: int):
+        """Copy global planes [z_begin, +count) of a host lattice (uint64 words) into the ring."""
+        import numpy as np
+
+        full = np.asarray(words_u64).view(np.uint32).view(np.int32).reshape(self.plan.L, self.plan.wpp)
+        for (z, n) in self.plan.plane_pieces_global(z_begin, count):
+            for (slot, m) in self.plan.pieces(z, n):
+                self.buf[slot:slot + m].copy_(self.torch.from_numpy(full[z:z + m].copy()))
+                z += m
+
+    def phase(self, sweep: int, phase: int, bz0: int, nbz: int):
+        _native.check(_native.lib().lfg_kmc_slab_phase(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
+                                                       bz0, nbz, int(sweep), phase))
+
+    def successes(self) -> int:
+        c = _native.Counters()
+        _native.check(_native.lib().lfg_kmc_counters(self.h, C.byref(c)))
+        return int(c.successes)
+
+    def open_bond_sums(self, z_begin: int, count: int):
+        a, b = C.c_int64(), C.c_int64()
+        _native.check(_native.lib().lfg_kmc_slab_open_bond_sums(
+            self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap, z_begin, count, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+
+def kmc_sweep_origin(plan: SlabPlan, seed: int, sweep: int):
+    out = (C.c_int32 * 11)()
+    kp = _native.KmcPlan(plan.bk)
+    _native.check(_native.lib().lfg_kmc_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep),
+                                                     C.cast(out, C.POINTER(C.c_int32))))
+    return int(out[0]), int(out[1]), int(out[2]), [int(out[3 + k]) for k in range(8)]
+
+
+class ShardedKmc:
+    """z-slab-sharded KMC lattice (SlabPlan); `engines`/`ranks`/`comm` as for
+    ShardedKpz.  `origin` maps (plan, seed, sweep) to (ox, oy, oz, order); it
+    defaults to the library's draw (tests may pass the oracle's)."""
+
+    def __init__(self, plan: SlabPlan, seed: int, engines, ranks, comm, origin=None):
+        self.plan = plan
+        self.seed = seed
+        self.engines = list(engines)
+        self.ranks = list(ranks)
+        self.comm = comm
+        self.origin = origin or kmc_sweep_origin
+        self.sweep_index = 0
+        self.oz = None
+
+    def _exchange(self, fn):
+        if isinstance(self.comm, LocalComm):
+            self.comm.exchange([fn(r) for r in self.ranks])
+        else:
+            self.comm.exchange(fn(self.ranks[0]))
+
+    def _window(self, rank):
+        return self.plan.start(self.oz, rank) - 2, self.plan.H + 4  # owned planes + two ghosts per side
+
+    # ---- initial state (no communication: the init is position-keyed) ------
+    def make_random_alloy(self, c: float, alloy_seed: int, sweep_index: int = 0):
+        self.sweep_index = sweep_index
+        self.oz = self.origin(self.plan, self.seed, sweep_index)[2]
+        for e, r in zip(self.engines, self.ranks):
+            z, n = self._window(r)
+            e.init_random_alloy(z, n, c, alloy_seed)
+        for e in self.engines:
+            e.sync()
+
+    def upload(self, words_u64, sweep_index: int = 0):
+        """Every rank takes its window of a full host lattice (reference word layout)."""
+        self.sweep_index = sweep_index
+        self.oz = self.origin(self.plan, self.seed, sweep_index)[2]
+        for e, r in zip(self.engines, self.ranks):
+            z, n = self._window(r)
+            e.load_planes(words_u64, z, n)
+        for e in self.engines:
+            e.sync()
+
+    # ---- sweeps ------------------------------------------------------------
+    def sweep(self, n: int = 1):
+        pl = self.plan
+        for _ in range(n):
+            s = self.sweep_index
+            _, _, oz, order = self.origin(pl, self.seed, s)
+            if oz != self.oz:
+                old = self.oz
+                self._exchange(lambda r: pl.roll(old, oz, r))
+                self.oz = oz
+            for k in range(8):
+                sz = order[k] >> 2
+                self._exchange(lambda r: pl.ghost(oz, r, sz, 2))
+                for e, r in zip(self.engines, self.ranks):
+                    b0, nb = pl.block_rows(r)
+                    e.phase(s, k, b0, nb)
+                self._exchange(lambda r: pl.writeback(oz, r, sz))
+            self.sweep_index += 1
+        for e in self.engines:
+            e.sync()
+
+    def _allreduce(self, vals):
+        if isinstance(self.comm, DistComm):
+            import torch
+
+            t = torch.tensor(vals, dtype=torch.int64)
+            if not self.comm.stage and self.engines[0].buf.is_cuda:
+                t = t.to(self.engines[0].buf.device)
+            self.comm.dist.all_reduce(t, group=self.comm.group)
+            return [int(v) for v in t.cpu().tolist()]
+        return vals
+
+    def successes(self) -> int:
+        return self._allreduce([sum(e.successes() for e in self.engines)])[0]
+
+    # ---- readout -----------------------------------------------------------
+    def owned_pieces(self, rank: int):
+        return self.plan.plane_pieces_global(self.plan.start(self.oz, rank), self.plan.H)
+
+    def open_bond_sums(self):
+        """open_bonds_per_particle (kmc.cpp:20-40) sums over the whole lattice."""
+        pl = self.plan
+        for sz in (0, 1):
+            self._exchange(lambda r: pl.ghost(self.oz, r, sz, 1))
+        np_, no = 0, 0
+        for e, r in zip(self.engines, self.ranks):
+            for (z, n) in self.owned_pieces(r):
+                a, b = e.open_bond_sums(z, n)
+                np_ += a
+                no += b
+        return tuple(self._allreduce([np_, no]))
+
+    def gather_planes(self):
+        """Full lattice as a CPU int32 tensor [L, L*L/32] (owned planes of every rank)."""
+        import torch
+
+        L, wpp = self.plan.L, self.plan.wpp
+        out = torch.zeros((L, wpp), dtype=torch.int32)
+        for e, r in zip(self.engines, self.ranks):
+            e.sync()
+            for (a, n) in self.owned_pieces(r):
+                z = a
+                for (slot, m) in self.plan.pieces(a, n):
+                    out[z:z + m] = e.rows(slot, m).cpu()
+                    z += m
+        if isinstance(self.comm, DistComm):
+            dist = self.comm.dist
+            dev = "cpu" if self.comm.stage else self.engines[0].buf.device
+            t = out.to(dev)
+            lo = (t & 0xFFFF).to(torch.int64)
+            hi = ((t >> 16) & 0xFFFF).to(torch.int64)
+            dist.all_reduce(lo, group=self.comm.group)
+            dist.all_reduce(hi, group=self.comm.group)
+            out = ((hi << 16) | lo).to(torch.int32).cpu()
+        return out

@@ -55,3 +55,33 @@ def test_sharded_equals_single(lfg, L, world, p, q, nsweeps):
     finally:
         for e in engines:
             e.close()
+
+
+# ----------------------------------------------------------------- KMC z-slabs
+@pytest.mark.parametrize("L,world,bk,both,nsweeps", [(128, 2, 16, 1, 2), (128, 4, 16, 0, 2),
+                                                     (256, 8, 16, 1, 1), (128, 2, 32, 1, 2)])
+def test_sharded_kmc_equals_single(lfg, L, world, bk, both, nsweeps):
+    """k z-slabs on cuda:0 (LocalComm plane exchanges) == the single lattice,
+    bit for bit: words, exchange count and open-bond sums."""
+    from paper_1204_5072_b200.shard import CudaSlabEngine, LocalComm, ShardedKmc, SlabPlan
+
+    seed, eps = 77 + world, 1.5
+    with lfg.KmcLattice(L, eps, bool(both), seed, block=bk) as k:
+        k.make_random_alloy(0.5, 5)
+        w0 = k.download()
+        c = k.sweep(nsweeps)
+        ref = k.download()
+        ref_ob = k.open_bond_sums()
+    pl = SlabPlan(L, world, bk)
+    engines = [CudaSlabEngine(pl, eps, bool(both), seed, 0) for _ in range(world)]
+    try:
+        sk = ShardedKmc(pl, seed, engines, list(range(world)), LocalComm(engines))
+        sk.make_random_alloy(0.5, 5)  # position-keyed Philox init: same sites as the single lattice
+        assert np.array_equal(sk.gather_planes().numpy().reshape(-1).view(np.uint64), w0)
+        sk.sweep(nsweeps)
+        assert sk.successes() == c.successes
+        assert np.array_equal(sk.gather_planes().numpy().reshape(-1).view(np.uint64), ref)
+        assert sk.open_bond_sums() == tuple(ref_ob)
+    finally:
+        for e in engines:
+            e.close()
