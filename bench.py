@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--p", type=float, default=1.0)
     ap.add_argument("--q", type=float, default=0.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--block-x", type=int, default=0, help="DT device block width (0: library default)")
+    ap.add_argument("--block-y", type=int, default=0, help="DT device block height (0: library default)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -295,7 +297,7 @@ def run_b200(args):
 
     peak, peak_kind = measured_peaks()
     if world == 1:
-        k = lfg.KpzLattice(L, args.p, args.q, args.seed, device=local)
+        k = lfg.KpzLattice(L, args.p, args.q, args.seed, block_x=args.block_x, block_y=args.block_y, device=local)
         k.set_stream(stream.cuda_stream)
         k.make_flat_slopes()
         plan = k.plan

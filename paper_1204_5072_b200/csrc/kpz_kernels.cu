@@ -86,12 +86,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t mbar, uint32_t by
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait_parity0(uint32_t mbar) {
+__device__ __forceinline__ void mbar_wait_parity(uint32_t mbar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred P;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], 0;\n\t"
-        "@!P bra WAIT_%=;\n\t}" ::"r"(mbar)
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(mbar), "r"(parity)
         : "memory");
 }
 
@@ -308,28 +308,65 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
 // A = ceil_2048(base - 1536), which lies at most 511 bytes above base - 1536.
 size_t kpz_phase_smem_bytes(int by) { return size_t(by + 9) * 256 + 512; }
 
+// Completion-flag dependencies of the whole-sweep kernel (below): before an
+// activation of phase k > 0 is staged, thread 0 waits until the phase-(k-1)
+// blocks in its 8-neighbourhood carry this launch's epoch.  `flags == nullptr`
+// (phase kernels, phase 0) means no wait.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct KpzDeps {
+    const uint32_t* flags;  // [nby][nbx] of this replica, or nullptr
+    int nbx, nby, ddx, ddy;  // ddx/ddy: previous set differs in x / y parity
+    uint32_t epoch;
+    __device__ __forceinline__ bool active() const { return flags != nullptr; }
+    // Straight-line (no divergent loop): the four blocks (bxi +- ddx, byi +- ddy)
+    // -- two distinct ones when only one parity differs -- carry this epoch.
+    __device__ __forceinline__ bool ready(int bxi, int byi) const {
+        const int x0 = (bxi - ddx + nbx) % nbx, x1 = (bxi + ddx) % nbx;
+        const int y0 = (byi - ddy + nby) % nby, y1 = (byi + ddy) % nby;
+        const uint32_t a = ld_acquire_u32(flags + y0 * nbx + x0), b = ld_acquire_u32(flags + y0 * nbx + x1);
+        const uint32_t c = ld_acquire_u32(flags + y1 * nbx + x0), d = ld_acquire_u32(flags + y1 * nbx + x1);
+        return ((a ^ epoch) | (b ^ epoch) | (c ^ epoch) | (d ^ epoch)) == 0u;
+    }
+    // Block-wide wait; the loop condition is a bar.red result (block-uniform),
+    // so no divergent control flow reaches the rounds that follow.
+    __device__ __forceinline__ void wait_block(int bxi, int byi) const {
+        if (!flags) return;
+        for (;;) {
+            int ok = 1;
+            if (threadIdx.x == 0) ok = ready(bxi, byi);
+            if (__syncthreads_and(ok)) break;
+            __nanosleep(128);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk copies read what the acquires saw
+    }
+};
+
+// One activation of device block (bxi, byi) (block-set `set`) of replica
+// `rep`: stage, 512 single-hit rounds, write back, count.  `mbar_parity` is
+// the phase of the CTA's staging mbarrier (initialised by the caller) that this
+// activation's bulk copies complete.
 template <bool GENERAL, bool FULL, int kNT, bool MW>
-__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
-    kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
-    extern __shared__ __align__(16) uint32_t sm_raw[];
-    const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
-    const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;  // shared address of line 0
-    uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);  // generic pointer to line 0 (lines < 6 unused)
+__device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint32_t* const sm, const uint32_t smA,
+                                                     const int rep, const uint64_t seed, const KpzSweep& sw,
+                                                     const int bxi, const int byi, const uint32_t mbar_parity,
+                                                     const bool init_mbar, const KpzDeps& deps) {
     const int L = a.L, Lm = L - 1, wpr = L >> 5, wmask = wpr - 1;
     const int Wt = a.bx >> 5;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int rep = a.rep0 + int(blockIdx.z);
-    const uint64_t seed = a.seeds[blockIdx.z];
     const uint64_t sweep = a.sweep;
     // Rows live at buffer slot (global row & rmask): rmask = L-1 for a whole
     // lattice, C-1 for a strip shard whose ring buffer holds C >= H + 4 by + 2 rows.
     const int rmask = Lm & a.row_mask;
     uint32_t* __restrict__ f = a.f + size_t(rep) * size_t(a.row_mask + 1) * size_t(wpr);
-
-    const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, sweep);
-    const int set = sw.set(a.phase);
-    const int bxi = 2 * int(blockIdx.x) + (set & 1);
-    const int byi = a.brow0 + 2 * int(blockIdx.y) + (set >> 1);  // brow0 even
     const uint32_t block_id = uint32_t(byi) * uint32_t(L / a.bx) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * a.bx) & Lm;
     const int Y0 = (sw.oy + byi * a.by) & Lm;
@@ -350,8 +387,9 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
         const int a0 = w0 & ~3, m = w0 & 3;
         const int n1 = min(40, wpr - a0);  // words before the x wrap (a multiple of 4)
         const uint32_t rows = uint32_t(a.by + 2);
+        deps.wait_block(bxi, byi);
         if (threadIdx.x == 0) {
-            mbar_init(mbar, 1);
+            if (init_mbar) mbar_init(mbar, 1);
             mbar_arrive_expect_tx(mbar, rows * 160u);
         }
         __syncthreads();
@@ -361,7 +399,7 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
             bulk_g2s(dst, row + a0, uint32_t(n1) * 4u, mbar);
             if (n1 < 40) bulk_g2s(dst + uint32_t(n1) * 4u, row, uint32_t(40 - n1) * 4u, mbar);
         }
-        mbar_wait_parity0(mbar);
+        mbar_wait_parity(mbar, mbar_parity);
         for (int R = warp - 1; R <= a.by; R += nwarps) {
             const uint32_t* line = sm + (R + 8) * 64;
             const uint32_t lo = line[m + lane + 1], hi = line[m + lane + 2];
@@ -375,6 +413,7 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
             if (lane < 2) sm[lane ? (R + 8) * 64 + 32 : (R + 7) * 64 + 63] = __funnelshift_r(elo, ehi, b);
         }
     } else {
+        deps.wait_block(bxi, byi);
         for (int R = warp - 1; R <= a.by; R += nwarps) {
             const uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
             for (int k = lane; k < Wt + 2; k += 32) {
@@ -428,6 +467,86 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
     }
 }
 
+// DT phase kernel: one CTA per active block of phase a.phase.
+template <bool GENERAL, bool FULL, int kNT, bool MW>
+__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
+    kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
+    extern __shared__ __align__(16) uint32_t sm_raw[];
+    const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
+    const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;  // shared address of line 0
+    uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);  // generic pointer to line 0 (lines < 6 unused)
+    const int rep = a.rep0 + int(blockIdx.z);
+    const uint64_t seed = a.seeds[blockIdx.z];
+    const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
+    const int set = sw.set(a.phase);
+    kpz_block_activation<GENERAL, FULL, kNT, MW>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
+                                                 a.brow0 + 2 * int(blockIdx.y) + (set >> 1), 0u, true,
+                                                 KpzDeps{nullptr, 1, 1, 0, 0, 0u});
+}
+
+// Whole-sweep kernel (resident lattice): the four DT phases of sweep a.sweep in
+// one persistent launch.  CTAs take activations in phase-major order
+// (round-robin over the resident grid); an activation of phase k > 0 first waits until the blocks of
+// phase k-1 in its 8-neighbourhood have published completion (flag = epoch).
+// Every earlier-phase neighbour is then complete as well (each one is adjacent
+// to a phase-(k-1) neighbour that waited for it), and later-phase neighbours
+// cannot start before this block publishes, so the schedule -- and therefore
+// the lattice -- is exactly that of four back-to-back phase launches, while
+// the tail of each phase overlaps the start of the next (no wave-quantisation
+// gap between phases).
+struct KpzSweepArgs {
+    KpzPhaseArgs p;            // p.phase unused; one replica p.rep0 (seed p.seeds[0])
+    uint32_t* flags;           // [L/by][L/bx] completion epochs of this replica
+    unsigned int* next_job;    // claim counter (zeroed before the launch)
+    uint32_t epoch;            // unique per launch
+    int32_t lg_hx, lg_pp;      // log2(L/bx/2), log2(active blocks per phase): shifts keep the
+                               // job -> block mapping on the uniform datapath (no division)
+};
+
+template <bool GENERAL, bool FULL, int kNT, bool MW>
+__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
+    kpz_dtr_sweep_kernel(const __grid_constant__ KpzSweepArgs s) {
+    extern __shared__ __align__(16) uint32_t sm_raw[];
+    const KpzPhaseArgs& a = s.p;
+    const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
+    const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;
+    uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);
+    const int nbx = a.L / a.bx, nby = a.L / a.by;
+    const int njobs = 4 << s.lg_pp;
+    uint32_t parity = 0;
+    bool first = true;
+    // Static round-robin: CTA c runs jobs c, c + G, c + 2G, ... in order (the
+    // job index stays a function of blockIdx, so the block/set/RNG bookkeeping
+    // keeps to the uniform datapath as in the phase kernel).  Every CTA's
+    // current job is its smallest unfinished one, so the globally smallest
+    // unfinished job always has its (smaller) dependencies done: no deadlock,
+    // given co-residency (cooperative launch).
+    for (int job = int(blockIdx.x); job < njobs; job += int(gridDim.x)) {
+        const int k = job >> s.lg_pp, idx = job & ((1 << s.lg_pp) - 1);
+        const uint64_t seed = a.seeds[0];
+        const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
+        const int set = sw.set(k);
+        // Phase k visits its block rows starting at row k (mod L/by/2): the
+        // first rows of a phase then depend on rows the previous phase finished
+        // long ago, never on its last (periodic-wrap) row.
+        const int hy_mask = (1 << (s.lg_pp - s.lg_hx)) - 1;
+        const int bxi = 2 * (idx & ((1 << s.lg_hx) - 1)) + (set & 1);
+        const int byi = 2 * (((idx >> s.lg_hx) + k) & hy_mask) + (set >> 1);
+        uint32_t* const fl = s.flags;
+        const int prev = k > 0 ? sw.set(k - 1) : set;
+        const KpzDeps deps{k > 0 ? fl : nullptr, nbx, nby, (prev & 1) != (set & 1), (prev >> 1) != (set >> 1),
+                           s.epoch};
+        kpz_block_activation<GENERAL, FULL, kNT, MW>(a, sm, smA, a.rep0, seed, sw, bxi, byi, parity, first, deps);
+        parity ^= 1u;
+        first = false;
+        __syncthreads();  // every warp's write-back issued before the release
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_u32(fl + byi * nbx + bxi, s.epoch);
+        }
+    }
+}
+
 // Tiles per lane for a block height: the largest NT <= LFG_KPZ_NT with by >= 16 NT.
 static int kpz_nt_for(int by) {
     int nt = LFG_KPZ_NT;
@@ -468,6 +587,76 @@ cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int r
         else launch_nt<1>(b, grid, smem, st);
     }
     return cudaGetLastError();
+}
+
+// ---- whole-sweep launcher
+template <bool GENERAL, bool FULL, int NT, bool MW>
+static cudaError_t launch_sweep_cfg(const KpzSweepArgs& s, int njobs, size_t smem, cudaStream_t st) {
+    auto kern = kpz_dtr_sweep_kernel<GENERAL, FULL, NT, MW>;
+    const int threads = 32 * (s.p.by / 16 / NT);
+    static int per_sm[2][2][3][2] = {};  // occupancy cache per instantiation (device-independent enough: B200 only)
+    int& occ = per_sm[GENERAL][FULL][NT == 4 ? 2 : NT - 1][MW];
+    if (occ == 0) {  // smem attribute for the largest plan (block_y = 128); occupancy for this one
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kpz_phase_smem_bytes(128)));
+        if (e != cudaSuccess) return e;
+    }
+    {
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+    }
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::min(njobs, occ * nsm);
+    void* args[] = {const_cast<KpzSweepArgs*>(&s)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(unsigned(grid)), dim3(unsigned(threads)),
+                                       args, smem, st);
+}
+
+template <int NT, bool MW>
+static cudaError_t launch_sweep_nt(const KpzSweepArgs& s, int njobs, size_t smem, cudaStream_t st) {
+    const bool full = s.p.bx == 1024;
+    if (s.p.general)
+        return full ? launch_sweep_cfg<true, true, NT, MW>(s, njobs, smem, st)
+                    : launch_sweep_cfg<true, false, NT, MW>(s, njobs, smem, st);
+    return full ? launch_sweep_cfg<false, true, NT, MW>(s, njobs, smem, st)
+                : launch_sweep_cfg<false, false, NT, MW>(s, njobs, smem, st);
+}
+
+static int ilog2(int v) {
+    int l = 0;
+    while ((1 << l) < v) ++l;
+    return l;
+}
+
+cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, uint32_t* flags,
+                             unsigned int* next_job, uint32_t& epoch, cudaStream_t st) {
+    const size_t smem = kpz_phase_smem_bytes(a.by);
+    const int nt = kpz_nt_for(a.by);
+    const size_t nblocks = size_t(a.L / a.bx) * size_t(a.L / a.by);
+    for (int r = 0; r < replicas; ++r) {  // one launch per replica
+        KpzSweepArgs s{};
+        s.p = a;
+        s.p.rep0 = r;
+        s.p.seeds[0] = seeds[r];
+        s.flags = flags + size_t(r) * nblocks;
+        s.next_job = next_job;
+        s.epoch = ++epoch;
+        s.lg_hx = ilog2(a.L / a.bx / 2);
+        s.lg_pp = s.lg_hx + ilog2(a.L / a.by / 2);
+        cudaError_t e = cudaMemsetAsync(next_job, 0, sizeof(unsigned int), st);
+        if (e != cudaSuccess) return e;
+        const int njobs = 4 << s.lg_pp;
+        const bool mw = a.by > 16 * nt;
+        if (nt >= 4) e = mw ? launch_sweep_nt<(LFG_KPZ_NT >= 4 ? 4 : 1), true>(s, njobs, smem, st)
+                            : launch_sweep_nt<(LFG_KPZ_NT >= 4 ? 4 : 1), false>(s, njobs, smem, st);
+        else if (nt == 2) e = mw ? launch_sweep_nt<2, true>(s, njobs, smem, st) : launch_sweep_nt<2, false>(s, njobs, smem, st);
+        else e = mw ? launch_sweep_nt<1, true>(s, njobs, smem, st) : launch_sweep_nt<1, false>(s, njobs, smem, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 template <int NT, bool MW>

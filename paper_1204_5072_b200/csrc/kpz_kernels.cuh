@@ -29,6 +29,12 @@ struct KpzPhaseArgs {
 size_t kpz_phase_smem_bytes(int by);
 cudaError_t kpz_phase_kernel_attrs();
 cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st);
+// All four phases of sweep a.sweep in one persistent launch (resident lattice,
+// a.brow0 = 0, a.nbrow = L/by).  flags: [replicas][L/bx][L/by] u32 completion
+// epochs (any initial content); next_job: one u32 of scratch; epoch: per-handle
+// launch counter (incremented here).
+cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, uint32_t* flags,
+                             unsigned int* next_job, uint32_t& epoch, cudaStream_t st);
 cudaError_t kpz_launch_init_flat(uint32_t* f, int L, int replicas, cudaStream_t st);
 cudaError_t kpz_launch_init_zero_slopes(uint32_t* f, int L, int replicas, cudaStream_t st);
 cudaError_t kpz_launch_from_slopes(const uint32_t* X, const uint32_t* Y, int L, uint8_t* f0_scratch,

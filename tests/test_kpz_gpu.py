@@ -8,6 +8,8 @@ Tolerance: none -- integer/bit state must match exactly; W^2 is compared as
 the same double expression over exact int64 sums.
 """
 import hashlib
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -197,3 +199,41 @@ def test_large_lattice_matches_oracle_one_sweep(lfg, oracle):
             gx, gy = k.download()
         assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist()
         assert (gx == x).all() and (gy == y).all()
+
+
+_SWEEP_KERNEL_PROG = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_1204_5072_b200 as lfg
+out = []
+for (L, p, q, seed, bx, by, n) in json.loads(sys.argv[2]):
+    with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by) as k:
+        k.make_flat_slopes()
+        c = k.sweep(n)
+        x, y = k.download()
+        out.append([c.deposits, c.detaches, hashlib.sha256(x.tobytes() + y.tobytes()).hexdigest()])
+print(json.dumps(out))
+"""
+
+
+def test_sweep_kernel_matches_phase_launches(lfg):
+    """The persistent whole-sweep kernel (LFG_KPZ_SWEEP_KERNEL=1, flag-ordered
+    phases) reproduces the four-launch sweep bit for bit."""
+    import hashlib
+    import json
+    import subprocess
+
+    cases = [(2048, 1.0, 0.0, 5, 1024, 128, 3), (4096, 0.95, 0.05, 6, 1024, 64, 2), (1024, 1.0, 0.0, 7, 256, 32, 2)]
+    ref = []
+    for (L, p, q, seed, bx, by, n) in cases:
+        with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by) as k:
+            k.make_flat_slopes()
+            c = k.sweep(n)
+            x, y = k.download()
+            ref.append([c.deposits, c.detaches, hashlib.sha256(x.tobytes() + y.tobytes()).hexdigest()])
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LFG_KPZ_SWEEP_KERNEL="1")
+    r = subprocess.run([sys.executable, "-c", _SWEEP_KERNEL_PROG, root, json.dumps(cases)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1]) == ref
