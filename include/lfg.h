@@ -90,6 +90,16 @@ LFG_API int lfg_kpz_init_flat(lfg_kpz* h);
  * (the reference's reconstruct_heights error, kpz.cpp:42-44). */
 LFG_API int lfg_kpz_upload(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords);
 LFG_API int lfg_kpz_download(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size_t nwords);
+/* Stream-ordered variants (return after enqueueing on the handle's stream;
+ * host buffers must be pinned and stay untouched until lfg_kpz_synchronize):
+ * several handles on their own streams overlap one lattice's device->host
+ * copy with another's host->device copy (full-duplex PCIe).  The closure
+ * check of upload_async is deferred: lfg_kpz_upload_check synchronises and
+ * returns LFG_ECLOSURE if any upload since the last check was not integrable
+ * (the replica's state is then unspecified, unlike lfg_kpz_upload). */
+LFG_API int lfg_kpz_upload_async(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords);
+LFG_API int lfg_kpz_upload_check(lfg_kpz* h);
+LFG_API int lfg_kpz_download_async(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size_t nwords);
 
 /* kpz_sweep_sequential (kpz.cpp:5-19) replaced by n_mcs two-layer DTr sweeps.
  * out: NULL or an array of `replicas` counters for this call. */
@@ -106,6 +116,9 @@ LFG_API int lfg_kpz_reset_counters(lfg_kpz* h);
  * h(0,0)=0; W2 = sum2/n - (sum/n)^2 finished on the host exactly as kpz.cpp:78-80. */
 LFG_API int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2);
 LFG_API int lfg_kpz_interface_width(lfg_kpz* h, int32_t replica, double* w2);
+/* Stream-ordered W^2 sums: out3[0] = sum h, out3[1] + out3[2] = sum h^2
+ * (pinned host int64[3], valid after lfg_kpz_synchronize). */
+LFG_API int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3);
 /* reconstruct_heights (kpz.cpp:21-49): n = L*L int32, row-major j*L+i. */
 LFG_API int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n);
 

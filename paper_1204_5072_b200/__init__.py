@@ -108,6 +108,21 @@ class KpzLattice:
     def download_ptr(self, x_ptr: int, y_ptr: int, replica: int = 0) -> None:
         check(_native.lib().lfg_kpz_download(self._h, replica, x_ptr, y_ptr, words2(self.L)))
 
+    # stream-ordered host transfers (pinned pointers; complete at synchronize())
+    def upload_ptr_async(self, x_ptr: int, y_ptr: int, replica: int = 0) -> None:
+        check(_native.lib().lfg_kpz_upload_async(self._h, replica, x_ptr, y_ptr, words2(self.L)))
+
+    def upload_check(self) -> None:
+        """Raise ClosureError if an upload_ptr_async since the last check was not integrable."""
+        check(_native.lib().lfg_kpz_upload_check(self._h))
+
+    def download_ptr_async(self, x_ptr: int, y_ptr: int, replica: int = 0) -> None:
+        check(_native.lib().lfg_kpz_download_async(self._h, replica, x_ptr, y_ptr, words2(self.L)))
+
+    def width_sums_async(self, out3_ptr: int, replica: int = 0) -> None:
+        """Enqueue the W^2 scan; pinned int64[3] at out3_ptr holds (sum h, s2a, s2b) after synchronize()."""
+        check(_native.lib().lfg_kpz_width_sums_async(self._h, replica, out3_ptr))
+
     # -- dynamics ---------------------------------------------------------
     def sweep(self, sweeps: int = 1):
         """kpz_sweep_sequential(f, params, rng, sweeps) (kpz.cpp:5-19) -> Counters

@@ -303,33 +303,80 @@ int lfg_kpz_init_flat(lfg_kpz* h) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// H2D of the two slope planes + device conversion to spins (h->fnew) + the
+// closure re-derivation check (mismatches counted into h->dmis).
+void enqueue_upload(lfg_kpz* h, const uint64_t* x, const uint64_t* y) {
+    ensure_slope_scratch(h);
+    if (!h->f0) h->f0 = dmalloc<uint8_t>(size_t(h->L), "alloc scratch");
+    if (!h->fnew) h->fnew = dmalloc<uint32_t>(h->words_per_replica(), "alloc scratch");
+    if (!h->dmis) {
+        h->dmis = dmalloc<unsigned long long>(1, "alloc scratch");
+        cuda_check(cudaMemsetAsync(h->dmis, 0, 8, h->stream), "memset");
+    }
+    const size_t bytes = size_t(h->L) * h->L / 8;
+    cuda_check(cudaMemcpyAsync(h->sx, x, bytes, cudaMemcpyHostToDevice, h->stream), "upload x");
+    cuda_check(cudaMemcpyAsync(h->sy, y, bytes, cudaMemcpyHostToDevice, h->stream), "upload y");
+    cuda_check(kpz_launch_from_slopes(h->sx, h->sy, h->L, h->f0, h->fnew, h->stream), "slopes->spins");
+    cuda_check(kpz_launch_to_slopes(h->fnew, h->L, nullptr, nullptr, h->sx, h->sy, h->dmis, h->stream),
+               "closure check");
+}
+
+void check_upload_args(lfg_kpz* h, int32_t replica, const void* x, const void* y, size_t nwords) {
+    check_handle(h);
+    check_replica(h, replica);
+    const size_t need = size_t(h->L) * h->L / 64;
+    if (nwords != need || !x || !y)
+        throw Error(LFG_EINVAL, "upload: expected " + std::to_string(need) + " words per plane");
+}
+
+[[noreturn]] void throw_closure() {
+    throw Error(LFG_ECLOSURE, "reconstruct_heights: slope field violates closure; heights would be path-dependent");
+}
+
+}  // namespace
+
+extern "C" {
+
 int lfg_kpz_upload(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords) {
     return guarded([&] {
-        check_handle(h);
-        check_replica(h, replica);
-        const size_t need = size_t(h->L) * h->L / 64;
-        if (nwords != need || !x || !y)
-            throw Error(LFG_EINVAL, "upload: expected " + std::to_string(need) + " words per plane");
+        check_upload_args(h, replica, x, y, nwords);
         DeviceGuard g(h->device);
-        ensure_slope_scratch(h);
-        if (!h->f0) h->f0 = dmalloc<uint8_t>(size_t(h->L), "alloc scratch");
-        if (!h->fnew) h->fnew = dmalloc<uint32_t>(h->words_per_replica(), "alloc scratch");
         if (!h->dmis) h->dmis = dmalloc<unsigned long long>(1, "alloc scratch");
-        const size_t bytes = need * 8;
-        cuda_check(cudaMemcpyAsync(h->sx, x, bytes, cudaMemcpyHostToDevice, h->stream), "upload x");
-        cuda_check(cudaMemcpyAsync(h->sy, y, bytes, cudaMemcpyHostToDevice, h->stream), "upload y");
-        cuda_check(kpz_launch_from_slopes(h->sx, h->sy, h->L, h->f0, h->fnew, h->stream), "slopes->spins");
-        cuda_check(cudaMemsetAsync(h->dmis, 0, 8, h->stream), "memset");
-        cuda_check(kpz_launch_to_slopes(h->fnew, h->L, nullptr, nullptr, h->sx, h->sy, h->dmis, h->stream),
-                   "closure check");
+        cuda_check(cudaMemsetAsync(h->dmis, 0, 8, h->stream), "memset");  // (a pending async failure is superseded)
+        enqueue_upload(h, x, y);
         cuda_check(cudaMemcpyAsync(h->hpin, h->dmis, 8, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
-        if (h->hpin[0] != 0)
-            throw Error(LFG_ECLOSURE,
-                        "reconstruct_heights: slope field violates closure; heights would be path-dependent");
+        if (h->hpin[0] != 0) throw_closure();  // state unchanged
         cuda_check(cudaMemcpyAsync(h->rep(replica), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice,
                                    h->stream), "commit");
         sync(h);
+    });
+}
+
+int lfg_kpz_upload_async(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_t* y, size_t nwords) {
+    return guarded([&] {
+        check_upload_args(h, replica, x, y, nwords);
+        DeviceGuard g(h->device);
+        enqueue_upload(h, x, y);  // mismatches accumulate in dmis until lfg_kpz_upload_check
+        cuda_check(cudaMemcpyAsync(h->rep(replica), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice,
+                                   h->stream), "commit");
+    });
+}
+
+int lfg_kpz_upload_check(lfg_kpz* h) {
+    return guarded([&] {
+        check_handle(h);
+        DeviceGuard g(h->device);
+        if (!h->dmis) return;
+        cuda_check(cudaMemcpyAsync(h->hpin, h->dmis, 8, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        cuda_check(cudaMemsetAsync(h->dmis, 0, 8, h->stream), "memset");
+        sync(h);
+        if (h->hpin[0] != 0) throw_closure();
     });
 }
 
@@ -347,6 +394,22 @@ int lfg_kpz_download(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size
         cuda_check(cudaMemcpyAsync(x, h->sx, need * 8, cudaMemcpyDeviceToHost, h->stream), "download x");
         cuda_check(cudaMemcpyAsync(y, h->sy, need * 8, cudaMemcpyDeviceToHost, h->stream), "download y");
         sync(h);
+    });
+}
+
+int lfg_kpz_download_async(lfg_kpz* h, int32_t replica, uint64_t* x, uint64_t* y, size_t nwords) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        const size_t need = size_t(h->L) * h->L / 64;
+        if (nwords != need || !x || !y)
+            throw Error(LFG_EINVAL, "download: expected " + std::to_string(need) + " words per plane");
+        DeviceGuard g(h->device);
+        ensure_slope_scratch(h);
+        cuda_check(kpz_launch_to_slopes(h->rep(replica), h->L, h->sx, h->sy, nullptr, nullptr, nullptr, h->stream),
+                   "spins->slopes");
+        cuda_check(cudaMemcpyAsync(x, h->sx, need * 8, cudaMemcpyDeviceToHost, h->stream), "download x");
+        cuda_check(cudaMemcpyAsync(y, h->sy, need * 8, cudaMemcpyDeviceToHost, h->stream), "download y");
     });
 }
 
@@ -435,6 +498,20 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         sync(h);
         *sum = int64_t(h->hpin[0]);
         *sum2 = int64_t(h->hpin[1] + h->hpin[2]);
+    });
+}
+
+int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3) {
+    return guarded([&] {
+        check_handle(h);
+        check_replica(h, replica);
+        if (!out3) throw Error(LFG_EINVAL, "null output");
+        DeviceGuard g(h->device);
+        ensure_width_scratch(h);
+        cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
+        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->seglen, h->wout, h->stream),
+                   "width scan");
+        cuda_check(cudaMemcpyAsync(out3, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
     });
 }
 

@@ -237,3 +237,58 @@ def test_sweep_kernel_matches_phase_launches(lfg):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert json.loads(r.stdout.strip().splitlines()[-1]) == ref
+
+
+def test_async_transfers_match_sync_calls(lfg, oracle):
+    """upload_async / sweep_async / width_sums_async / download_async on two
+    handles with their own streams == the synchronous calls."""
+    import torch
+
+    L = 2048
+    x0, y0 = oracle.kpz_flat(L)
+    ref = []
+    for seed in (31, 32):
+        with lfg.KpzLattice(L, 0.95, 0.05, seed) as k:
+            k.upload(x0, y0)
+            k.sweep(2)
+            ref.append((k.width_sums(), *k.download()))
+    ks = [lfg.KpzLattice(L, 0.95, 0.05, seed) for seed in (31, 32)]
+    sts = [torch.cuda.Stream() for _ in ks]
+    hx = [torch.from_numpy(x0.view(np.int64).copy()).pin_memory() for _ in ks]
+    hy = [torch.from_numpy(y0.view(np.int64).copy()).pin_memory() for _ in ks]
+    o3 = torch.zeros((2, 3), dtype=torch.int64).pin_memory()
+    try:
+        for i, k in enumerate(ks):
+            k.set_stream(sts[i].cuda_stream)
+        for _ in range(2):
+            for i, k in enumerate(ks):
+                k.upload_ptr_async(hx[i].data_ptr(), hy[i].data_ptr())
+                k.sweep_async(1)
+                k.width_sums_async(o3[i].data_ptr())
+                k.download_ptr_async(hx[i].data_ptr(), hy[i].data_ptr())
+        for i, k in enumerate(ks):
+            k.synchronize()
+            k.upload_check()
+            s, s2 = int(o3[i, 0]), int(o3[i, 1]) + int(o3[i, 2])
+            # each step re-uploads the previous step's download: 2 sweeps from the flat start
+            assert (s, s2) == tuple(ref[i][0])
+            assert np.array_equal(hx[i].numpy().view(np.uint64), ref[i][1])
+            assert np.array_equal(hy[i].numpy().view(np.uint64), ref[i][2])
+    finally:
+        for k in ks:
+            k.close()
+
+
+def test_upload_async_check_reports_closure(lfg, oracle):
+    import torch
+
+    L = 64
+    x, y = oracle.kpz_flat(L)
+    x[3] ^= np.uint64(1 << 5)
+    hx = torch.from_numpy(x.view(np.int64).copy()).pin_memory()
+    hy = torch.from_numpy(y.view(np.int64).copy()).pin_memory()
+    with lfg.KpzLattice(L) as k:
+        k.upload_ptr_async(hx.data_ptr(), hy.data_ptr())
+        with pytest.raises(lfg.ClosureError, match="closure"):
+            k.upload_check()
+        k.upload_check()  # the failure was reported once
