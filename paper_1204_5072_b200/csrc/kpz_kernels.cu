@@ -101,36 +101,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 
-// FMA-pipe integer ops (IMAD.HI / IMAD / IMAD.SHL), kept as such so that the
-// ALU pipe (LOP3/SHF, half rate per SMSP) only carries the pattern logic.
-__device__ __forceinline__ uint32_t mulhi_u32(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
+// FMA-pipe shift (IMAD.SHL): keeps the anchor-field advance off the ALU pipe.
 __device__ __forceinline__ uint32_t mullo_u32(uint32_t a, uint32_t b) {
     uint32_t d;
     asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
     return d;
 }
-__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
 
-#ifndef LFG_KPZ_HALFSHIFT
-#define LFG_KPZ_HALFSHIFT 0
-#endif
-#ifndef LFG_KPZ_LUT
-#define LFG_KPZ_LUT 0
-#endif
-#ifndef LFG_KPZ_IMADDR
-#define LFG_KPZ_IMADDR 0
-#endif
-#ifndef LFG_KPZ_SWITCH
-#define LFG_KPZ_SWITCH 0
-#endif
 
 template <bool MW>
 __device__ __forceinline__ void round_barrier() {
@@ -155,9 +132,6 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
                                                   uint32_t& ndep, uint32_t& ndet) {
     uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
-#if LFG_KPZ_LUT
-    uint32_t bitw[NT];
-#endif
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
         const uint32_t pw = addr[n] + (HY << 11);
@@ -165,26 +139,12 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
         nb[n] = lds32(HX ? pw + 4u : pw - 4u);
         up[n] = lds32(pw + 256);
         dn[n] = lds32(pw - 256);
-#if LFG_KPZ_LUT
-        bitw[n] = lds32(xd[n] + (HX << 6));  // xd holds the LUT address of 1 << xd
-#endif
     }
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
-#if LFG_KPZ_HALFSHIFT
-        // Only the active half's 16 bits matter: the shift towards the inside of
-        // the word needs no neighbour bit and runs on the FMA pipe.
-        const uint32_t Rw = HX ? __funnelshift_r(own[n], nb[n], 1) : mulhi_u32(own[n], 0x80000000u);
-        const uint32_t Lw = HX ? mullo_u32(own[n], 2u) : __funnelshift_l(nb[n], own[n], 1);
-#else
         const uint32_t Rw = __funnelshift_r(own[n], nb[n], 1);  // bit i = f(i+1)
         const uint32_t Lw = __funnelshift_l(nb[n], own[n], 1);  // bit i = f(i-1)
-#endif
-#if LFG_KPZ_LUT
-        const uint32_t bit = bitw[n];
-#else
         const uint32_t bit = (HX ? 0x10000u : 1u) << xd[n];
-#endif
         if (!GENERAL) {
             const uint32_t flip = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), bit);
             res[n] = own[n] ^ flip;
@@ -216,8 +176,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
 template <bool GENERAL, bool FULL, int NT, bool MW>
 __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT], bool active, uint64_t seed,
                                                  uint64_t sweep, uint32_t block_id, const uint32_t (&tile_id)[NT],
-                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet,
-                                                 uint32_t lut) {
+                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
 #pragma unroll 1
     for (int m4 = 0; m4 < kRounds / 64; ++m4) {
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
@@ -249,31 +208,13 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
                         uint32_t addr[NT], xd[NT], u[NT];
 #pragma unroll
                         for (int n = 0; n < NT; ++n) {
-#if LFG_KPZ_LUT
-                            xd[n] = mad_u32(mulhi_u32(xw[n], 16u), 4u, lut);  // LUT address of 1 << field
-#else
                             xd[n] = __umulhi(xw[n], 16u);  // top 4 bits, then advance
-#endif
                             xw[n] = mullo_u32(xw[n], 16u);
-#if LFG_KPZ_IMADDR
-                            // row field at the top of yw: address = field * 256 + base (FMA pipe)
-                            addr[n] = mad_u32(mulhi_u32(yw[n], 8u), 256u, lane_base[n]);
-                            yw[n] = mullo_u32(yw[n], 8u);
-#else
                             // row field k of this quarter -> bits 8..10 (bits above masked by the LOP3)
                             addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u << (3 * k)), 0x700u);
-#endif
                             u[n] = GENERAL ? sel4(Uw[n], k) : 0u;
                         }
                         if (FULL || active) {
-#if LFG_KPZ_SWITCH
-                            switch (setw & 3u) {
-                                case 0: kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
-                                case 1: kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
-                                case 2: kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
-                                default: kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet); break;
-                            }
-#else
                             if (setw & 2u) {
                                 if (setw & 1u)
                                     kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
@@ -285,15 +226,12 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
                                 else
                                     kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
                             }
-#endif
                         }
                         setw >>= 2;
                         round_barrier<MW>();
                     }
-#if !LFG_KPZ_IMADDR
 #pragma unroll
                     for (int n = 0; n < NT; ++n) yw[n] <<= 12;  // next 4 row fields
-#endif
                 }
             }
         }
@@ -423,9 +361,6 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
             }
         }
     }
-    // One-hot LUT (line 6, words 16..47, one bank per entry): lut[i] = 1 << i.
-    const uint32_t lut = smA + 6u * 256u + 64u;
-    if (LFG_KPZ_LUT && threadIdx.x < 32) sm[6 * 64 + 16 + threadIdx.x] = 1u << threadIdx.x;
     __syncthreads();
 
     const int tx = lane;
@@ -438,7 +373,7 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
     }
     uint32_t ndep = 0, ndet = 0;
     kpz_block_rounds<GENERAL, FULL, kNT, MW>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP, a.thrQ,
-                                             ndep, ndet, lut);
+                                             ndep, ndet);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     if (FULL) {
         for (int R = warp; R < a.by; R += nwarps) {

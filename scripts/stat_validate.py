@@ -101,6 +101,7 @@ def main():
     ap.add_argument("--beta-lo", type=int, default=32)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-ref", action="store_true")
+    ap.add_argument("--save-samples", action="store_true", help="store per-seed W^2(t) and <h>(t)")
     a = ap.parse_args()
     ts = sample_times(a.t)
     seeds = [1000003 * (i + 1) for i in range(a.seeds)]
@@ -110,6 +111,16 @@ def main():
     rep = {"L": a.L, "p": a.p, "q": a.q, "t": ts, "gpu_seeds": a.seeds, "gpu_seconds": tg,
            "gpu": {"w2_mean": gw.mean(0).tolist(), "w2_se": (gw.std(0, ddof=1) / math.sqrt(len(seeds))).tolist(),
                    "h_mean": gh.mean(0).tolist(), "h_se": (gh.std(0, ddof=1) / math.sqrt(len(seeds))).tolist()}}
+    if a.save_samples:
+        rep["gpu"]["w2"] = gw.tolist()
+        rep["gpu"]["h"] = gh.tolist()
+    if a.no_ref:
+        lo, hi = a.beta_lo, a.t
+        sg = per_seed_beta(ts, gw, lo, hi)
+        rep["beta"] = {"window": [lo, hi], "estimator": "slope of log <W^2> vs log t, /2",
+                       "gpu": beta_fit(ts, gw.mean(0), lo, hi),
+                       "gpu_per_seed_mean": float(sg.mean()) if len(sg) else None,
+                       "gpu_per_seed_se": float(sg.std(ddof=1) / math.sqrt(len(sg))) if len(sg) > 1 else None}
     if not a.no_ref:
         nref = a.ref_seeds or a.seeds
         t0 = time.time()
