@@ -249,8 +249,24 @@ class DistComm:
         self.stage = dist.get_backend(group) == "gloo" and getattr(engine.buf, "is_cuda", False)
 
     def exchange(self, ops):
+        """Post the matched sends/receives of this rank.  Device buffers over NCCL:
+        the P2P ops are ordered after the work already on the engine's stream and
+        the stream waits for them on the device (no host synchronisation), so the
+        next phase kernel on that stream consumes the received rows in order.
+        gloo with device buffers stages through host memory (synchronous)."""
         dist = self.dist
         e = self.engine
+        if not ops:
+            return
+        on_device = getattr(e.buf, "is_cuda", False)
+        if on_device and not self.stage:
+            torch = e.torch
+            with torch.cuda.stream(e.stream):
+                p2p = [dist.P2POp(dist.isend if kind == "send" else dist.irecv, e.rows(slot, m), peer, self.group)
+                       for kind, peer, b, n in ops for (slot, m) in e.plan.pieces(b, n)]
+                for w in dist.batch_isend_irecv(p2p):
+                    w.wait()  # stream-ordered wait on the engine's stream
+            return
         e.sync()
         p2p, unstage = [], []
         for kind, peer, b, n in ops:
@@ -267,7 +283,7 @@ class DistComm:
                 w.wait()
         for t, h in unstage:
             t.copy_(h)
-        if hasattr(e, "torch") and e.buf.is_cuda:
+        if on_device:
             e.torch.cuda.current_stream(e.buf.device).synchronize()
 
 
