@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--L", type=int, default=1 << 16)
+    ap.add_argument("--L", type=int, default=0,
+                    help="lattice edge (0: 2^16 = configs[1] at N=1; 2^17 = configs[2]'s strip-sharded lattice at N>1)")
     ap.add_argument("--p", type=float, default=1.0)
     ap.add_argument("--q", type=float, default=0.0)
     ap.add_argument("--seed", type=int, default=1)
@@ -50,7 +51,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kmc", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.L == 0:
+        a.L = (1 << 16) if int(os.environ.get("WORLD_SIZE", "1")) == 1 else (1 << 17)
+    return a
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -441,10 +445,13 @@ def run_b200(args):
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            eng.buf.copy_(hbuf, non_blocking=True)
+            with torch.cuda.stream(eng.stream):       # ordered before the phase kernels / exchanges
+                eng.buf.copy_(hbuf, non_blocking=True)
             sk.sweep(1)
             w2 = sk.interface_width()
-            hbuf.copy_(eng.buf)
+            with torch.cuda.stream(eng.stream):
+                hbuf.copy_(eng.buf, non_blocking=True)
+            eng.sync()
         barrier()
         dt = time.perf_counter() - t0
         t = torch.tensor([dt], device="cuda")
@@ -472,10 +479,13 @@ def run_b200(args):
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (flat start)",
                 "config": {"workload": f"KPZ octahedron DTr, L={L}x{L}, p={args.p}, q={args.q}, flat start, "
-                                       f"1 MCS per step (BASELINE.json configs[1])",
+                                       f"1 MCS per step (BASELINE.json "
+                                       + ("configs[1])" if world == 1 else
+                                          "configs[2]'s strip-sharded L=2^17 lattice; p, q of the metric)"),
                            "plan": {"block_x": plan[0], "block_y": plan[1], "domain": "16x8"},
                            "parallelism": mode,
-                           "l2": "lattice 512 MiB >> 126 MB L2: no flush needed"},
+                           "l2": f"lattice {L * L // 8 >> 20} MiB ({L * L // 8 // world >> 20} MiB per GPU) >> 126 MB L2: "
+                                 f"no flush needed"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": 4 * args.steps, "kmc": kmc}
         print(json.dumps(line), flush=True)

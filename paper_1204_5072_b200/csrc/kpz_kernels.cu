@@ -438,8 +438,11 @@ struct KpzSweepArgs {
                                // job -> block mapping on the uniform datapath (no division)
 };
 
+#ifndef LFG_KPZ_SWEEP_MINB
+#define LFG_KPZ_SWEEP_MINB 6
+#endif
 template <bool GENERAL, bool FULL, int kNT, bool MW>
-__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
+__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : LFG_KPZ_SWEEP_MINB) : 12)
     kpz_dtr_sweep_kernel(const __grid_constant__ KpzSweepArgs s) {
     extern __shared__ __align__(16) uint32_t sm_raw[];
     const KpzPhaseArgs& a = s.p;
@@ -475,10 +478,15 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
         parity ^= 1u;
         first = false;
         __syncthreads();  // every warp's write-back issued before the release
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release_u32(fl + byi * nbx + bxi, s.epoch);
-        }
+        // thread 0 publishes; predicated inside one asm block so the loop keeps a
+        // branch-free (uniform) control flow for the next activation
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.eq.u32 p, %2, 0;\n\t"
+            "@p fence.acq_rel.gpu;\n\t"
+            "@p st.release.gpu.global.u32 [%0], %1;\n\t}" ::"l"(fl + byi * nbx + bxi),
+            "r"(s.epoch), "r"(uint32_t(threadIdx.x))
+            : "memory");
     }
 }
 
