@@ -1,0 +1,103 @@
+"""SPEC.md acceptance criteria that concern the B200 path (run with -m gpu).
+
+ 3. KMC quench observable: L=64, c=0.325, eps=1.5, 1000 MCS, >= 5 seeds: first sample within
+    8.1 +- 0.15, windowed mean decreases by >= 15 % by MCS 1000.
+ 5. Scheduler fidelity (KMC): L=32, c=0.325, eps=1.5, 500 MCS, 50 realizations: the DT mean
+    trajectory within 3 combined standard errors of the reference's sequential sweep
+    (kmc_mcs_sequential from the unmodified sources) at t in {10, 100, 500}.
+ 6. Conservation: KPZ row sums of sigma_x and column sums of sigma_y, and the KMC B count,
+    unchanged after 10^4 MCS, exactly.
+"""
+import math
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lfg():
+    import paper_1204_5072_b200 as m
+
+    if m.device_count() < 1:
+        pytest.fail("no CUDA device visible to liblfg.so")
+    return m
+
+
+def test_acceptance3_kmc_quench(lfg):
+    first, last = [], []
+    for s in range(5):
+        with lfg.KmcLattice(64, 1.5, False, 100 + s) as k:
+            k.make_random_alloy(0.325, 17 + s)
+            first.append(k.open_bonds_per_particle())
+            win = []
+            done = 0
+            for t in (900, 925, 950, 975, 1000):  # windowed mean near MCS 1000
+                k.sweep(t - done)
+                done = t
+                win.append(k.open_bonds_per_particle())
+            last.append(float(np.mean(win)))
+    for f in first:
+        assert abs(f - 8.1) <= 0.15
+    assert np.mean(last) <= 0.85 * np.mean(first)
+
+
+def _ref_traj(seed):
+    import pyoracle
+
+    ref = pyoracle.RefLib()
+    w, st = ref.make_random_alloy(32, 0.325, "lcg64", seed)
+    out, t = [], 0
+    for tt in (10, 100, 500):
+        _, st = ref.kmc_sweep_sequential(32, w, 1.5, False, "lcg64", st, tt - t)
+        t = tt
+        out.append(ref.open_bonds_per_particle(32, w))
+    return out
+
+
+def test_acceptance5_kmc_scheduler_fidelity(lfg, reflib):
+    n = 50
+    gpu = np.zeros((n, 3))
+    for r in range(n):
+        with lfg.KmcLattice(32, 1.5, False, 1000 + r) as k:
+            k.make_random_alloy(0.325, 5000 + r)
+            done = 0
+            for j, t in enumerate((10, 100, 500)):
+                k.sweep(t - done)
+                done = t
+                gpu[r, j] = k.open_bonds_per_particle()
+    with ProcessPoolExecutor() as ex:
+        ref = np.array(list(ex.map(_ref_traj, [7 * r + 3 for r in range(n)])))
+    se = np.sqrt(gpu.var(0, ddof=1) / n + ref.var(0, ddof=1) / n)
+    z = (gpu.mean(0) - ref.mean(0)) / se
+    assert np.all(np.abs(z) <= 3.0), (gpu.mean(0), ref.mean(0), z)
+
+
+def test_acceptance6_conservation_1e4_mcs(lfg, oracle):
+    L = 256
+    with lfg.KpzLattice(L, 0.95, 0.05, 77) as k:
+        k.make_flat_slopes()
+        x0, y0 = k.download()
+        c = k.sweep(10000)
+        assert c.attempts == 10000 * L * L
+        x, y = k.download()
+
+    def row_sums_x(words):  # sum_i sigma_x(i, j) for every row j (bit 1 <=> +1)
+        b = np.unpackbits(words.view(np.uint8), bitorder="little").reshape(L, L).astype(np.int64)
+        return (2 * b - 1).sum(axis=1)
+
+    def col_sums_y(words):  # sum_j sigma_y(i, j) for every column i
+        b = np.unpackbits(words.view(np.uint8), bitorder="little").reshape(L, L).astype(np.int64)
+        return (2 * b - 1).sum(axis=0)
+
+    assert np.array_equal(row_sums_x(x), row_sums_x(x0))
+    assert np.array_equal(col_sums_y(y), col_sums_y(y0))
+    assert oracle.closure_holds(L, x, y)
+    with lfg.KmcLattice(32, 1.5, True, 5) as m:
+        m.make_random_alloy(0.5, 9)
+        n0 = m.count_b()
+        cm = m.sweep(10000)
+        assert cm.attempts == 10000 * 32 ** 3 // 2 and cm.successes > 0
+        assert m.count_b() == n0
