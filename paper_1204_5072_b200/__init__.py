@@ -57,6 +57,8 @@ class KpzLattice:
         self.L = int(L)
         self.replicas = len(seeds)
         self.device = device
+        self.p, self.q, self.seeds = float(p), float(q), list(seeds)
+        self._cnt_base = [(0, 0, 0)] * len(seeds)  # (attempts, deposits, detaches) restored by load()
         got = KpzPlan()
         check(L_.lfg_kpz_get_plan(h, C.byref(got)))
         self.plan = (int(got.block_x), int(got.block_y))
@@ -140,10 +142,32 @@ class KpzLattice:
     def counters(self, replica: int = 0) -> Counters:
         c = Counters()
         check(_native.lib().lfg_kpz_counters(self._h, replica, C.byref(c)))
+        a0, d0, e0 = self._cnt_base[replica]
+        if a0 or d0 or e0:
+            c.attempts += a0
+            c.deposits += d0
+            c.detaches += e0
+            c.successes += d0 + e0
         return c
 
     def reset_counters(self) -> None:
         check(_native.lib().lfg_kpz_reset_counters(self._h))
+        self._cnt_base = [(0, 0, 0)] * self.replicas
+
+    # -- snapshot / exact resume ------------------
+    def save(self, path: str) -> None:
+        """Snapshot: the reference's slope planes of every replica + (p, q, seeds, plan,
+        next sweep index, counters).  The counter-based RNG makes load() + sweep(n) continue
+        the trajectory bit for bit."""
+        from .snapshot import save_kpz
+
+        save_kpz(self, path)
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "KpzLattice":
+        from .snapshot import load_kpz
+
+        return load_kpz(path, device)
 
     # -- observables ------------------------------------------------------
     def width_sums(self, replica: int = 0):
@@ -166,6 +190,7 @@ class KpzLattice:
     # -- state / plumbing -------------------------------------------------
     def set_params(self, p: float, q: float) -> None:
         check(_native.lib().lfg_kpz_set_params(self._h, float(p), float(q)))
+        self.p, self.q = float(p), float(q)
 
     @property
     def sweep_index(self) -> int:
@@ -179,6 +204,7 @@ class KpzLattice:
 
     def set_seed(self, seed: int, replica: int = 0) -> None:
         check(_native.lib().lfg_kpz_set_seed(self._h, replica, int(seed)))
+        self.seeds[replica] = int(seed)
 
     def set_stream(self, stream_ptr: int) -> None:
         check(_native.lib().lfg_kpz_set_stream(self._h, C.c_void_p(stream_ptr)))
@@ -208,6 +234,8 @@ class KmcLattice:
         self._h = h
         self.L = int(L)
         self.device = device
+        self.eps, self.both_active, self.seed = float(eps), bool(both_active), int(seed)
+        self._cnt_base = (0, 0)  # (attempts, exchanges) restored by load()
         got = KmcPlan()
         check(L_.lfg_kmc_get_plan(h, C.byref(got)))
         self.plan = int(got.block)
@@ -262,10 +290,29 @@ class KmcLattice:
     def counters(self) -> Counters:
         c = Counters()
         check(_native.lib().lfg_kmc_counters(self._h, C.byref(c)))
+        a0, s0 = self._cnt_base
+        if a0 or s0:
+            c.attempts += a0
+            c.successes += s0
+            c.deposits += s0
         return c
 
     def reset_counters(self) -> None:
         check(_native.lib().lfg_kmc_reset_counters(self._h))
+        self._cnt_base = (0, 0)
+
+    def save(self, path: str) -> None:
+        """Snapshot: occupancy words (reference layout) + (eps, mode, seed, plan, next sweep
+        index, counters); load() + sweep(n) continues bit for bit."""
+        from .snapshot import save_kmc
+
+        save_kmc(self, path)
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "KmcLattice":
+        from .snapshot import load_kmc
+
+        return load_kmc(path, device)
 
     def open_bond_sums(self):
         a, b = C.c_int64(), C.c_int64()
@@ -285,6 +332,7 @@ class KmcLattice:
 
     def set_params(self, eps: float, both_active: bool) -> None:
         check(_native.lib().lfg_kmc_set_params(self._h, float(eps), int(bool(both_active))))
+        self.eps, self.both_active = float(eps), bool(both_active)
 
     @property
     def sweep_index(self) -> int:
@@ -298,6 +346,7 @@ class KmcLattice:
 
     def set_seed(self, seed: int) -> None:
         check(_native.lib().lfg_kmc_set_seed(self._h, int(seed)))
+        self.seed = int(seed)
 
     def set_stream(self, stream_ptr: int) -> None:
         check(_native.lib().lfg_kmc_set_stream(self._h, C.c_void_p(stream_ptr)))
