@@ -119,6 +119,14 @@ LFG_API int lfg_kpz_interface_width(lfg_kpz* h, int32_t replica, double* w2);
 /* Stream-ordered W^2 sums: out3[0] = sum h, out3[1] + out3[2] = sum h^2
  * (pinned host int64[3], valid after lfg_kpz_synchronize). */
 LFG_API int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3);
+/* Debug instrumentation for the write-disjointness check (the
+ * reference's WriteLog, write_log.hpp:10-60): while enabled, every sweep
+ * writes one uint32 record per attempt into dev_buf (device memory, >= L*L
+ * words; phase k at offset k*L*L/4, then [512 rounds][tiles of the launch]):
+ * global tile id (bits 0-19), anchor column in the domain xd (20-23), row yd
+ * (24-26), inner set hx (27) / hy (28), accepted (29).  Single-replica handles
+ * with block_x < 1024; dev_buf = NULL disables.  Uses the per-phase kernels. */
+LFG_API int lfg_kpz_debug_record_anchors(lfg_kpz* h, void* dev_buf, size_t capacity_words);
 /* reconstruct_heights (kpz.cpp:21-49): n = L*L int32, row-major j*L+i. */
 LFG_API int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n);
 

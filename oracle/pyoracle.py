@@ -222,6 +222,8 @@ class RefLib:
         _sig(lib, "ref_metropolis_prob", I, I, I, D, C.POINTER(D))
         _sig(lib, "ref_fcc_neighbors", I, I32, I32, I32, I32, i32p)
         _sig(lib, "ref_schedule_ahead_of_time_steps", I, I32, I32, I32, i32p, I32, C.POINTER(I32))
+        _sig(lib, "ref_writelog_violations", I, I32, I64, i64p, i32p, i64p, i64p, C.POINTER(I64),
+             C.POINTER(I64), i64p)
 
     def _check(self, rc):
         if rc != 0:
@@ -332,6 +334,17 @@ class RefLib:
         o = C.c_int64()
         self._check(self.lib.ref_count_b(L, w, C.byref(o)))
         return o.value
+
+    def writelog_violations(self, workers, group_off, task_worker, task_woff, write_site):
+        """lf::WriteLog over a recorded schedule (groups = barrier intervals); returns
+        (violations, writes, first violation (site, worker_a, worker_b) or None)."""
+        nv, nw = C.c_int64(), C.c_int64()
+        first = np.zeros(3, np.int64)
+        self._check(self.lib.ref_writelog_violations(
+            int(workers), len(group_off) - 1, np.ascontiguousarray(group_off, np.int64),
+            np.ascontiguousarray(task_worker, np.int32), np.ascontiguousarray(task_woff, np.int64),
+            np.ascontiguousarray(write_site, np.int64), C.byref(nv), C.byref(nw), first))
+        return nv.value, nw.value, (tuple(int(v) for v in first) if nv.value else None)
 
     def metropolis_prob(self, ni, nf, eps):
         o = C.c_double()

@@ -13,6 +13,7 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "lf/counters.hpp"
 #include "lf/kmc.hpp"
@@ -20,6 +21,7 @@
 #include "lf/lattice.hpp"
 #include "lf/rng.hpp"
 #include "lf/schedule.hpp"
+#include "lf/write_log.hpp"
 
 #include "oracle_core.hpp"
 
@@ -364,6 +366,39 @@ int ref_schedule_ahead_of_time_steps(int32_t blocks, int32_t workers, int32_t se
         auto s = lf::schedule_ahead_of_time(blocks, workers, sets);
         *n = int32_t(s.size());
         for (size_t k = 0; k < s.size() && int32_t(k) < cap; ++k) sizes[k] = int32_t(s[k].size());
+    });
+}
+
+// ------------------------------------------------------------------ write log
+// Drive the reference's lf::WriteLog (write_log.hpp:16-49) with a recorded
+// schedule.  Groups are barrier intervals: every task of a group is begun
+// before any of the group's writes is logged and all are ended afterwards, so
+// tasks of one group are mutually concurrent and groups are ordered.  Returns
+// the number of violations (same site written by distinct workers in
+// overlapping tasks) and the first one.
+int ref_writelog_violations(int32_t workers, int64_t ngroups, const int64_t* group_off, const int32_t* task_worker,
+                            const int64_t* task_woff, const int64_t* write_site, int64_t* nviol, int64_t* nwrites,
+                            int64_t* first3) {
+    return guarded([&] {
+        lf::WriteLog log(workers);
+        std::vector<int32_t> tid;
+        for (int64_t g = 0; g < ngroups; ++g) {
+            const int64_t t0 = group_off[g], t1 = group_off[g + 1];
+            tid.assign(size_t(t1 - t0), 0);
+            for (int64_t t = t0; t < t1; ++t) tid[size_t(t - t0)] = log.begin_task(task_worker[t]);
+            for (int64_t t = t0; t < t1; ++t)
+                for (int64_t w = task_woff[t]; w < task_woff[t + 1]; ++w)
+                    log.log_write(task_worker[t], tid[size_t(t - t0)], write_site[w]);
+            for (int64_t t = t0; t < t1; ++t) log.end_task(task_worker[t], tid[size_t(t - t0)]);
+        }
+        const auto v = log.violations();
+        *nviol = int64_t(v.size());
+        *nwrites = log.write_count();
+        if (!v.empty()) {
+            first3[0] = v[0].site;
+            first3[1] = v[0].worker_a;
+            first3[2] = v[0].worker_b;
+        }
     });
 }
 

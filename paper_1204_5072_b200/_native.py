@@ -107,6 +107,7 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_upload_check", P)
     _sig(L, "lfg_kpz_download_async", P, I32, P, P, SZ)
     _sig(L, "lfg_kpz_width_sums_async", P, I32, P)
+    _sig(L, "lfg_kpz_debug_record_anchors", P, P, SZ)
     _sig(L, "lfg_kpz_sweep", P, I64, C.POINTER(Counters))
     _sig(L, "lfg_kpz_sweep_async", P, I64)
     _sig(L, "lfg_kpz_phase", P, U64, I32)

@@ -52,6 +52,7 @@ struct lfg_kpz {
     unsigned long long* wout = nullptr;     // [3]
     bool strip_only = false;                // created by lfg_kpz_create_strip: no resident lattice
     int32_t* hbuf = nullptr;                // [L][L] heights (small L)
+    uint32_t* wlog = nullptr;               // debug anchor records ([4 phases][L^2/4]) or nullptr
     uint32_t* flags = nullptr;              // [R][L/bx][L/by] whole-sweep kernel completion epochs
     unsigned int* next_job = nullptr;       // whole-sweep kernel claim counter
     uint32_t epoch = 0;
@@ -158,13 +159,14 @@ void enqueue_sweeps(lfg_kpz* h, int64_t n) {
     }
     for (int64_t s = 0; s < n; ++s) {
         a.sweep = h->sweep + uint64_t(s);
-        if (sweep_kernel_enabled()) {
+        if (sweep_kernel_enabled() && !h->wlog) {
             cuda_check(kpz_launch_sweep(a, h->seeds.data(), h->R, h->flags, h->next_job, h->epoch, h->stream),
                        "kpz_dtr_sweep launch");
             continue;
         }
         for (int k = 0; k < 4; ++k) {
             a.phase = k;
+            a.wlog = h->wlog ? h->wlog + size_t(k) * (size_t(h->L) * h->L / 4) : nullptr;
             cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
         }
     }
@@ -498,6 +500,22 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         sync(h);
         *sum = int64_t(h->hpin[0]);
         *sum2 = int64_t(h->hpin[1] + h->hpin[2]);
+    });
+}
+
+int lfg_kpz_debug_record_anchors(lfg_kpz* h, void* dev_buf, size_t capacity_words) {
+    return guarded([&] {
+        check_handle(h);
+        check_resident(h);
+        if (!dev_buf) {
+            h->wlog = nullptr;
+            return;
+        }
+        if (h->R != 1) throw Error(LFG_EINVAL, "debug_record_anchors: single-replica handles only");
+        if (h->bx >= 1024) throw Error(LFG_EINVAL, "debug_record_anchors: needs a plan with block_x < 1024");
+        if (capacity_words < size_t(h->L) * h->L)
+            throw Error(LFG_EINVAL, "debug_record_anchors: buffer must hold L*L words (one sweep)");
+        h->wlog = static_cast<uint32_t*>(dev_buf);
     });
 }
 

@@ -130,7 +130,7 @@ __device__ __forceinline__ void round_barrier() {
 template <int HX, int HY, bool GENERAL, int NT>
 __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
-                                                  uint32_t& ndep, uint32_t& ndet) {
+                                                  uint32_t& ndep, uint32_t& ndet, uint32_t (&acc)[NT]) {
     uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -149,6 +149,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
             const uint32_t flip = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), bit);
             res[n] = own[n] ^ flip;
             count_if_nonzero(ndep, flip);
+            acc[n] = flip;
         } else {
             const uint32_t okP = uint64_t(u[n]) < thrP ? bit : 0u;
             const uint32_t okQ = uint64_t(u[n]) < thrQ ? bit : 0u;
@@ -157,6 +158,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
             res[n] = own[n] ^ (dep | det);
             count_if_nonzero(ndep, dep);
             count_if_nonzero(ndet, det);
+            acc[n] = dep | det;
         }
     }
 #pragma unroll
@@ -173,10 +175,21 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
 // binds this kernel -- which also makes the loop body position-independent,
 // so only 4 rounds are unrolled (small I-cache footprint).  lane_base has
 // bits 8..10 clear, so the row offset yd*256 merges with one LOP3.
-template <bool GENERAL, bool FULL, int NT, bool MW>
+// Debug write-set recording (lfg_kpz_debug_record_anchors): one word per
+// (round, tile) of the launch -- tile_id | xd << 20 | yd << 24 | hx << 27 |
+// hy << 28 | accepted << 29 -- from which the host rebuilds every write of
+// kpz_attempt_impl (kpz.hpp:97-105) for the reference's WriteLog check.
+struct KpzAnchorLog {
+    uint32_t* out;     // this launch: [kRounds][tiles_in_launch]
+    uint32_t stride;   // tiles_in_launch
+    uint32_t slot[4];  // this lane's tile slots (NT <= 4)
+};
+
+template <bool GENERAL, bool FULL, int NT, bool MW, bool WLOG = false>
 __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT], bool active, uint64_t seed,
                                                  uint64_t sweep, uint32_t block_id, const uint32_t (&tile_id)[NT],
-                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet) {
+                                                 uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet,
+                                                 const KpzAnchorLog& wlog = KpzAnchorLog{}) {
 #pragma unroll 1
     for (int m4 = 0; m4 < kRounds / 64; ++m4) {
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
@@ -214,17 +227,26 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
                             addr[n] = lop3<0xF8>(lane_base[n], __umulhi(yw[n], 2048u << (3 * k)), 0x700u);
                             u[n] = GENERAL ? sel4(Uw[n], k) : 0u;
                         }
+                        uint32_t acc[NT];
                         if (FULL || active) {
                             if (setw & 2u) {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc);
                                 else
-                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc);
                             } else {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc);
                                 else
-                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet);
+                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc);
+                            }
+                            if (WLOG) {
+                                const uint32_t r = uint32_t(64 * m4 + 16 * j + 8 * h + 4 * q + k);
+#pragma unroll
+                                for (int n = 0; n < NT; ++n)
+                                    wlog.out[r * wlog.stride + wlog.slot[n]] =
+                                        tile_id[n] | (xd[n] << 20) | (((addr[n] >> 8) & 7u) << 24) |
+                                        ((setw & 3u) << 27) | (acc[n] ? 1u << 29 : 0u);
                             }
                         }
                         setw >>= 2;
@@ -292,7 +314,7 @@ struct KpzDeps {
 // `rep`: stage, 512 single-hit rounds, write back, count.  `mbar_parity` is
 // the phase of the CTA's staging mbarrier (initialised by the caller) that this
 // activation's bulk copies complete.
-template <bool GENERAL, bool FULL, int kNT, bool MW>
+template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false>
 __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint32_t* const sm, const uint32_t smA,
                                                      const int rep, const uint64_t seed, const KpzSweep& sw,
                                                      const int bxi, const int byi, const uint32_t mbar_parity,
@@ -372,8 +394,18 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
         lane_base[n] = smA + uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
     }
     uint32_t ndep = 0, ndet = 0;
-    kpz_block_rounds<GENERAL, FULL, kNT, MW>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP, a.thrQ,
-                                             ndep, ndet);
+    KpzAnchorLog wl{};
+    if (WLOG) {
+        const uint32_t tpb = uint32_t(Wt * (a.by >> 4));
+        wl.out = a.wlog;
+        wl.stride = gridDim.x * gridDim.y * tpb;
+#pragma unroll
+        for (int n = 0; n < kNT; ++n)
+            wl.slot[n] = (blockIdx.y * gridDim.x + blockIdx.x) * tpb + uint32_t(warp + n * nwarps) * uint32_t(Wt) +
+                         uint32_t(tx);
+    }
+    kpz_block_rounds<GENERAL, FULL, kNT, MW, WLOG>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP,
+                                                   a.thrQ, ndep, ndet, wl);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     if (FULL) {
         for (int R = warp; R < a.by; R += nwarps) {
@@ -402,8 +434,9 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
     }
 }
 
-// DT phase kernel: one CTA per active block of phase a.phase.
-template <bool GENERAL, bool FULL, int kNT, bool MW>
+// DT phase kernel: one CTA per active block of phase a.phase.  WLOG: the
+// debug instantiation that records every attempt for the write-set check.
+template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false>
 __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
     kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm_raw[];
@@ -414,7 +447,7 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
     const uint64_t seed = a.seeds[blockIdx.z];
     const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
     const int set = sw.set(a.phase);
-    kpz_block_activation<GENERAL, FULL, kNT, MW>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
+    kpz_block_activation<GENERAL, FULL, kNT, MW, WLOG>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
                                                  a.brow0 + 2 * int(blockIdx.y) + (set >> 1), 0u, true,
                                                  KpzDeps{nullptr, 1, 1, 0, 0, 0u});
 }
@@ -501,6 +534,11 @@ template <int NT, bool MW>
 static void launch_cfg(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
     const dim3 block(unsigned(32 * (b.by / 16 / NT)));
     const bool full = b.bx == 1024;
+    if (b.wlog && !full && NT <= 2) {  // debug recording (block_x < 1024 plans only)
+        if (b.general) kpz_dtr_phase_kernel<true, false, NT, MW, true><<<grid, block, smem, st>>>(b);
+        else kpz_dtr_phase_kernel<false, false, NT, MW, true><<<grid, block, smem, st>>>(b);
+        return;
+    }
     if (b.general) {
         if (full) kpz_dtr_phase_kernel<true, true, NT, MW><<<grid, block, smem, st>>>(b);
         else kpz_dtr_phase_kernel<true, false, NT, MW><<<grid, block, smem, st>>>(b);
@@ -605,6 +643,11 @@ cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int r
 template <int NT, bool MW>
 static cudaError_t attrs_cfg(int smem) {
     const cudaFuncAttribute at = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if (NT <= 2) {
+        cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW, true>, at, smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT, MW, true>, at, smem);
+        if (e != cudaSuccess) return e;
+    }
     cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT, MW>, at, smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW>, at, smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT, MW>, at, smem);

@@ -23,6 +23,7 @@ struct KpzPhaseArgs {
     int32_t rep0;                   // first replica of this launch (set by the launcher)
     int32_t row_mask;               // buffer row slot = global row & row_mask (L-1: whole lattice)
     int32_t brow0, nbrow;           // block rows [brow0, brow0 + nbrow) of the shifted frame (strips)
+    uint32_t* wlog;                 // debug: this phase's [512 rounds][tiles] anchor records, or nullptr
     uint64_t seeds[kMaxRepPerLaunch];
 };
 
