@@ -58,6 +58,12 @@ __device__ __forceinline__ void global_flip(uint32_t* w, int L, int gx, int gy, 
     atomicXor(w + (idx >> 5), 1u << (idx & 31));
 }
 
+__device__ __forceinline__ unsigned long long lds_u64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+
 // kFccOffsets (lattice.hpp:147-151) in closed form: group g = dir >> 2 picks
 // the two non-zero axes ((x,y), (x,z), (y,z)); bit 1 of dir negates the first,
 // bit 0 the second.  Register arithmetic instead of a divergent constant-bank
@@ -197,7 +203,9 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
     const int zm = Lm & a.zmask;  // plane slot mask
-    if (threadIdx.x < 13) s_thr[threadIdx.x] = (uint64_t(a.thr_hi[threadIdx.x]) << 32) | a.thr_lo[threadIdx.x];
+    for (int i = int(threadIdx.x); i < 13; i += int(blockDim.x))  // blockDim may be 8
+        s_thr[i] = (uint64_t(a.thr_hi[i]) << 32) | a.thr_lo[i];
+    const uint32_t thr_sh = uint32_t(__cvta_generic_to_shared(s_thr));  // once, not per round
 
     // Stage: row word bit k = global bit X0 - 8 + k (k = lx + 8).
     const int wpr = L >> 5, wm = wpr - 1;
@@ -240,15 +248,15 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r + 1));  // next round, overlaps the loads
         const int here = int((own >> (lx + kK16Ofs)) & 1u), pb = int((par >> (px + kK16Ofs)) & 1u);
         const int n_site = k16_count(sf, se, lx), n_part = k16_count(pf, pe, px);
-        // kmc_attempt_impl (kmc.hpp:84-111)
-        if ((BOTH || here) && pb != here) {
-            const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
-            if (d <= 0 || uint64_t(W.z) < s_thr[d]) {
-                atomicXor(cur + sr, 1u << (lx + kK16Ofs));
-                atomicXor(cur + pr, 1u << (px + kK16Ofs));
-                ++nsucc;
-            }
-        }
+        // kmc_attempt_impl (kmc.hpp:84-111), branch-free: every lane loads its
+        // threshold (d <= 0 -> entry 0 = 2^32, always accepted) and XORs a
+        // possibly-empty mask, so the round has no divergent control flow.
+        const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
+        const int di = d < 0 ? 0 : d;  // d <= 12
+        const bool acc = (BOTH || here) && pb != here && uint64_t(W.z) < lds_u64(thr_sh + 8u * uint32_t(di));
+        atomicXor(cur + sr, acc ? 1u << (lx + kK16Ofs) : 0u);
+        atomicXor(cur + pr, acc ? 1u << (px + kK16Ofs) : 0u);
+        nsucc += acc ? 1u : 0u;
         __syncwarp(wmask);
     }
     // Write-back of the 1-ring-extended block: bits lx in [-1, 17) of rows

@@ -136,3 +136,18 @@ def test_kmc_phase_api_and_resume(lfg, oracle):
         b.synchronize()
         assert np.array_equal(a.download(), b.download())
         assert a.counters().successes == b.counters().successes
+
+
+@pytest.mark.parametrize("both", [False, True])
+def test_kmc_large_d_thresholds(lfg, oracle, both):
+    """Small eps makes every Metropolis threshold d = 1..12 matter (exp(-d eps) ~ 0.5..0.95):
+    the 16^3 kernel's 8-thread CTAs must still see the whole 13-entry table."""
+    L, eps, seed = 64, 0.05, 321
+    w, _ = oracle.kmc_random_alloy(L, 0.5, "lcg64", 8)
+    w_ref = w.copy()
+    c_ref = oracle.kmc_sweep_dt(L, w_ref, eps, both, seed, 0, 3, 16)
+    with lfg.KmcLattice(L, eps, both, seed, block=16) as k:
+        k.upload(w)
+        c = k.sweep(3)
+        assert [c.attempts, c.successes] == c_ref.tolist()
+        assert np.array_equal(k.download(), w_ref)
