@@ -292,3 +292,32 @@ def test_upload_async_check_reports_closure(lfg, oracle):
         with pytest.raises(lfg.ClosureError, match="closure"):
             k.upload_check()
         k.upload_check()  # the failure was reported once
+
+
+def test_bench_size_properties(lfg, oracle):
+    """L = 2^16 (the bench lattice, BASELINE configs[1]) with the production plan: two sweeps,
+    then the downloaded reference-layout slope field is closed (integrable), the row sums of
+    sigma_x and column sums of sigma_y are conserved, and the attempt accounting is exact."""
+    L = 1 << 16
+    with lfg.KpzLattice(L, 1.0, 0.0, 99) as k:
+        assert k.plan == (1024, 128)
+        k.make_flat_slopes()
+        x0, y0 = k.download()
+        c = k.sweep(2)
+        assert c.attempts == 2 * L * L and c.detaches == 0 and c.deposits > 0.1 * c.attempts
+        x, y = k.download()
+    wpr = L // 64
+
+    def row_ones(w):  # +1 bits per row
+        return np.bitwise_count(w.reshape(L, wpr)).sum(axis=1, dtype=np.int64)
+
+    def col_ones(w):  # +1 bits per column, in row chunks (the unpacked lattice is 4 GiB)
+        acc = np.zeros(L, np.int64)
+        rows = w.reshape(L, wpr)
+        for r0 in range(0, L, 512):
+            acc += np.unpackbits(rows[r0:r0 + 512].view(np.uint8), axis=1, bitorder="little").sum(axis=0, dtype=np.int64)
+        return acc
+
+    assert np.array_equal(row_ones(x), row_ones(x0))  # sigma_x row sums
+    assert np.array_equal(col_ones(y), col_ones(y0))  # sigma_y column sums
+    assert oracle.closure_holds(L, x, y)
