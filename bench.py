@@ -309,17 +309,41 @@ def run_b200(args):
         run = lambda n: k.sweep_async(n)  # noqa: E731
         mode = "1 GPU"
     else:
-        from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, ShardedKpz, StripPlan
+        from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, PeerComm, ShardedKpz, StripPlan
 
         bx, by = min(1024, L // 2), min(128, L // 2)
         plan = (bx, by)
         pl = StripPlan(L, world, bx, by)
         eng = CudaStripEngine(pl, args.p, args.q, args.seed, local)
-        sk = ShardedKpz(pl, args.seed, [eng], [rank], DistComm(eng))
+        # Default: peer memory (CUDA IPC over NVLink; ghost rows pushed by the phase
+        # kernel's write-back, device-side step barriers).  LFG_COMM=nccl selects
+        # torch.distributed P2P; a peer setup failure falls back to it.
+        comm, how = None, "torch.distributed " + dist.get_backend()
+        if os.environ.get("LFG_COMM", "peer") == "peer":
+            try:
+                comm, how = PeerComm(eng), "peer memory (CUDA IPC / NVLink), fused write-back push"
+            except Exception as ex:  # reported in the JSON line
+                how = f"torch.distributed {dist.get_backend()} (peer setup failed: {ex})"
+        if comm is None:
+            comm = DistComm(eng)
+        sk = ShardedKpz(pl, args.seed, [eng], [rank], comm)
         sk.make_flat_slopes()
+        if isinstance(comm, PeerComm):  # a peer barrier that times out anywhere -> everyone falls back
+            try:
+                sk.sweep(1)
+                bad = 0
+            except Exception:
+                bad = 1
+            t = torch.tensor([bad], device="cuda")
+            dist.all_reduce(t)
+            if int(t.item()):
+                comm.close()
+                comm, how = DistComm(eng), f"torch.distributed {dist.get_backend()} (peer barrier timed out)"
+                sk = ShardedKpz(pl, args.seed, [eng], [rank], comm)
+                sk.make_flat_slopes()
         stream = eng.stream
         run = sk.sweep
-        mode = f"strip-sharded x{world} (rows rolled per sweep, one ghost row per phase, {dist.get_backend()})"
+        mode = f"strip-sharded x{world} (rows rolled per sweep, one ghost row per phase; {how})"
 
     run(args.warmup)
     barrier()

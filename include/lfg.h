@@ -159,6 +159,15 @@ LFG_API int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t row_capacity, in
                                 int32_t block_row_count, uint64_t sweep, int32_t phase);
 /* Fill global rows [row_begin, +row_count) (mod L): pattern 0 = make_flat_slopes,
  * 1 = all slopes -1 (SlopeField constructor). */
+/* lfg_kpz_strip_phase with the ghost-row exchange fused into the write-back:
+ * the blocks that write global row push_row_dn (push_row_up) also store it
+ * into the ring buffer peer_dn (peer_up) of the lower (upper) neighbour -- a
+ * device pointer from lfg_ipc_open_handle, same row_capacity -- over NVLink.
+ * NULL / -1 disables a side.  Ordering with the neighbour is the caller's
+ * (lfg_peer_signal / lfg_peer_wait). */
+LFG_API int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t block_row_begin,
+                                     int32_t block_rows, uint64_t sweep, int32_t phase, void* peer_dn,
+                                     int32_t push_row_dn, void* peer_up, int32_t push_row_up);
 LFG_API int lfg_kpz_strip_fill(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t row_begin, int32_t row_count,
                                int32_t pattern);
 /* W^2 pieces (kpz.cpp:62-81 split by rows): H0 = row-0 heights (int32[L], needs global row 0);
@@ -170,6 +179,26 @@ LFG_API int lfg_kpz_strip_width_partials(lfg_kpz* h, const void* rows, int32_t r
  * sum h and sum h^2 - sum p^2 (add the all-reduced P2 to get sum h^2). */
 LFG_API int lfg_kpz_width_combine(lfg_kpz* h, const void* H0, const void* P1, const void* D, const void* seg_len,
                                   int32_t nseg, int64_t* sum, int64_t* sum2_without_p2);
+
+/* ------------------------------------------------------------ peer memory
+ * Single-node shard exchange without a collective library (one process per
+ * GPU; NVLink peer access through CUDA IPC).  Handles are 64 opaque bytes. */
+/* Handle of the allocation containing dev_ptr and dev_ptr's byte offset in it
+ * (pointers from a caching allocator may be interior); the opener adds the offset
+ * to the base that lfg_ipc_open_handle returns. */
+LFG_API int lfg_ipc_get_handle(const void* dev_ptr, void* handle64, uint64_t* offset);
+LFG_API int lfg_ipc_open_handle(const void* handle64, int32_t device, void** dev_ptr);
+LFG_API int lfg_ipc_close(void* dev_ptr, int32_t device);
+/* Device-side step barrier on `stream`: signal stores `value` (release, system
+ * scope) into flag_a / flag_b (either may be NULL; typically a neighbour's flag
+ * through its IPC pointer); wait blocks the stream until both local flags have
+ * reached `value` (wrap-around compare), giving up after max_spins polls with
+ * *err_flag = 1 (device memory, may be NULL) instead of hanging. */
+LFG_API int lfg_peer_signal(void* stream, void* flag_a, void* flag_b, uint32_t value, int32_t device);
+LFG_API int lfg_peer_wait(void* stream, const void* flag_a, const void* flag_b, uint32_t value, uint64_t max_spins,
+                          void* err_flag, int32_t device);
+/* cudaMemcpyAsync(cudaMemcpyDefault) on `stream` (peer copies between rings). */
+LFG_API int lfg_copy_async(void* dst, const void* src, size_t bytes, void* stream, int32_t device);
 
 #ifdef __cplusplus
 }

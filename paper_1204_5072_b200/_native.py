@@ -127,6 +127,13 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_create_strip", C.POINTER(P), I32, D, D, U64, C.POINTER(KpzPlan), I32)
     _sig(L, "lfg_kpz_sweep_origin", I32, C.POINTER(KpzPlan), U64, U64, C.POINTER(I32))
     _sig(L, "lfg_kpz_strip_phase", P, P, I32, I32, I32, U64, I32)
+    _sig(L, "lfg_kpz_strip_phase_push", P, P, I32, I32, I32, U64, I32, P, I32, P, I32)
+    _sig(L, "lfg_ipc_get_handle", P, P, C.POINTER(U64))
+    _sig(L, "lfg_ipc_open_handle", P, I32, C.POINTER(P))
+    _sig(L, "lfg_ipc_close", P, I32)
+    _sig(L, "lfg_peer_signal", P, P, P, C.c_uint32, I32)
+    _sig(L, "lfg_peer_wait", P, P, P, C.c_uint32, U64, P, I32)
+    _sig(L, "lfg_copy_async", P, P, SZ, P, I32)
     _sig(L, "lfg_kpz_strip_fill", P, P, I32, I32, I32, I32)
     _sig(L, "lfg_kpz_strip_row0_heights", P, P, I32, P)
     _sig(L, "lfg_kpz_strip_width_partials", P, P, I32, I32, I32, I32, P, P, P)

@@ -681,6 +681,11 @@ void check_ring(const lfg_kpz* h, const void* rows, int32_t cap) {
 
 int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0, int32_t nbrow, uint64_t sweep,
                         int32_t phase) {
+    return lfg_kpz_strip_phase_push(h, rows, cap, brow0, nbrow, sweep, phase, nullptr, -1, nullptr, -1);
+}
+
+int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0, int32_t nbrow, uint64_t sweep,
+                             int32_t phase, void* peer_dn, int32_t push_row_dn, void* peer_up, int32_t push_row_up) {
     return guarded([&] {
         check_handle(h);
         check_ring(h, rows, cap);
@@ -704,6 +709,10 @@ int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0, int3
         a.nbrow = nbrow;
         a.sweep = sweep;
         a.phase = phase;
+        a.peer_dn = static_cast<uint32_t*>(peer_dn);
+        a.peer_up = static_cast<uint32_t*>(peer_up);
+        a.push_row_dn = peer_dn ? push_row_dn : -1;
+        a.push_row_up = peer_up ? push_row_up : -1;
         cuda_check(kpz_launch_phase(a, h->seeds.data(), 1, h->stream), "kpz_dtr_phase launch");
         h->attempts[0] += int64_t(nbrow) * h->by * h->L / 4;
     });

@@ -407,24 +407,44 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
     kpz_block_rounds<GENERAL, FULL, kNT, MW, WLOG>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP,
                                                    a.thrQ, ndep, ndet, wl);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
+    // A row that a strip neighbour reads as its ghost is also stored straight
+    // into that neighbour's ring buffer (NVLink peer memory): the exchange is
+    // fused into the write-back, no separate collective.
+    const bool push = a.peer_dn != nullptr || a.peer_up != nullptr;
+    auto peer_row = [&](int R) -> uint32_t* {
+        const int gy = (Y0 + R) & Lm;
+        uint32_t* p = gy == a.push_row_dn ? a.peer_dn : (gy == a.push_row_up ? a.peer_up : nullptr);
+        return p ? p + uint32_t(gy & rmask) * uint32_t(wpr) : nullptr;
+    };
     if (FULL) {
         for (int R = warp; R < a.by; R += nwarps) {
             uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
+            uint32_t* const prow = push ? peer_row(R) : nullptr;
             const uint32_t cur = sm[(R + 8) * 64 + lane];             // slot lane
             const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, cur, 1);  // slot lane-1
             const uint32_t lo = lane == 0 ? sm[sm_slot(R, -1)] : prv;
-            row[(w0 + 1 + lane) & wmask] = __funnelshift_l(lo, cur, b);
-            if (lane == 31 && b != 0) row[(w0 + 33) & wmask] = __funnelshift_l(cur, sm[(R + 8) * 64 + 32], b);
+            const uint32_t v = __funnelshift_l(lo, cur, b);
+            row[(w0 + 1 + lane) & wmask] = v;
+            if (prow) prow[(w0 + 1 + lane) & wmask] = v;
+            if (lane == 31 && b != 0) {
+                const uint32_t v2 = __funnelshift_l(cur, sm[(R + 8) * 64 + 32], b);
+                row[(w0 + 33) & wmask] = v2;
+                if (prow) prow[(w0 + 33) & wmask] = v2;
+            }
         }
     } else {
         for (int R = warp; R < a.by; R += nwarps) {
             uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
+            uint32_t* const prow = push ? peer_row(R) : nullptr;
             for (int k = lane; k <= Wt; k += 32) {
                 if (k == Wt && b == 0) continue;  // would rewrite the unchanged right halo word
-                row[(w0 + 1 + k) & wmask] = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
+                const uint32_t v = __funnelshift_l(sm[sm_slot(R, k - 1)], sm[sm_slot(R, k)], b);
+                row[(w0 + 1 + k) & wmask] = v;
+                if (prow) prow[(w0 + 1 + k) & wmask] = v;
             }
         }
     }
+    if (push) __threadfence_system();  // peer stores visible system-wide before the step signal
     // Counters: deposits, detaches per replica.
     ndep = __reduce_add_sync(0xFFFFFFFFu, ndep);
     if (GENERAL) ndet = __reduce_add_sync(0xFFFFFFFFu, ndet);
@@ -668,6 +688,44 @@ cudaError_t kpz_phase_kernel_attrs() {
     if (e == cudaSuccess) e = attrs_nt<2>(smem);
     if (e == cudaSuccess && LFG_KPZ_NT >= 4) e = attrs_nt<4>(smem);
     return e;
+}
+
+// ============================================================ shard step barrier
+__global__ void peer_signal_kernel(uint32_t* flag_a, uint32_t* flag_b, uint32_t value) {
+    asm volatile("fence.sc.sys;" ::: "memory");
+    if (flag_a) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_a), "r"(value) : "memory");
+    if (flag_b) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag_b), "r"(value) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void peer_wait_kernel(const uint32_t* flag_a, const uint32_t* flag_b, uint32_t value,
+                                 unsigned long long max_spins, uint32_t* err) {
+    for (unsigned long long n = 0;; ++n) {
+        const bool a = !flag_a || int32_t(ld_acquire_sys(flag_a) - value) >= 0;
+        const bool b = !flag_b || int32_t(ld_acquire_sys(flag_b) - value) >= 0;
+        if (a && b) break;
+        if (n >= max_spins) {  // a peer never arrived: report instead of hanging the stream
+            if (err) atomicExch(err, 1u);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
+
+cudaError_t peer_launch_signal(uint32_t* flag_a, uint32_t* flag_b, uint32_t value, cudaStream_t st) {
+    peer_signal_kernel<<<1, 1, 0, st>>>(flag_a, flag_b, value);
+    return cudaGetLastError();
+}
+
+cudaError_t peer_launch_wait(const uint32_t* flag_a, const uint32_t* flag_b, uint32_t value,
+                             unsigned long long max_spins, uint32_t* err, cudaStream_t st) {
+    peer_wait_kernel<<<1, 1, 0, st>>>(flag_a, flag_b, value, max_spins, err);
+    return cudaGetLastError();
 }
 
 // ============================================================ init / convert

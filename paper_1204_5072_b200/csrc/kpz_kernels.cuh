@@ -24,8 +24,22 @@ struct KpzPhaseArgs {
     int32_t row_mask;               // buffer row slot = global row & row_mask (L-1: whole lattice)
     int32_t brow0, nbrow;           // block rows [brow0, brow0 + nbrow) of the shifted frame (strips)
     uint32_t* wlog;                 // debug: this phase's [512 rounds][tiles] anchor records, or nullptr
+    // Fused peer push (strip shards over NVLink): blocks writing global row
+    // push_row_dn / push_row_up also store it into the lower / upper
+    // neighbour's ring buffer (same capacity; peer pointer from CUDA IPC).
+    uint32_t* peer_dn;
+    uint32_t* peer_up;
+    int32_t push_row_dn, push_row_up;  // -1: none
     uint64_t seeds[kMaxRepPerLaunch];
 };
+
+// Device-side step barrier between strip shards (no host synchronisation):
+// signal stores `value` (release, system scope) into up to two peer flags;
+// wait spins until both local flags reach `value` (acquire) or max_spins
+// elapse (then *err = 1).
+cudaError_t peer_launch_signal(uint32_t* flag_a, uint32_t* flag_b, uint32_t value, cudaStream_t st);
+cudaError_t peer_launch_wait(const uint32_t* flag_a, const uint32_t* flag_b, uint32_t value,
+                             unsigned long long max_spins, uint32_t* err, cudaStream_t st);
 
 size_t kpz_phase_smem_bytes(int by);
 cudaError_t kpz_phase_kernel_attrs();

@@ -166,6 +166,13 @@ class CudaStripEngine:
         _native.check(_native.lib().lfg_kpz_strip_phase(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
                                                         brow0, nbrow, int(sweep), phase))
 
+    def phase_push(self, sweep: int, phase: int, brow0: int, nbrow: int, peer_dn, row_dn: int, peer_up,
+                   row_up: int):
+        _native.check(_native.lib().lfg_kpz_strip_phase_push(
+            self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap, brow0, nbrow, int(sweep), phase,
+            C.c_void_p(peer_dn) if peer_dn else None, int(row_dn), C.c_void_p(peer_up) if peer_up else None,
+            int(row_up)))
+
     def counters(self):
         c = _native.Counters()
         _native.check(_native.lib().lfg_kpz_counters(self.h, 0, C.byref(c)))
@@ -287,6 +294,96 @@ class DistComm:
             e.torch.cuda.current_stream(e.buf.device).synchronize()
 
 
+class PeerComm(DistComm):
+    """Single-node shard exchange over NVLink peer memory, without a collective
+    library and without host synchronisation (one process per GPU).
+
+    Each rank exports its ring buffer and a two-word step-flag array through CUDA
+    IPC; neighbours open them once.  Rows move by peer copies on the engine's
+    stream (rolls, readout ghosts) or -- in the sweep -- are stored straight into
+    the neighbour's ring by the phase kernel's write-back
+    (lfg_kpz_strip_phase_push), and a device-side step barrier
+    (lfg_peer_signal / lfg_peer_wait: release/acquire flags in peer memory)
+    orders each phase after both neighbours' previous phase.  torch.distributed
+    (any backend) is used only at setup to swap the IPC handles and by the
+    readouts' reductions.  A wait that never completes sets an error flag
+    (checked after every sweep) instead of hanging."""
+
+    fused_push = True
+
+    def __init__(self, engine, group=None, max_spins: int = 1 << 24):
+        super().__init__(engine, group)
+        e = engine
+        torch = e.torch
+        lib = _native.lib()
+        self.lib = lib
+        self.device = e.buf.device.index or 0
+        self.flags = torch.zeros(2, dtype=torch.int32, device=e.buf.device)  # [from lower, from upper]
+        self.err = torch.zeros(1, dtype=torch.int32, device=e.buf.device)
+        self.max_spins = int(max_spins)
+        e.sync()
+        mine = []
+        for t in (e.buf, self.flags):
+            hd, off = (C.c_char * 64)(), C.c_uint64()
+            _native.check(lib.lfg_ipc_get_handle(C.c_void_p(t.data_ptr()), hd, C.byref(off)))
+            mine.append((bytes(hd), int(off.value)))
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        self.up, self.dn = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        self._opened, self._bases = {}, []
+        for peer in {self.up, self.dn}:
+            ptrs = []
+            for hbytes, off in allh[peer]:
+                p = C.c_void_p()
+                _native.check(lib.lfg_ipc_open_handle(C.create_string_buffer(hbytes, 64), self.device, C.byref(p)))
+                self._bases.append(int(p.value))
+                ptrs.append(int(p.value) + off)
+            self._opened[peer] = ptrs  # (ring buffer, flags)
+        self.epoch = 0
+
+    def close(self):
+        for p in self._bases:
+            self.lib.lfg_ipc_close(C.c_void_p(p), self.device)
+        self._opened, self._bases = {}, []
+
+    def peer_ring(self, peer: int) -> int:
+        return self._opened[peer][0]
+
+    def step(self):
+        """Device-side barrier with both neighbours (stream-ordered)."""
+        self.epoch += 1
+        st = C.c_void_p(self.engine.stream.cuda_stream)
+        f_up = self._opened[self.up][1] + 0   # I am the upper neighbour's lower neighbour: its slot 0
+        f_dn = self._opened[self.dn][1] + 4   # ... and the lower neighbour's upper neighbour: its slot 1
+        _native.check(self.lib.lfg_peer_signal(st, C.c_void_p(f_up), C.c_void_p(f_dn), self.epoch, self.device))
+        fl = self.flags.data_ptr()
+        _native.check(self.lib.lfg_peer_wait(st, C.c_void_p(fl), C.c_void_p(fl + 4), self.epoch, self.max_spins,
+                                             C.c_void_p(self.err.data_ptr()), self.device))
+
+    def check(self):
+        if int(self.err.item()) != 0:
+            raise _native.TransportError("peer step barrier timed out (a neighbour did not arrive)")
+
+    def exchange(self, ops):
+        """Generic row exchange: barrier, my sends as peer copies into the
+        receivers' rings (same slots), barrier."""
+        if not ops:
+            return
+        e = self.engine
+        st = C.c_void_p(e.stream.cuda_stream)
+        row_bytes = e.buf.shape[1] * 4
+        self.step()
+        for kind, peer, b, n in ops:
+            if kind != "send":
+                continue
+            base = self.peer_ring(peer)
+            for (slot, m) in e.plan.pieces(b, n):
+                _native.check(self.lib.lfg_copy_async(C.c_void_p(base + slot * row_bytes),
+                                                      C.c_void_p(e.rows(slot, m).data_ptr()), m * row_bytes, st,
+                                                      self.device))
+        self.step()
+
+
 # ----------------------------------------------------------------------------- driver
 class ShardedKpz:
     """Strip-sharded lattice.  `engines` are this process's shards (all of them
@@ -322,6 +419,8 @@ class ShardedKpz:
 
     def sweep(self, n: int = 1):
         pl = self.plan
+        if getattr(self.comm, "fused_push", False):
+            return self._sweep_fused(n)
         for _ in range(n):
             s = self.sweep_index
             _, oy, sets = sweep_origin(pl, self.seed, s)
@@ -338,6 +437,38 @@ class ShardedKpz:
             self.sweep_index += 1
         for e in self.engines:
             e.sync()
+
+    def _sweep_fused(self, n: int):
+        """Peer-memory sweep: per sweep the roll and a full refresh of both ghost
+        rows (peer copies), then per phase one device-side step barrier and the
+        phase kernel, whose write-back also stores the strip's first row into the
+        lower neighbour's ring (sy = 0 phases, when that row changes) or its last
+        row into the upper neighbour's ring (sy = 1)."""
+        pl, comm = self.plan, self.comm
+        e, r = self.engines[0], self.ranks[0]
+        for _ in range(n):
+            s = self.sweep_index
+            _, oy, sets = sweep_origin(pl, self.seed, s)
+            ops = []
+            if oy != self.oy:
+                ops += pl.roll(self.oy, oy, r)
+                self.oy = oy
+            comm.exchange(ops)
+            comm.exchange(pl.ghost(oy, r, 0) + pl.ghost(oy, r, 1))
+            first = pl.start(oy, r)
+            last = (first + pl.H - 1) % pl.L
+            b0, nb = pl.block_rows(r)
+            for k in range(4):
+                sy = sets[k] >> 1
+                comm.step()
+                if sy == 0:
+                    e.phase_push(s, k, b0, nb, comm.peer_ring(comm.dn), first, None, -1)
+                else:
+                    e.phase_push(s, k, b0, nb, None, -1, comm.peer_ring(comm.up), last)
+            self.sweep_index += 1
+        comm.step()
+        e.sync()
+        comm.check()
 
     def counters_local(self):
         tot = [0, 0]
