@@ -334,7 +334,7 @@ def run_b200(args):
                 bad = 0
             except Exception:
                 bad = 1
-            t = torch.tensor([bad], device="cuda")
+            t = torch.tensor([bad], device="cuda" if dist.get_backend() == "nccl" else "cpu")
             dist.all_reduce(t)
             if int(t.item()):
                 comm.close()
