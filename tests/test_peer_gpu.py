@@ -75,3 +75,49 @@ def test_peer_sharded_equals_single(tmp_path, world, p, q, nsweeps):
     px, py = spins_to_slopes(got["rows"].view(np.uint32), L)
     assert np.array_equal(px, x) and np.array_equal(py, y)
     assert tuple(got["sums"]) == ref_sums
+
+
+def _kmc_worker(rank, world, port, L, both, seed, nsweeps, out):
+    sys.path.insert(0, os.path.dirname(HERE))
+    import torch
+    import torch.distributed as dist
+
+    from paper_1204_5072_b200.shard import CudaSlabEngine, PeerComm, ShardedKmc, SlabPlan
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    pl = SlabPlan(L, world, 16)
+    eng = CudaSlabEngine(pl, 1.5, both, seed, 0)
+    comm = PeerComm(eng, max_spins=1 << 23)
+    sk = ShardedKmc(pl, seed, [eng], [rank], comm)
+    sk.make_random_alloy(0.5, 5)
+    sk.sweep(nsweeps)
+    planes = sk.gather_planes().numpy()
+    succ = sk.successes()
+    ob = sk.open_bond_sums()
+    if rank == 0:
+        np.savez(out, planes=planes, succ=succ, ob=np.array(ob, np.int64))
+    dist.barrier()
+    comm.close()
+    eng.close()
+    dist.destroy_process_group()
+
+
+def test_peer_sharded_kmc_equals_single(tmp_path):
+    import paper_1204_5072_b200 as lfg
+
+    L, both, seed, nsweeps, world = 128, True, 91, 2, 2
+    out = str(tmp_path / "kmc.npz")
+    mp.start_processes(_kmc_worker, args=(world, _free_port(), L, both, seed, nsweeps, out), nprocs=world,
+                       join=True, start_method="spawn")
+    got = np.load(out)
+    with lfg.KmcLattice(L, 1.5, both, seed, block=16) as k:
+        k.make_random_alloy(0.5, 5)
+        c = k.sweep(nsweeps)
+        ref = k.download()
+        ref_ob = k.open_bond_sums()
+    assert int(got["succ"]) == c.successes
+    assert np.array_equal(got["planes"].reshape(-1).view(np.uint64), ref)
+    assert tuple(got["ob"]) == tuple(ref_ob)
