@@ -130,6 +130,16 @@ void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel exe
 // Default: four phase launches -- measured faster on B200 (979 vs 801
 // attempts/ns at L = 2^16): the persistent kernel's extra live state costs the
 // round loop its load batching (ncu: short-scoreboard stalls 1% -> 20%).
+// Chained phase launches (programmatic dependent launch + per-block flags);
+// LFG_KPZ_PDL=0 disables.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LFG_KPZ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool sweep_kernel_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("LFG_KPZ_SWEEP_KERNEL");
@@ -164,9 +174,17 @@ void enqueue_sweeps(lfg_kpz* h, int64_t n) {
                        "kpz_dtr_sweep launch");
             continue;
         }
+        const bool chain = pdl_enabled() && !h->wlog && h->R <= kMaxRepPerLaunch;
+        const uint32_t epoch = chain ? ++h->epoch : 0u;
         for (int k = 0; k < 4; ++k) {
             a.phase = k;
             a.wlog = h->wlog ? h->wlog + size_t(k) * (size_t(h->L) * h->L / 4) : nullptr;
+            if (chain) {  // phases 1-3 overlap the previous phase's tail (per-block flags)
+                a.dflags = h->flags;
+                a.depoch = epoch;
+                a.chain_wait = k > 0;
+                a.pdl = 1;
+            }
             cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
         }
     }

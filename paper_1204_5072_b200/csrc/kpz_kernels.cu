@@ -286,27 +286,29 @@ struct KpzDeps {
     const uint32_t* flags;  // [nby][nbx] of this replica, or nullptr
     int nbx, nby, ddx, ddy;  // ddx/ddy: previous set differs in x / y parity
     uint32_t epoch;
-    __device__ __forceinline__ bool active() const { return flags != nullptr; }
-    // Straight-line (no divergent loop): the four blocks (bxi +- ddx, byi +- ddy)
-    // -- two distinct ones when only one parity differs -- carry this epoch.
-    __device__ __forceinline__ bool ready(int bxi, int byi) const {
-        const int x0 = (bxi - ddx + nbx) % nbx, x1 = (bxi + ddx) % nbx;
-        const int y0 = (byi - ddy + nby) % nby, y1 = (byi + ddy) % nby;
-        const uint32_t a = ld_acquire_u32(flags + y0 * nbx + x0), b = ld_acquire_u32(flags + y0 * nbx + x1);
-        const uint32_t c = ld_acquire_u32(flags + y1 * nbx + x0), d = ld_acquire_u32(flags + y1 * nbx + x1);
-        return ((a ^ epoch) | (b ^ epoch) | (c ^ epoch) | (d ^ epoch)) == 0u;
-    }
-    // Block-wide wait; the loop condition is a bar.red result (block-uniform),
-    // so no divergent control flow reaches the rounds that follow.
+    // Block-wide wait: every thread polls the four flags (like an mbarrier
+    // try_wait loop), then orders the bulk copies that follow after the acquires.
     __device__ __forceinline__ void wait_block(int bxi, int byi) const {
         if (!flags) return;
-        for (;;) {
-            int ok = 1;
-            if (threadIdx.x == 0) ok = ready(bxi, byi);
-            if (__syncthreads_and(ok)) break;
-            __nanosleep(128);
-        }
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk copies read what the acquires saw
+        // block counts are powers of two
+        const int x0 = (bxi - ddx) & (nbx - 1), x1 = (bxi + ddx) & (nbx - 1);
+        const int y0 = (byi - ddy) & (nby - 1), y1 = (byi + ddy) & (nby - 1);
+        asm volatile(
+            "{\n\t.reg .pred pok;\n\t.reg .u32 va, vb, vc, vd;\n"
+            "KPZ_DEPS_POLL_%=:\n\t"
+            "ld.acquire.gpu.global.u32 va, [%0];\n\t"
+            "ld.acquire.gpu.global.u32 vb, [%1];\n\t"
+            "ld.acquire.gpu.global.u32 vc, [%2];\n\t"
+            "ld.acquire.gpu.global.u32 vd, [%3];\n\t"
+            "xor.b32 va, va, %4;\n\txor.b32 vb, vb, %4;\n\txor.b32 vc, vc, %4;\n\txor.b32 vd, vd, %4;\n\t"
+            "or.b32 va, va, vb;\n\tor.b32 vc, vc, vd;\n\tor.b32 va, va, vc;\n\t"
+            "setp.ne.u32 pok, va, 0;\n\t"
+            "@pok nanosleep.u32 64;\n\t"
+            "@pok bra KPZ_DEPS_POLL_%=;\n\t"
+            "fence.proxy.async.global;\n\t}"  // bulk copies read what the acquires saw
+            ::"l"(flags + y0 * nbx + x0), "l"(flags + y0 * nbx + x1), "l"(flags + y1 * nbx + x0),
+            "l"(flags + y1 * nbx + x1), "r"(epoch)
+            : "memory");
     }
 };
 
@@ -456,7 +458,10 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
 
 // DT phase kernel: one CTA per active block of phase a.phase.  WLOG: the
 // debug instantiation that records every attempt for the write-set check.
-template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false>
+// CHAIN: chained phase launches -- the CTA allows the next phase's launch to
+// begin (programmatic dependent launch), waits (a.chain_wait) for the previous
+// phase's blocks around it, and publishes its own completion in a.dflags.
+template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false, bool CHAIN = false>
 __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
     kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm_raw[];
@@ -467,9 +472,30 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) :
     const uint64_t seed = a.seeds[blockIdx.z];
     const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
     const int set = sw.set(a.phase);
-    kpz_block_activation<GENERAL, FULL, kNT, MW, WLOG>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
-                                                 a.brow0 + 2 * int(blockIdx.y) + (set >> 1), 0u, true,
-                                                 KpzDeps{nullptr, 1, 1, 0, 0, 0u});
+    if constexpr (!CHAIN) {
+        kpz_block_activation<GENERAL, FULL, kNT, MW, WLOG>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
+                                                     a.brow0 + 2 * int(blockIdx.y) + (set >> 1), 0u, true,
+                                                     KpzDeps{nullptr, 1, 1, 0, 0, 0u});
+    } else {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        const int nbx = a.L / a.bx, nby = a.L / a.by;
+        // block rows start at row `phase` (mod rows): the first CTAs to start
+        // depend on rows the previous phase finished early
+        const int iy = int((blockIdx.y + uint32_t(a.phase)) & (gridDim.y - 1u));
+        const int bxi = 2 * int(blockIdx.x) + (set & 1), byi = a.brow0 + 2 * iy + (set >> 1);
+        uint32_t* const fl = a.dflags + size_t(rep) * size_t(nbx) * size_t(nby);
+        // set(phase) ^ set(phase - 1) of this replica, precomputed by the launcher
+        // (deriving it here from the sweep permutation costs the rounds their
+        // uniform-datapath code generation)
+        const int d = int((a.dd[blockIdx.z >> 5] >> (2 * (blockIdx.z & 31))) & 3u);
+        const KpzDeps deps{a.chain_wait ? fl : nullptr, nbx, nby, d & 1, d >> 1, a.depoch};
+        kpz_block_activation<GENERAL, FULL, kNT, MW, WLOG>(a, sm, smA, rep, seed, sw, bxi, byi, 0u, true, deps);
+        __syncthreads();  // every warp's write-back issued before the release
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release_u32(fl + byi * nbx + bxi, a.depoch);
+        }
+    }
 }
 
 // Whole-sweep kernel (resident lattice): the four DT phases of sweep a.sweep in
@@ -559,13 +585,32 @@ static void launch_cfg(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream
         else kpz_dtr_phase_kernel<false, false, NT, MW, true><<<grid, block, smem, st>>>(b);
         return;
     }
-    if (b.general) {
-        if (full) kpz_dtr_phase_kernel<true, true, NT, MW><<<grid, block, smem, st>>>(b);
-        else kpz_dtr_phase_kernel<true, false, NT, MW><<<grid, block, smem, st>>>(b);
-    } else {
-        if (full) kpz_dtr_phase_kernel<false, true, NT, MW><<<grid, block, smem, st>>>(b);
-        else kpz_dtr_phase_kernel<false, false, NT, MW><<<grid, block, smem, st>>>(b);
+    if (b.dflags) {
+        const auto kern = b.general ? (full ? kpz_dtr_phase_kernel<true, true, NT, MW, false, true>
+                                            : kpz_dtr_phase_kernel<true, false, NT, MW, false, true>)
+                                    : (full ? kpz_dtr_phase_kernel<false, true, NT, MW, false, true>
+                                            : kpz_dtr_phase_kernel<false, false, NT, MW, false, true>);
+        if (!(b.pdl && b.chain_wait)) {
+            kern<<<grid, block, smem, st>>>(b);
+            return;
+        }
+        // may start while the previous phase's last wave still runs
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, b);
+        return;
     }
+    const auto kern = b.general ? (full ? kpz_dtr_phase_kernel<true, true, NT, MW> : kpz_dtr_phase_kernel<true, false, NT, MW>)
+                                : (full ? kpz_dtr_phase_kernel<false, true, NT, MW> : kpz_dtr_phase_kernel<false, false, NT, MW>);
+    kern<<<grid, block, smem, st>>>(b);
 }
 
 template <int NT>
@@ -582,6 +627,13 @@ cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int r
         b.rep0 = r0;
         const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
         for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
+        if (b.dflags && b.chain_wait) {
+            for (auto& w : b.dd) w = 0;
+            for (int r = 0; r < nr; ++r) {
+                const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seeds[r0 + r], a.sweep);
+                b.dd[r >> 5] |= uint64_t(sw.set(a.phase) ^ sw.set(a.phase - 1)) << (2 * (r & 31));
+            }
+        }
         const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.nbrow / 2), unsigned(nr));
         if (nt >= 4) launch_nt<(LFG_KPZ_NT >= 4 ? 4 : 1)>(b, grid, smem, st);
         else if (nt == 2) launch_nt<2>(b, grid, smem, st);
@@ -672,6 +724,10 @@ static cudaError_t attrs_cfg(int smem) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW>, at, smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT, MW>, at, smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT, MW>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT, MW, false, true>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW, false, true>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT, MW, false, true>, at, smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT, MW, false, true>, at, smem);
     return e;
 }
 

@@ -30,6 +30,17 @@ struct KpzPhaseArgs {
     uint32_t* peer_dn;
     uint32_t* peer_up;
     int32_t push_row_dn, push_row_up;  // -1: none
+    // Chained phases (programmatic dependent launch): each block publishes
+    // dflags[rep][block] = depoch when done; a launch with chain_wait set waits,
+    // per block, for the previous phase's blocks around it instead of for the
+    // whole previous grid (pdl: this launch may overlap the previous one).
+    uint32_t* dflags;
+    uint32_t depoch;
+    int32_t chain_wait;
+    int32_t pdl;
+    // per replica r of this launch: bits 2r, 2r+1 of dd[r >> 5] = x / y parity
+    // of set(phase) ^ set(phase - 1), filled by the launcher from the seeds
+    uint64_t dd[kMaxRepPerLaunch / 32];
     uint64_t seeds[kMaxRepPerLaunch];
 };
 
