@@ -515,6 +515,7 @@ struct KpzSweepArgs {
     uint32_t epoch;            // unique per launch
     int32_t lg_hx, lg_pp;      // log2(L/bx/2), log2(active blocks per phase): shifts keep the
                                // job -> block mapping on the uniform datapath (no division)
+    uint32_t dd;               // bits 2k, 2k+1: x / y parity of set(k) ^ set(k - 1), k = 1..3
 };
 
 #ifndef LFG_KPZ_SWEEP_MINB
@@ -550,9 +551,8 @@ __global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : LFG_
         const int bxi = 2 * (idx & ((1 << s.lg_hx) - 1)) + (set & 1);
         const int byi = 2 * (((idx >> s.lg_hx) + k) & hy_mask) + (set >> 1);
         uint32_t* const fl = s.flags;
-        const int prev = k > 0 ? sw.set(k - 1) : set;
-        const KpzDeps deps{k > 0 ? fl : nullptr, nbx, nby, (prev & 1) != (set & 1), (prev >> 1) != (set >> 1),
-                           s.epoch};
+        const int d = int((s.dd >> (2 * k)) & 3u);  // host-computed (see the phase kernel)
+        const KpzDeps deps{k > 0 ? fl : nullptr, nbx, nby, d & 1, d >> 1, s.epoch};
         kpz_block_activation<GENERAL, FULL, kNT, MW>(a, sm, smA, a.rep0, seed, sw, bxi, byi, parity, first, deps);
         parity ^= 1u;
         first = false;
@@ -699,6 +699,10 @@ cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int r
         s.epoch = ++epoch;
         s.lg_hx = ilog2(a.L / a.bx / 2);
         s.lg_pp = s.lg_hx + ilog2(a.L / a.by / 2);
+        {
+            const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seeds[r], a.sweep);
+            for (int k = 1; k < 4; ++k) s.dd |= uint32_t(sw.set(k) ^ sw.set(k - 1)) << (2 * k);
+        }
         cudaError_t e = cudaMemsetAsync(next_job, 0, sizeof(unsigned int), st);
         if (e != cudaSuccess) return e;
         const int njobs = 4 << s.lg_pp;
