@@ -13,9 +13,18 @@
 // write 1 (kmc.hpp:140-141) < the one-domain gap, so attempts of a round are
 // independent and the result equals the CPU oracle bit for bit.
 #include <cstdint>
+#include <cstdlib>
 
 #include "kmc_kernels.cuh"
+
 #include "lfg_common.cuh"
+
+#ifndef LFG_KMC_WIDE_SPLIT
+#define LFG_KMC_WIDE_SPLIT 1
+#endif
+#ifndef LFG_KMC_WIDE_PRED
+#define LFG_KMC_WIDE_PRED 0
+#endif
 
 namespace lfg {
 
@@ -276,6 +285,136 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     if (threadIdx.x == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
 }
 
+// ---------------------------------------------------------------- bk = 16, wide
+// Latency-bound phases (few active blocks, e.g. 512 at 256^3: under one warp
+// per SMSP) run one block per full warp.  Lane t + 8j (tile t, group j) draws
+// the Philox words of round 4b + j of its tile and precomputes everything of
+// that attempt that does not depend on the lattice (site, partner, their rows
+// and bit positions); the four rounds of the batch then run back to back, each
+// fetching its precomputed attempt with two shuffles.  Every group evaluates
+// the attempt (the same instruction stream) and group 0 applies it, so a
+// round's dependent chain is loads -> counts -> threshold -> XOR, with the
+// generator and the site arithmetic off it (4 rounds per warp-instruction).
+// Attempt order, draws and acceptance are those of kmc_dt16_phase_kernel.
+__device__ __forceinline__ int k16_count_at(const uint32_t (&f)[4], const uint32_t (&e)[4], uint32_t bit) {
+    const uint32_t m2 = 5u << (bit - 1u), m1 = 1u << bit;
+    return __popc(f[0] & m2) + __popc(f[1] & m2) + __popc(f[2] & m2) + __popc(f[3] & m2) + __popc(e[0] & m1) +
+           __popc(e[1] & m1) + __popc(e[2] & m1) + __popc(e[3] & m1);
+}
+
+template <bool BOTH>
+__global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    extern __shared__ __align__(16) uint32_t sk16[];
+    __shared__ unsigned long long s_thr[13];
+    const int L = a.L, Lm = L - 1, lane = int(threadIdx.x), t = lane & 7, j = lane >> 3;
+    uint32_t* const cur = sk16;
+    uint32_t* const org = cur + kK16Rows;
+    const int nb = L >> 4, h = nb >> 1;
+    const int blin = int(blockIdx.x);
+    const KmcSweep sw = kmc_sweep_draw(16, a.seed, a.sweep);
+    const int set = sw.set(a.phase);
+    const int bxi = 2 * (blin % h) + (set & 1);
+    const int byi = 2 * ((blin / h) % h) + ((set >> 1) & 1);
+    const int bzi = a.bz0 + 2 * (blin / (h * h)) + (set >> 2);
+    const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
+    const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
+    const int zm = Lm & a.zmask;
+    if (lane < 13) s_thr[lane] = (uint64_t(a.thr_hi[lane]) << 32) | a.thr_lo[lane];
+    const uint32_t thr_sh = uint32_t(__cvta_generic_to_shared(s_thr));
+
+    const int wpr = L >> 5, wm = wpr - 1;
+    const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
+    for (int rr = lane; rr < kK16Rows; rr += 32) {
+        const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
+        const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+        const uint32_t v = __funnelshift_r(row[w0 & wm], row[(w0 + 1) & wm], bo);
+        cur[rr] = v;
+        org[rr] = v;
+    }
+    __syncwarp();
+
+    const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
+    const uint32_t tl = uint32_t(L / 8);
+    const uint32_t tile_id = (uint32_t(bzi * 2 + tz) * tl + uint32_t(byi * 2 + ty)) * tl + uint32_t(bxi * 2 + tx);
+    const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;
+    const bool apply = j == 0;
+    uint32_t nsucc = 0;
+    U4 V = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int b = 0; b < kKmcRounds / 4; ++b) {
+        if ((b & 7) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(b >> 3));
+        // this lane's attempt: tile t, round 4b + j (KmcKernel::draw_site, kmc.hpp:154-171)
+        const int r = 4 * b + j;
+        const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r));
+        const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
+        const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
+        const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
+        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((W.x >> 4) & 1u);
+        int dx, dy, dz;
+        fcc_offset(int(below(W.y, 12)), dx, dy, dz);
+        // rows < 512, bit positions lx + 8, px + 8 in [7, 24]
+        const uint32_t pack = uint32_t(k16_row(ly, lz)) | (uint32_t(k16_row(ly + dy, lz + dz)) << 9) |
+                              (uint32_t(lx + kK16Ofs) << 18) | (uint32_t(lx + dx + kK16Ofs) << 23);
+        uint32_t pk[4], wz[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            pk[q] = __shfl_sync(0xFFFFFFFFu, pack, t + 8 * q);
+            wz[q] = __shfl_sync(0xFFFFFFFFu, W.z, t + 8 * q);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int sr = int(pk[q] & 511u), pr = int((pk[q] >> 9) & 511u);
+            const uint32_t bs = (pk[q] >> 18) & 31u, bp = pk[q] >> 23;
+            const uint32_t own = cur[sr], par = cur[pr];
+#if LFG_KMC_WIDE_SPLIT
+            // odd groups count the partner's neighbours, even groups the site's
+            const int cr = (j & 1) ? pr : sr;
+            const uint32_t cb = (j & 1) ? bp : bs;
+            const uint32_t cf[4] = {cur[cr - 1], cur[cr + 1], cur[cr - kK16E], cur[cr + kK16E]};
+            const uint32_t ce[4] = {cur[cr - kK16E - 1], cur[cr + kK16E - 1], cur[cr - kK16E + 1], cur[cr + kK16E + 1]};
+            const int n_own = k16_count_at(cf, ce, cb);
+            const int n_oth = __shfl_xor_sync(0xFFFFFFFFu, n_own, 8);
+            const int n_site = (j & 1) ? n_oth : n_own, n_part = (j & 1) ? n_own : n_oth;
+#else
+            const uint32_t sf[4] = {cur[sr - 1], cur[sr + 1], cur[sr - kK16E], cur[sr + kK16E]};
+            const uint32_t se[4] = {cur[sr - kK16E - 1], cur[sr + kK16E - 1], cur[sr - kK16E + 1], cur[sr + kK16E + 1]};
+            const uint32_t pf[4] = {cur[pr - 1], cur[pr + 1], cur[pr - kK16E], cur[pr + kK16E]};
+            const uint32_t pe[4] = {cur[pr - kK16E - 1], cur[pr + kK16E - 1], cur[pr - kK16E + 1], cur[pr + kK16E + 1]};
+            const int n_site = k16_count_at(sf, se, bs), n_part = k16_count_at(pf, pe, bp);
+#endif
+            const int here = int((own >> bs) & 1u), pb = int((par >> bp) & 1u);
+            // kmc_attempt_impl (kmc.hpp:84-111), branch-free as in kmc_dt16_phase_kernel
+            const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
+            const int di = d < 0 ? 0 : d;
+            const bool acc = apply && (BOTH || here) && pb != here && uint64_t(wz[q]) < lds_u64(thr_sh + 8u * uint32_t(di));
+#if LFG_KMC_WIDE_PRED
+            if (acc) {  // only applying lanes touch the words (no same-address atomics from idle groups)
+                atomicXor(cur + sr, 1u << bs);
+                atomicXor(cur + pr, 1u << bp);
+            }
+#else
+            atomicXor(cur + sr, acc ? 1u << bs : 0u);
+            atomicXor(cur + pr, acc ? 1u << bp : 0u);
+#endif
+            nsucc += acc ? 1u : 0u;
+            __syncwarp();
+        }
+    }
+    const int gx = (X0 - 1 + L) & Lm, gw = gx >> 5, gb = gx & 31;
+    for (int q = lane; q < 18 * 18; q += 32) {
+        const int ly = q % 18 - 1, lz = q / 18 - 1;
+        const int rr = k16_row(ly, lz);
+        const uint32_t d = ((cur[rr] ^ org[rr]) >> (kK16Ofs - 1)) & 0x3FFFFu;
+        if (d) {
+            uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+            atomicXor(row + gw, d << gb);
+            if (gb > 14) atomicXor(row + ((gw + 1) & wm), d >> (32 - gb));
+        }
+    }
+    nsucc = __reduce_add_sync(0xFFFFFFFFu, nsucc);
+    if (lane == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
+}
+
 // Blocks per CTA: bk = 16 (8 threads) packs four blocks in one warp; bk = 32
 // (64 threads) is one block per CTA.
 int kmc_blocks_per_cta(int bk) {
@@ -303,6 +442,15 @@ cudaError_t kmc_phase_kernel_attrs() {
     return e;
 }
 
+// LFG_KMC_WIDE=0 keeps latency-bound 16^3 phases on the 8-lane kernel (A/B).
+static bool kmc_wide_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("LFG_KMC_WIDE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
     const int tpb = (a.bk / 8) * (a.bk / 8) * (a.bk / 8);
     const int h = a.L / a.bk / 2;
@@ -318,6 +466,11 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         const int per = active >= 4 * 4 * 148 ? 4 : 1;
         const dim3 g16 = dim3(unsigned(active / per)), b16 = dim3(unsigned(8 * per));
         const size_t sm16 = size_t(per) * 2 * kK16Rows * sizeof(uint32_t);
+        if (per == 1 && kmc_wide_enabled()) {  // one block per full warp (see kmc_dt16w_phase_kernel)
+            if (a.both) kmc_dt16w_phase_kernel<true><<<g16, dim3(32), sm16, st>>>(a);
+            else kmc_dt16w_phase_kernel<false><<<g16, dim3(32), sm16, st>>>(a);
+            return cudaGetLastError();
+        }
         if (a.both) kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
         else kmc_dt16_phase_kernel<false><<<g16, b16, sm16, st>>>(a);
         return cudaGetLastError();
