@@ -22,6 +22,9 @@
 #ifndef LFG_KMC_WIDE_SPLIT
 #define LFG_KMC_WIDE_SPLIT 1
 #endif
+#ifndef LFG_KMC_WIDE_MASK
+#define LFG_KMC_WIDE_MASK 1
+#endif
 #ifndef LFG_KMC_WIDE_PRED
 #define LFG_KMC_WIDE_PRED 0
 #endif
@@ -355,11 +358,22 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
         // rows < 512, bit positions lx + 8, px + 8 in [7, 24]
         const uint32_t pack = uint32_t(k16_row(ly, lz)) | (uint32_t(k16_row(ly + dy, lz + dz)) << 9) |
                               (uint32_t(lx + kK16Ofs) << 18) | (uint32_t(lx + dx + kK16Ofs) << 23);
+#if LFG_KMC_WIDE_MASK
+        // Metropolis acceptance for every possible d at once: bit d set iff
+        // W.z < threshold(d) (64-bit compare, thresholds from the constant bank),
+        // so the round looks its d up in a register instead of shared memory.
+        uint32_t accm = 0;
+#pragma unroll
+        for (int dd = 0; dd < 13; ++dd)
+            accm |= (a.thr_hi[dd] != 0u || W.z < a.thr_lo[dd]) ? 1u << dd : 0u;
+#else
+        const uint32_t accm = W.z;
+#endif
         uint32_t pk[4], wz[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            pk[q] = __shfl_sync(0xFFFFFFFFu, pack, t + 8 * q);
-            wz[q] = __shfl_sync(0xFFFFFFFFu, W.z, t + 8 * q);
+        for (int q = 0; q < 4; ++q) {  // volatile: keep the exchange ahead of the rounds
+            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(pk[q]) : "r"(pack), "r"(t + 8 * q));
+            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(wz[q]) : "r"(accm), "r"(t + 8 * q));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -386,7 +400,11 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
             // kmc_attempt_impl (kmc.hpp:84-111), branch-free as in kmc_dt16_phase_kernel
             const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
             const int di = d < 0 ? 0 : d;
+#if LFG_KMC_WIDE_MASK
+            const bool acc = apply && (BOTH || here) && pb != here && ((wz[q] >> di) & 1u);
+#else
             const bool acc = apply && (BOTH || here) && pb != here && uint64_t(wz[q]) < lds_u64(thr_sh + 8u * uint32_t(di));
+#endif
 #if LFG_KMC_WIDE_PRED
             if (acc) {  // only applying lanes touch the words (no same-address atomics from idle groups)
                 atomicXor(cur + sr, 1u << bs);
