@@ -19,15 +19,6 @@
 
 #include "lfg_common.cuh"
 
-#ifndef LFG_KMC_WIDE_SPLIT
-#define LFG_KMC_WIDE_SPLIT 1
-#endif
-#ifndef LFG_KMC_WIDE_MASK
-#define LFG_KMC_WIDE_MASK 1
-#endif
-#ifndef LFG_KMC_WIDE_PRED
-#define LFG_KMC_WIDE_PRED 0
-#endif
 
 namespace lfg {
 
@@ -308,7 +299,6 @@ __device__ __forceinline__ int k16_count_at(const uint32_t (&f)[4], const uint32
 template <bool BOTH>
 __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sk16[];
-    __shared__ unsigned long long s_thr[13];
     const int L = a.L, Lm = L - 1, lane = int(threadIdx.x), t = lane & 7, j = lane >> 3;
     uint32_t* const cur = sk16;
     uint32_t* const org = cur + kK16Rows;
@@ -322,8 +312,6 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
     const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
     const int zm = Lm & a.zmask;
-    if (lane < 13) s_thr[lane] = (uint64_t(a.thr_hi[lane]) << 32) | a.thr_lo[lane];
-    const uint32_t thr_sh = uint32_t(__cvta_generic_to_shared(s_thr));
 
     const int wpr = L >> 5, wm = wpr - 1;
     const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
@@ -343,11 +331,14 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     const bool apply = j == 0;
     uint32_t nsucc = 0;
     U4 V = {0, 0, 0, 0};
-#pragma unroll 1
-    for (int b = 0; b < kKmcRounds / 4; ++b) {
-        if ((b & 7) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(b >> 3));
-        // this lane's attempt: tile t, round 4b + j (KmcKernel::draw_site, kmc.hpp:154-171)
-        const int r = 4 * b + j;
+    // This lane's attempt of batch bb: tile t, round 4 bb + j (KmcKernel::draw_site,
+    // kmc.hpp:154-171), packed as rows (< 512) and bit positions (lx + 8, px + 8 in
+    // [7, 24]); accm bit d is the Metropolis verdict W.z < threshold(d) for every
+    // possible d (64-bit compare against the constant-bank thresholds), so a round
+    // looks its d up in a register.
+    auto prepare = [&](int bb, uint32_t& pack, uint32_t& accm) {
+        if ((bb & 7) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(bb >> 3));
+        const int r = 4 * bb + j;
         const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r));
         const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
         const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
@@ -355,32 +346,36 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
         const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((W.x >> 4) & 1u);
         int dx, dy, dz;
         fcc_offset(int(below(W.y, 12)), dx, dy, dz);
-        // rows < 512, bit positions lx + 8, px + 8 in [7, 24]
-        const uint32_t pack = uint32_t(k16_row(ly, lz)) | (uint32_t(k16_row(ly + dy, lz + dz)) << 9) |
-                              (uint32_t(lx + kK16Ofs) << 18) | (uint32_t(lx + dx + kK16Ofs) << 23);
-#if LFG_KMC_WIDE_MASK
-        // Metropolis acceptance for every possible d at once: bit d set iff
-        // W.z < threshold(d) (64-bit compare, thresholds from the constant bank),
-        // so the round looks its d up in a register instead of shared memory.
-        uint32_t accm = 0;
+        pack = uint32_t(k16_row(ly, lz)) | (uint32_t(k16_row(ly + dy, lz + dz)) << 9) |
+               (uint32_t(lx + kK16Ofs) << 18) | (uint32_t(lx + dx + kK16Ofs) << 23);
+        accm = 0;
 #pragma unroll
-        for (int dd = 0; dd < 13; ++dd)
-            accm |= (a.thr_hi[dd] != 0u || W.z < a.thr_lo[dd]) ? 1u << dd : 0u;
-#else
-        const uint32_t accm = W.z;
-#endif
-        uint32_t pk[4], wz[4];
+        for (int dd = 0; dd < 13; ++dd) accm |= (a.thr_hi[dd] != 0u || W.z < a.thr_lo[dd]) ? 1u << dd : 0u;
+    };
+    uint32_t pk[4], am[4];
+    auto exchange = [&](uint32_t pack, uint32_t accm) {  // round q of the batch comes from group q
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // volatile: keep the exchange ahead of the rounds
+        for (int q = 0; q < 4; ++q) {
             asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(pk[q]) : "r"(pack), "r"(t + 8 * q));
-            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(wz[q]) : "r"(accm), "r"(t + 8 * q));
+            asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(am[q]) : "r"(accm), "r"(t + 8 * q));
         }
+    };
+    {
+        uint32_t pack, accm;
+        prepare(0, pack, accm);
+        exchange(pack, accm);
+    }
+#pragma unroll 1
+    for (int b = 0; b < kKmcRounds / 4; ++b) {
+        // the next batch's draws do not depend on the lattice: software-pipelined
+        // one batch ahead so their latency hides under this batch's rounds
+        uint32_t pack_n, accm_n;
+        prepare(b + 1, pack_n, accm_n);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int sr = int(pk[q] & 511u), pr = int((pk[q] >> 9) & 511u);
             const uint32_t bs = (pk[q] >> 18) & 31u, bp = pk[q] >> 23;
             const uint32_t own = cur[sr], par = cur[pr];
-#if LFG_KMC_WIDE_SPLIT
             // odd groups count the partner's neighbours, even groups the site's
             const int cr = (j & 1) ? pr : sr;
             const uint32_t cb = (j & 1) ? bp : bs;
@@ -389,34 +384,17 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
             const int n_own = k16_count_at(cf, ce, cb);
             const int n_oth = __shfl_xor_sync(0xFFFFFFFFu, n_own, 8);
             const int n_site = (j & 1) ? n_oth : n_own, n_part = (j & 1) ? n_own : n_oth;
-#else
-            const uint32_t sf[4] = {cur[sr - 1], cur[sr + 1], cur[sr - kK16E], cur[sr + kK16E]};
-            const uint32_t se[4] = {cur[sr - kK16E - 1], cur[sr + kK16E - 1], cur[sr - kK16E + 1], cur[sr + kK16E + 1]};
-            const uint32_t pf[4] = {cur[pr - 1], cur[pr + 1], cur[pr - kK16E], cur[pr + kK16E]};
-            const uint32_t pe[4] = {cur[pr - kK16E - 1], cur[pr + kK16E - 1], cur[pr - kK16E + 1], cur[pr + kK16E + 1]};
-            const int n_site = k16_count_at(sf, se, bs), n_part = k16_count_at(pf, pe, bp);
-#endif
             const int here = int((own >> bs) & 1u), pb = int((par >> bp) & 1u);
             // kmc_attempt_impl (kmc.hpp:84-111), branch-free as in kmc_dt16_phase_kernel
             const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
             const int di = d < 0 ? 0 : d;
-#if LFG_KMC_WIDE_MASK
-            const bool acc = apply && (BOTH || here) && pb != here && ((wz[q] >> di) & 1u);
-#else
-            const bool acc = apply && (BOTH || here) && pb != here && uint64_t(wz[q]) < lds_u64(thr_sh + 8u * uint32_t(di));
-#endif
-#if LFG_KMC_WIDE_PRED
-            if (acc) {  // only applying lanes touch the words (no same-address atomics from idle groups)
-                atomicXor(cur + sr, 1u << bs);
-                atomicXor(cur + pr, 1u << bp);
-            }
-#else
+            const bool acc = apply && (BOTH || here) && pb != here && ((am[q] >> di) & 1u);
             atomicXor(cur + sr, acc ? 1u << bs : 0u);
             atomicXor(cur + pr, acc ? 1u << bp : 0u);
-#endif
             nsucc += acc ? 1u : 0u;
             __syncwarp();
         }
+        exchange(pack_n, accm_n);
     }
     const int gx = (X0 - 1 + L) & Lm, gw = gx >> 5, gb = gx & 31;
     for (int q = lane; q < 18 * 18; q += 32) {
