@@ -438,13 +438,14 @@ cudaError_t kmc_phase_kernel_attrs() {
     return e;
 }
 
-// LFG_KMC_WIDE=0 keeps latency-bound 16^3 phases on the 8-lane kernel (A/B).
-static bool kmc_wide_enabled() {
-    static const bool on = [] {
+// LFG_KMC_WIDE=0 keeps latency-bound 16^3 phases on the 8-lane kernel, =2
+// sends every 16^3 phase to the wide kernel (A/B).
+static int kmc_wide_mode() {
+    static const int mode = [] {
         const char* e = std::getenv("LFG_KMC_WIDE");
-        return !(e && e[0] == '0');
+        return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
     }();
-    return on;
+    return mode;
 }
 
 cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
@@ -462,9 +463,12 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         const int per = active >= 4 * 4 * 148 ? 4 : 1;
         const dim3 g16 = dim3(unsigned(active / per)), b16 = dim3(unsigned(8 * per));
         const size_t sm16 = size_t(per) * 2 * kK16Rows * sizeof(uint32_t);
-        if (per == 1 && kmc_wide_enabled()) {  // one block per full warp (see kmc_dt16w_phase_kernel)
-            if (a.both) kmc_dt16w_phase_kernel<true><<<g16, dim3(32), sm16, st>>>(a);
-            else kmc_dt16w_phase_kernel<false><<<g16, dim3(32), sm16, st>>>(a);
+        const int wide = kmc_wide_mode();
+        if ((per == 1 && wide == 1) || wide == 2) {  // one block per full warp (see kmc_dt16w_phase_kernel)
+            const dim3 gw = dim3(unsigned(active));
+            const size_t smw = 2 * kK16Rows * sizeof(uint32_t);
+            if (a.both) kmc_dt16w_phase_kernel<true><<<gw, dim3(32), smw, st>>>(a);
+            else kmc_dt16w_phase_kernel<false><<<gw, dim3(32), smw, st>>>(a);
             return cudaGetLastError();
         }
         if (a.both) kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
