@@ -188,6 +188,43 @@ __device__ __forceinline__ int k16_count(const uint32_t (&f)[4], const uint32_t 
            __popc(e[1] & m1) + __popc(e[2] & m1) + __popc(e[3] & m1);
 }
 
+// Stage the 20 x 20 rows of a 16^3 block (plus halo) into cur/org: row word
+// bit k = global bit X0 - 8 + k (k = lx + 8).  Lane `first` of `STRIDE` takes
+// rows first, first + STRIDE, ...; the global loads are issued in batches of
+// kBatch before any is used (the rows are L2 hits, but a load-use loop would
+// pay the full latency once per row).
+template <int STRIDE>
+__device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, uint32_t* org, int first, int X0,
+                                          int Y0, int Z0, int zm) {
+    constexpr int kIt = (kK16Rows + STRIDE - 1) / STRIDE, kBatch = kIt < 13 ? kIt : 13;
+    const int L = a.L, Lm = L - 1, wpr = L >> 5, wm = wpr - 1;
+    const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
+#pragma unroll 1
+    for (int i0 = 0; i0 < kIt; i0 += kBatch) {
+        uint32_t lo[kBatch], hi[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int rr = first + STRIDE * (i0 + i);
+            lo[i] = hi[i] = 0;
+            if (rr < kK16Rows) {
+                const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
+                const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+                lo[i] = row[w0 & wm];
+                hi[i] = row[(w0 + 1) & wm];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int rr = first + STRIDE * (i0 + i);
+            if (rr < kK16Rows) {
+                const uint32_t v = __funnelshift_r(lo[i], hi[i], bo);
+                cur[rr] = v;
+                org[rr] = v;
+            }
+        }
+    }
+}
+
 template <bool BOTH>
 __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sk16[];
@@ -210,16 +247,8 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         s_thr[i] = (uint64_t(a.thr_hi[i]) << 32) | a.thr_lo[i];
     const uint32_t thr_sh = uint32_t(__cvta_generic_to_shared(s_thr));  // once, not per round
 
-    // Stage: row word bit k = global bit X0 - 8 + k (k = lx + 8).
     const int wpr = L >> 5, wm = wpr - 1;
-    const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
-    for (int rr = t; rr < kK16Rows; rr += 8) {
-        const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
-        const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
-        const uint32_t v = __funnelshift_r(row[w0 & wm], row[(w0 + 1) & wm], bo);
-        cur[rr] = v;
-        org[rr] = v;
-    }
+    k16_stage<8>(a, cur, org, t, X0, Y0, Z0, zm);
     __syncwarp(wmask);
 
     const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
@@ -314,14 +343,7 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     const int zm = Lm & a.zmask;
 
     const int wpr = L >> 5, wm = wpr - 1;
-    const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
-    for (int rr = lane; rr < kK16Rows; rr += 32) {
-        const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
-        const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
-        const uint32_t v = __funnelshift_r(row[w0 & wm], row[(w0 + 1) & wm], bo);
-        cur[rr] = v;
-        org[rr] = v;
-    }
+    k16_stage<32>(a, cur, org, lane, X0, Y0, Z0, zm);
     __syncwarp();
 
     const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
