@@ -188,6 +188,14 @@ __device__ __forceinline__ int k16_count(const uint32_t (&f)[4], const uint32_t 
            __popc(e[1] & m1) + __popc(e[2] & m1) + __popc(e[3] & m1);
 }
 
+// Programmatic dependent launch: a phase launched with the programmatic
+// stream-serialisation attribute may start while the previous phase drains;
+// its CTAs do the lattice-independent set-up (sweep/origin draws, the first
+// batch of site draws) and then wait for the previous grid to complete and
+// flush before staging.  Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Stage the 20 x 20 rows of a 16^3 block (plus halo) into cur/org: row word
 // bit k = global bit X0 - 8 + k (k = lx + 8).  Lane `first` of `STRIDE` takes
 // rows first, first + STRIDE, ...; the global loads are issued in batches of
@@ -343,8 +351,7 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     const int zm = Lm & a.zmask;
 
     const int wpr = L >> 5, wm = wpr - 1;
-    k16_stage<32>(a, cur, org, lane, X0, Y0, Z0, zm);
-    __syncwarp();
+    pdl_trigger();
 
     const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
     const uint32_t tl = uint32_t(L / 8);
@@ -387,6 +394,9 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
         prepare(0, pack, accm);
         exchange(pack, accm);
     }
+    pdl_wait();  // everything above is independent of the lattice
+    k16_stage<32>(a, cur, org, lane, X0, Y0, Z0, zm);
+    __syncwarp();
 #pragma unroll 1
     for (int b = 0; b < kKmcRounds / 4; ++b) {
         // the next batch's draws do not depend on the lattice: software-pipelined
@@ -470,6 +480,27 @@ static int kmc_wide_mode() {
     return mode;
 }
 
+// Wide-kernel phase launches carry the programmatic stream-serialisation
+// attribute (see pdl_wait): +5 % at 256^3.  LFG_KMC_PDL=0 launches them plainly.
+static cudaError_t launch_pdl(void (*kern)(KmcPhaseArgs), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              const KmcPhaseArgs& a) {
+    static const bool on = [] {
+        const char* e = std::getenv("LFG_KMC_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
     const int tpb = (a.bk / 8) * (a.bk / 8) * (a.bk / 8);
     const int h = a.L / a.bk / 2;
@@ -489,10 +520,11 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         if ((per == 1 && wide == 1) || wide == 2) {  // one block per full warp (see kmc_dt16w_phase_kernel)
             const dim3 gw = dim3(unsigned(active));
             const size_t smw = 2 * kK16Rows * sizeof(uint32_t);
-            if (a.both) kmc_dt16w_phase_kernel<true><<<gw, dim3(32), smw, st>>>(a);
-            else kmc_dt16w_phase_kernel<false><<<gw, dim3(32), smw, st>>>(a);
-            return cudaGetLastError();
+            return launch_pdl(a.both ? kmc_dt16w_phase_kernel<true> : kmc_dt16w_phase_kernel<false>, gw, dim3(32), smw,
+                              st, a);
         }
+        // (no PDL here: with blocks filling the GPU, early-launched CTAs of the
+        // next phase land unevenly on the SMs -- 48 vs 86 att/ns at 512^3)
         if (a.both) kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
         else kmc_dt16_phase_kernel<false><<<g16, b16, sm16, st>>>(a);
         return cudaGetLastError();
