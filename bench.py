@@ -249,6 +249,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def duplex_copy_gbps(torch, ha, hb, device, reps=3):
+    """GB/s per direction with one pinned H2D and one D2H copy in flight at once."""
+    da = torch.empty_like(ha, device=f"cuda:{device}")
+    db = torch.empty_like(hb, device=f"cuda:{device}")
+    s1, s2 = torch.cuda.Stream(device=device), torch.cuda.Stream(device=device)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        with torch.cuda.stream(s1):
+            da.copy_(ha, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hb.copy_(db, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    del da, db
+    return reps * ha.numel() * ha.element_size() / dt / 1e9
+
+
 def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
     """BASELINE configs[3]: 3-D fcc binary alloy, 256^3 sc, c = 0.5, eps = 1.5,
     both species active; one step = one MCS (L^3/2 attempts)."""
@@ -462,6 +480,14 @@ def run_b200(args):
                "single_lattice_sync_calls": single, "w2_last": w2}
         for k2 in kes:
             k2.close()
+        # the ceiling of this leg: concurrent H2D + D2H of pinned buffers (scripts/pcie_bw.py)
+        try:
+            bw = duplex_copy_gbps(torch, hxs[0].view(torch.uint8), hys[0].view(torch.uint8), local)
+            e2e["pcie_duplex_GBps_per_direction"] = bw
+            e2e["pcie_ceiling_attempts_per_ns"] = attempts_per_step / (2 * L * L // 8 / (bw * 1e9)) / 1e9
+        except Exception as ex:  # informational only
+            e2e["pcie_duplex_note"] = f"not measured: {ex}"
+
     elif not args.no_e2e:
         # sharded: each rank moves its strip (spin rows) host<->device around one MCS + distributed W^2
         hbuf = torch.empty_like(eng.buf, device="cpu").pin_memory()
