@@ -239,6 +239,45 @@ def test_sweep_kernel_matches_phase_launches(lfg):
     assert json.loads(r.stdout.strip().splitlines()[-1]) == ref
 
 
+_REPLICA_PROG = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_1204_5072_b200 as lfg
+out = []
+for (L, p, q, seeds, bx, by, n) in json.loads(sys.argv[2]):
+    with lfg.KpzLattice(L, p, q, seeds=seeds, block_x=bx, block_y=by) as k:
+        k.make_flat_slopes()
+        cs = k.sweep(n)
+        cs = cs if isinstance(cs, list) else [cs]
+        for r in range(len(seeds)):
+            x, y = k.download(r)
+            out.append([cs[r].deposits, cs[r].detaches, hashlib.sha256(x.tobytes() + y.tobytes()).hexdigest()])
+print(json.dumps(out))
+"""
+
+
+def test_chained_phases_match_plain_launches():
+    """Chained phase launches (programmatic dependent launch; each block waits for
+    the previous phase's blocks around it, with a per-replica set order) give the
+    lattices of plain stream-ordered launches (LFG_KPZ_PDL=0) bit for bit --
+    several replicas with different seeds in one launch, many blocks per phase."""
+    import json
+    import subprocess
+
+    cases = [(4096, 0.95, 0.05, [5, 6, 7, 2**33 + 1, 99], 1024, 128, 3),
+             (2048, 1.0, 0.0, [11, 12, 13], 256, 32, 4),
+             (8192, 1.0, 0.0, [21], 1024, 128, 2)]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for pdl in ("1", "0"):
+        env = dict(os.environ, LFG_KPZ_PDL=pdl)
+        r = subprocess.run([sys.executable, "-c", _REPLICA_PROG, root, json.dumps(cases)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+
+
 def test_async_transfers_match_sync_calls(lfg, oracle):
     """upload_async / sweep_async / width_sums_async / download_async on two
     handles with their own streams == the synchronous calls."""
