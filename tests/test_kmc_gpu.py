@@ -151,3 +151,39 @@ def test_kmc_large_d_thresholds(lfg, oracle, both):
         c = k.sweep(3)
         assert [c.attempts, c.successes] == c_ref.tolist()
         assert np.array_equal(k.download(), w_ref)
+
+
+_KMC_PROG = r"""
+import hashlib, json, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np
+import paper_1204_5072_b200 as lfg
+out = []
+for (L, eps, both, seed, n) in json.loads(sys.argv[2]):
+    with lfg.KmcLattice(L, eps, both, seed, block=16) as k:
+        k.make_random_alloy(0.5, seed + 1)
+        c = k.sweep(n)
+        out.append([c.attempts, c.successes, hashlib.sha256(np.ascontiguousarray(k.download()).tobytes()).hexdigest()])
+print(json.dumps(out))
+"""
+
+
+def test_kmc_16_kernels_agree():
+    """The three 16^3 paths -- the full-warp kernel (latency-bound phases), the
+    8-lane kernel with one block per warp, and with four blocks per warp (>= 2368
+    active blocks, L = 512) -- give the same lattice (LFG_KMC_WIDE=0/1/2)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    cases = [(64, 1.5, True, 3, 3), (128, 0.3, False, 4, 2), (512, 1.5, True, 5, 1)]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("0", "1", "2"):
+        env = dict(os.environ, LFG_KMC_WIDE=mode)
+        r = subprocess.run([sys.executable, "-c", _KMC_PROG, root, json.dumps(cases)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1] == outs[2]
