@@ -52,6 +52,10 @@ LFG_API int lfg_kmc_set_sweep_index(lfg_kmc* h, uint64_t sweep);
 LFG_API int lfg_kmc_get_sweep_index(const lfg_kmc* h, uint64_t* sweep);
 LFG_API int lfg_kmc_set_seed(lfg_kmc* h, uint64_t seed);
 LFG_API int lfg_kmc_set_stream(lfg_kmc* h, void* cuda_stream);
+/* Performance hint, no reference counterpart: `lattices` handles (this one included) run
+ * sweeps side by side on their own streams (an ensemble).  Phases then pick the kernel
+ * that suits the combined block count (lattice states are unaffected). */
+LFG_API int lfg_kmc_set_concurrency(lfg_kmc* h, int32_t lattices);
 LFG_API int lfg_kmc_synchronize(lfg_kmc* h);
 /* Device pointer of the occupancy words ([L][L][L/32] uint32) for interop. */
 LFG_API int lfg_kmc_device_words(lfg_kmc* h, void** dev_ptr, size_t* bytes);

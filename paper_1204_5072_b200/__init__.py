@@ -351,6 +351,10 @@ class KmcLattice:
     def set_stream(self, stream_ptr: int) -> None:
         check(_native.lib().lfg_kmc_set_stream(self._h, C.c_void_p(stream_ptr)))
 
+    def set_concurrency(self, lattices: int) -> None:
+        """Hint: `lattices` handles sweep side by side (kernel choice only)."""
+        check(_native.lib().lfg_kmc_set_concurrency(self._h, int(lattices)))
+
     def synchronize(self) -> None:
         check(_native.lib().lfg_kmc_synchronize(self._h))
 

@@ -166,6 +166,7 @@ def _bind_kmc(L) -> None:
     _sig(L, "lfg_kmc_get_sweep_index", P, C.POINTER(U64))
     _sig(L, "lfg_kmc_set_seed", P, U64)
     _sig(L, "lfg_kmc_set_stream", P, P)
+    _sig(L, "lfg_kmc_set_concurrency", P, I32)
     _sig(L, "lfg_kmc_synchronize", P)
     _sig(L, "lfg_kmc_device_words", P, C.POINTER(P), C.POINTER(SZ))
     # z-slab sharded path

@@ -46,6 +46,8 @@ def _parser() -> argparse.ArgumentParser:
         p.add_argument("--tile-edge", type=int, default=0)
         p.add_argument("--samples", default=None, help="comma-separated sample times (default: 1.1^k)")
         p.add_argument("--device", type=int, default=0)
+        p.add_argument("--concurrency", type=int, default=8,
+                       help="realizations in flight at once, each on its own stream (1: sequential)")
         p.add_argument("--out", default=None, help="CSV file (default: stdout)")
 
     k = sub.add_parser("kpz", help="KPZ octahedron model, W^2(t) and <h>(t)")
@@ -77,18 +79,20 @@ def _config(a):
         raise UsageError(f"unknown scheduler {a.scheduler!r} (choices: twolayer, doubletile)")
     if a.size < 4 or a.size & (a.size - 1):
         raise UsageError(f"size must be a power of two, got {a.size}")
-    if a.mcs < 0 or a.realizations < 1:
-        raise UsageError("mcs must be >= 0 and realizations >= 1")
+    if a.mcs < 0 or a.realizations < 1 or a.concurrency < 1:
+        raise UsageError("mcs must be >= 0, realizations >= 1 and concurrency >= 1")
     samples = [int(x) for x in a.samples.split(",")] if a.samples else None
     if a.cmd in ("kpz", "bench"):
         if not (0.0 <= a.p <= 1.0 and 0.0 <= a.q <= 1.0) or a.p + a.q <= 0.0:
             raise UsageError("p and q must lie in [0,1] with p + q > 0")
         return ExperimentConfig("kpz", a.size, a.mcs, a.seed, a.realizations, samples, p=a.p, q=a.q,
-                                block_x=a.tile_edge, block_y=a.block_edge, device=a.device)
+                                block_x=a.tile_edge, block_y=a.block_edge, device=a.device,
+                                concurrency=a.concurrency)
     if not 0.0 <= a.conc <= 1.0 or a.eps < 0.0:
         raise UsageError("conc must lie in [0,1] and eps >= 0")
     return ExperimentConfig("kmc", a.size, a.mcs, a.seed, a.realizations, samples, conc=a.conc, eps=a.eps,
-                            both_active=a.both_active, block=a.block_edge, device=a.device)
+                            both_active=a.both_active, block=a.block_edge, device=a.device,
+                            concurrency=a.concurrency)
 
 
 def parse_and_run(argv=None) -> int:

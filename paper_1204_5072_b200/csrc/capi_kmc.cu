@@ -31,6 +31,7 @@ struct lfg_kmc {
     int64_t attempts = 0;
     uint64_t thr[13] = {};
     bool slab_only = false;             // created by lfg_kmc_create_slab: no resident lattice
+    int32_t share = 1;                  // lfg_kmc_set_concurrency
 
     size_t nwords() const { return size_t(L) * L * L / 32; }
 };
@@ -81,6 +82,7 @@ KmcPhaseArgs base_args(const lfg_kmc* h) {
     a.zmask = h->L - 1;
     a.bz0 = 0;
     a.nbz = h->L / h->bk;
+    a.share = h->share;
     return a;
 }
 
@@ -441,6 +443,14 @@ int lfg_kmc_set_stream(lfg_kmc* h, void* stream) {
         if (h->own_stream) cudaStreamDestroy(h->stream);
         h->own_stream = false;
         h->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int lfg_kmc_set_concurrency(lfg_kmc* h, int32_t lattices) {
+    return guarded([&] {
+        check_handle(h);
+        if (lattices < 1) throw Error(LFG_EINVAL, "concurrency must be >= 1");
+        h->share = lattices;
     });
 }
 

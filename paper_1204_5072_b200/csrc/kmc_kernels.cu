@@ -513,7 +513,8 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
     if (a.bk == 16) {
         // One block per warp while the phase has fewer blocks than ~4 per
         // SMSP (latency-bound: spread over all SMs); four per warp beyond.
-        const int per = active >= 4 * 4 * 148 ? 4 : 1;
+        // (`share` lattices running side by side count as that many times the blocks)
+        const int per = active * (a.share > 1 ? a.share : 1) >= 4 * 4 * 148 && active >= 4 ? 4 : 1;
         const dim3 g16 = dim3(unsigned(active / per)), b16 = dim3(unsigned(8 * per));
         const size_t sm16 = size_t(per) * 2 * kK16Rows * sizeof(uint32_t);
         const int wide = kmc_wide_mode();

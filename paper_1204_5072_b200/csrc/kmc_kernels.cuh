@@ -19,6 +19,7 @@ struct KmcPhaseArgs {
     uint32_t thr_hi[13];           // bit 32 (threshold == 2^32)
     int32_t zmask;                 // buffer plane slot = global z & zmask (L-1: whole lattice)
     int32_t bz0, nbz;              // block z-rows [bz0, bz0 + nbz) of the shifted frame (slabs)
+    int32_t share;                 // lattices sharing the GPU at once (kernel choice; >= 1)
 };
 
 int kmc_blocks_per_cta(int bk);

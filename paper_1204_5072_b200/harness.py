@@ -6,8 +6,9 @@ samples observables on a schedule and writes CSV rows
 ``#``-prefixed config-echo lines.  This module is that harness over the
 B200 path: KPZ two-layer DTr (observable W², plus ⟨h⟩ = -1 + 2 (dep - det) / L²) and KMC
 two-layer DT (observable open bonds per particle).  Realizations run as independent
-lattices with seeds ``seed + r``; wall time is measured around the update calls only
-(SPEC.md:454).  There is no CPU scheduler here: the CLI's ``--scheduler`` accepts the
+lattices with seeds ``seed + r``, several at once on their own CUDA streams
+(``concurrency``, CLI ``--concurrency``); wall time is measured around the update calls
+only.  There is no CPU scheduler here: the CLI's ``--scheduler`` accepts the
 two-layer DT schedule the device implements.
 """
 from __future__ import annotations
@@ -16,7 +17,7 @@ import csv
 import io
 import time
 from dataclasses import asdict, dataclass, field
-from typing import Iterable, List, Optional
+from typing import List, Optional
 
 from . import InvalidArgument, KmcLattice, KpzLattice
 
@@ -44,6 +45,7 @@ class ExperimentConfig:
     block: int = 0
     alloy_seed: Optional[int] = None
     device: int = 0
+    concurrency: int = 8            # realizations in flight at once (own streams)
     extra: dict = field(default_factory=dict)
 
     def validate(self) -> None:
@@ -55,6 +57,8 @@ class ExperimentConfig:
             raise InvalidArgument("mcs must be >= 0")
         if self.realizations < 1:
             raise InvalidArgument("realizations must be >= 1")
+        if self.concurrency < 1:
+            raise InvalidArgument("concurrency must be >= 1")
         if self.model == "kmc" and not (0.0 <= self.conc <= 1.0):
             raise InvalidArgument("conc must lie in [0, 1]")
 
@@ -77,48 +81,78 @@ class Row:
     realization_id: int
 
 
-def _kpz_realization(cfg: ExperimentConfig, r: int) -> Iterable[Row]:
+def _kpz_open(cfg: ExperimentConfig, r: int) -> KpzLattice:
+    k = KpzLattice(cfg.size, cfg.p, cfg.q, cfg.seed + r, block_x=cfg.block_x, block_y=cfg.block_y,
+                   device=cfg.device)
+    k.make_flat_slopes()
+    return k
+
+
+def _kpz_observe(cfg: ExperimentConfig, k: KpzLattice):
     L = cfg.size
-    with KpzLattice(L, cfg.p, cfg.q, cfg.seed + r, block_x=cfg.block_x, block_y=cfg.block_y,
-                    device=cfg.device) as k:
-        k.make_flat_slopes()
+    c = k.counters()
+    succ = c.deposits + c.detaches
+    return succ, [("W2", k.interface_width()), ("mean_height", -1.0 + 2.0 * (c.deposits - c.detaches) / (L * L))]
+
+
+def _kmc_open(cfg: ExperimentConfig, r: int) -> KmcLattice:
+    k = KmcLattice(cfg.size, cfg.eps, cfg.both_active, cfg.seed + r, block=cfg.block, device=cfg.device)
+    k.make_random_alloy(cfg.conc, (cfg.alloy_seed if cfg.alloy_seed is not None else cfg.seed) + 7919 * r)
+    return k
+
+
+def _kmc_observe(cfg: ExperimentConfig, k: KmcLattice):
+    return k.counters().successes, [("open_bonds_per_particle", k.open_bonds_per_particle())]
+
+
+def _run_batch(cfg: ExperimentConfig, rids: List[int]) -> List[Row]:
+    """Realizations `rids` side by side: every lattice has its own CUDA stream, so one
+    interval's sweeps of all of them are in flight together (a 256^3 KMC phase fills a
+    ninth of the GPU; several realizations fill it).  Wall time: from issuing the
+    interval's sweeps to the last one finishing, attributed equally to the realizations."""
+    kpz = cfg.model == "kpz"
+    opener, observe = (_kpz_open, _kpz_observe) if kpz else (_kmc_open, _kmc_observe)
+    per_mcs = cfg.size ** 2 if kpz else cfg.size ** 3 // 2
+    lats = []
+    try:
+        for r in rids:
+            lats.append(opener(cfg, r))
+            if not kpz and len(rids) > 1:
+                lats[-1].set_concurrency(len(rids))
+        out = {r: [] for r in rids}
         t, wall, att = 0, 0.0, 0
         for ts in cfg.sample_times():
             if ts > t:
                 t0 = time.perf_counter()
-                k.sweep(ts - t)
-                wall += (time.perf_counter() - t0) * 1e3
-                att += L * L * (ts - t)
+                if len(lats) == 1:
+                    lats[0].sweep_async(ts - t)
+                else:  # round-robin, one MCS at a time, so all streams stay fed
+                    for _ in range(ts - t):
+                        for k in lats:
+                            k.sweep_async(1)
+                for k in lats:
+                    k.synchronize()
+                wall += (time.perf_counter() - t0) * 1e3 / len(lats)
+                att += per_mcs * (ts - t)
                 t = ts
-            c = k.counters()
-            succ = c.deposits + c.detaches
-            yield Row(t, "W2", k.interface_width(), att, succ, wall, r)
-            yield Row(t, "mean_height", -1.0 + 2.0 * (c.deposits - c.detaches) / (L * L), att, succ, wall, r)
-
-
-def _kmc_realization(cfg: ExperimentConfig, r: int) -> Iterable[Row]:
-    L = cfg.size
-    with KmcLattice(L, cfg.eps, cfg.both_active, cfg.seed + r, block=cfg.block, device=cfg.device) as k:
-        k.make_random_alloy(cfg.conc, (cfg.alloy_seed if cfg.alloy_seed is not None else cfg.seed) + 7919 * r)
-        t, wall, att = 0, 0.0, 0
-        for ts in cfg.sample_times():
-            if ts > t:
-                t0 = time.perf_counter()
-                k.sweep(ts - t)
-                wall += (time.perf_counter() - t0) * 1e3
-                att += L ** 3 // 2 * (ts - t)
-                t = ts
-            succ = k.counters().successes
-            yield Row(t, "open_bonds_per_particle", k.open_bonds_per_particle(), att, succ, wall, r)
+            for r, k in zip(rids, lats):
+                succ, obs = observe(cfg, k)
+                out[r].extend(Row(t, name, v, att, succ, wall, r) for name, v in obs)
+        return [row for r in rids for row in out[r]]
+    finally:
+        for k in lats:
+            k.close()
 
 
 def run_experiment(cfg: ExperimentConfig) -> List[Row]:
-    """run_experiment: every realization's time series, in order."""
+    """run_experiment: every realization's time series, in order.
+    Realizations run in concurrent batches of ``cfg.concurrency`` lattices (1: one after
+    another); the lattices and their series do not depend on the batching."""
     cfg.validate()
-    gen = _kpz_realization if cfg.model == "kpz" else _kmc_realization
     rows: List[Row] = []
-    for r in range(cfg.realizations):
-        rows.extend(gen(cfg, r))
+    step = max(1, int(cfg.concurrency))
+    for r0 in range(0, cfg.realizations, step):
+        rows.extend(_run_batch(cfg, list(range(r0, min(cfg.realizations, r0 + step)))))
     return rows
 
 

@@ -82,3 +82,21 @@ def test_kmc_quench_first_sample(tmp_path):
     _, rows = read_csv(out.read_text())
     assert rows[0].t == 0 and abs(rows[0].value - 8.1) < 0.1
     assert rows[-1].t == 20 and rows[-1].value < rows[0].value
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["kpz", "kmc"])
+def test_concurrent_realizations_equal_sequential(model):
+    """Realizations in flight together on their own streams give the series of running
+    them one after another (only wall_ms differs)."""
+    from paper_1204_5072_b200.harness import run_experiment
+
+    kw = dict(p=0.95, q=0.05) if model == "kpz" else dict(conc=0.5, eps=1.5, both_active=True)
+    size = 128 if model == "kpz" else 32
+    rows = {}
+    for conc in (1, 3):
+        cfg = ExperimentConfig(model, size, 12, seed=9, realizations=5, concurrency=conc, **kw)
+        rows[conc] = [(r.t, r.observable_name, r.value, r.attempts, r.successes, r.realization_id)
+                      for r in run_experiment(cfg)]
+    assert rows[1] == rows[3]
+    assert {x[-1] for x in rows[1]} == set(range(5))
