@@ -289,6 +289,30 @@ def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
         out["both" if both else "b_only"] = {"value": (L ** 3 // 2) * steps / (ms * 1e6), "unit": "attempts/ns",
                                              "ms_per_mcs": ms / steps, "open_bonds": k.open_bonds_per_particle()}
         k.close()
+    # ensemble: 8 seeds side by side, each lattice on its own stream (sweeps issued
+    # round-robin), launches sized for the combined load (lfg_kmc_set_concurrency)
+    n = 8
+    ks = []
+    for i in range(n):
+        k = lfg.KmcLattice(L, 1.5, True, 100 + i)
+        k.set_concurrency(n)
+        k.make_random_alloy(0.5, 200 + i)
+        ks.append(k)
+    for k in ks:
+        k.sweep_async(warmup)
+    for k in ks:
+        k.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for k in ks:
+            k.sweep_async(1)
+    for k in ks:
+        k.synchronize()
+    dt = time.perf_counter() - t0
+    out["ensemble8_both"] = {"value": n * (L ** 3 // 2) * steps / (dt * 1e9), "unit": "attempts/ns",
+                             "note": "8 lattices (seeds) on 8 streams, wall clock incl. the final synchronize"}
+    for k in ks:
+        k.close()
     out["config"] = f"KMC fcc binary alloy {L}^3 sc, c=0.5, eps=1.5, DT blocks 16^3 (BASELINE.json configs[3])"
     out["note"] = ("L2-resident (2 MiB); only L^3/4096 tiles are active per single-hit round, so the 256^3 "
                    "case is latency-bound by construction")
