@@ -8,7 +8,6 @@
  6. Conservation: KPZ row sums of sigma_x and column sums of sigma_y, and the KMC B count,
     unchanged after 10^4 MCS, exactly.
 """
-import math
 from concurrent.futures import ProcessPoolExecutor
 
 import numpy as np
