@@ -423,16 +423,30 @@ def run_b200(args):
         avg_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / 4
         achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
-        traffic = None
+        traffic, ncu = None, {}
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-                traffic = json.load(f).get("kpz_dtr_phase", {}).get("dram_bytes_per_launch")
+                ncu = json.load(f).get("kpz_dtr_phase", {})
+            traffic = ncu.get("dram_bytes_per_launch")
         except Exception:
             pass
+        # The roofline that binds: SM issue.  Ceiling = warp-instruction issue rate of all
+        # SMSPs at the clock sampled during the timed region / warp-instructions per attempt
+        # (ncu count of one launch of this kernel at L = 2^16, p = 1).
+        issue = None
+        if ncu.get("inst_executed") and L == 1 << 16 and args.p == 1.0 and args.q == 0.0:
+            wi_per_att = ncu["inst_executed"] / (attempts_per_step / 4)
+            f_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
+            ceil_att = 148 * 4 * f_ghz / wi_per_att
+            issue = {"achieved_attempts_per_ns": bytes_per_launch / ALG_BYTES_PER_ATTEMPT / (avg_launch_ms * 1e6),
+                     "ceiling_attempts_per_ns": ceil_att, "warp_inst_per_attempt": wi_per_att,
+                     "frac": bytes_per_launch / ALG_BYTES_PER_ATTEMPT / (avg_launch_ms * 1e6) / ceil_att,
+                     "source": f"ncu inst_executed of one launch ({ncu.get('tag')}), 148 SMs x 4 issue slots/clk"}
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peak_kind, "kernel": "kpz_dtr_phase_kernel",
                     "avg_launch_ms": avg_launch_ms, "alg_bytes_per_launch": bytes_per_launch,
                     "binding_unit": "SM issue / ALU pipe (profiles/r01d_kpz_ncu.txt: issue 74%, ALU 59%, DRAM 6%)",
+                    "issue_roofline": issue,
                     "note": "algorithmic bytes = 0.5 B/attempt (two 1-bit slope planes read+written once per MCS, "
                             "SURVEY.md §8(d)); the device keeps 1 spin bit per site; the faithful single-hit "
                             "DTr kernel is issue-bound, not HBM-bound (DESIGN.md §4.1)"}
