@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kmc", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] single-GPU sub-measurement")
     a = ap.parse_args()
     if a.L == 0:
         a.L = (1 << 16) if int(os.environ.get("WORLD_SIZE", "1")) == 1 else (1 << 17)
@@ -319,6 +320,28 @@ def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
     return out
 
 
+def c3_measure(lfg, torch, stream, steps, warmup, L=1 << 17):
+    """BASELINE configs[2]'s lattice and parameters (L = 2^17, p = 0.95, q = 0.05, flat
+    start) on this one GPU: the denominator of its strong-scaling runs at N > 1."""
+    k = lfg.KpzLattice(L, 0.95, 0.05, 1)
+    try:
+        k.set_stream(stream.cuda_stream)
+        k.make_flat_slopes()
+        k.sweep_async(warmup)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        k.sweep_async(steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        return {"value": L * L * steps / (ms * 1e6), "unit": "attempts/ns", "ms_per_mcs": ms / steps,
+                "steps": steps, "config": f"KPZ DTr L={L}, p=0.95, q=0.05, flat start, plan {k.plan} "
+                                         f"(BASELINE.json configs[2] on 1 GPU)"}
+    finally:
+        k.close()
+
+
 def run_b200(args):
     import torch
 
@@ -564,6 +587,9 @@ def run_b200(args):
     kmc = None
     if rank == 0 and world == 1 and not args.no_kmc:
         kmc = kmc_measure(lfg, torch, stream, steps=20, warmup=3)
+    c3 = None
+    if rank == 0 and world == 1 and not args.no_c3:
+        c3 = c3_measure(lfg, torch, stream, steps=10, warmup=3)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "attempts/ns", "n_gpus": world, "steps": args.steps,
@@ -578,7 +604,7 @@ def run_b200(args):
                            "l2": f"lattice {L * L // 8 >> 20} MiB ({L * L // 8 // world >> 20} MiB per GPU) >> 126 MB L2: "
                                  f"no flush needed"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": 4 * args.steps, "kmc": kmc}
+                "gpu_launches": 4 * args.steps, "kmc": kmc, "c3_single_gpu": c3}
         print(json.dumps(line), flush=True)
     if world == 1:
         k.close()

@@ -7,7 +7,7 @@ for n in "$@"; do
   [ -n "$TESTS" ] && LFG_LIB=paper_1204_5072_b200/_lib/variants/$n/liblfg.so timeout 900 \
       python -m pytest $TESTS -x -q -m gpu > $OUT/pytest_$n.txt 2>&1
 done
-B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-kmc"
+B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-kmc --no-c3"
 for i in 1 2 3; do
   for pq in "1.0 0.0" "0.95 0.05"; do
     set -- $pq; P=$1; Q=$2; shift 2
