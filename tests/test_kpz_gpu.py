@@ -190,7 +190,9 @@ def test_large_lattice_properties(lfg, oracle):
 
 def test_large_lattice_matches_oracle_one_sweep(lfg, oracle):
     L = 2048
-    for (p, q) in ((1.0, 0.0), (0.95, 0.05)):
+    # (1, 0.5) and (0, 1): thresholds of exactly 2^32 and 0 on the TMA-staged path, where the
+    # acceptance compare is 32-bit with the "threshold == 2^32" predicate
+    for (p, q) in ((1.0, 0.0), (0.95, 0.05), (1.0, 0.5), (0.0, 1.0)):
         x, y = oracle.kpz_flat(L)
         c_ref = oracle.kpz_sweep_dtr(L, x, y, p, q, 31, 0, 1, 1024, 128)
         with lfg.KpzLattice(L, p, q, 31) as k:
