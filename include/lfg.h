@@ -66,7 +66,8 @@ LFG_API int lfg_device_count(int* count);
 typedef struct lfg_kpz lfg_kpz;
 
 /* Two-layer DTr geometry: device blocks block_x x block_y sites (0 = auto:
- * min(1024, L/2) x min(128, L/2)); inner 16x8 single-hit domains are fixed. */
+ * min(1024, L/2) x min(128, L/2)); powers of two, block_x in [32, 1024],
+ * block_y in [16, 256]; inner 16x8 single-hit domains are fixed. */
 typedef struct lfg_kpz_plan {
     int32_t block_x;
     int32_t block_y;

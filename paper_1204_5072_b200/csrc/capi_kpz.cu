@@ -84,9 +84,9 @@ void resolve_plan(lfg_kpz* h, const lfg_kpz_plan* plan) {
     if (bx < 32 || bx > 1024 || bx % 32 || !is_pow2(bx) || h->L % (2 * bx))
         throw Error(LFG_EINVAL, "DtrPlan: block_x must be a power of two in [32, min(1024, L/2)], got " +
                                     std::to_string(bx));
-    if (by < 16 || by > 128 || by % 16 || !is_pow2(by) || h->L % (2 * by))
-        throw Error(LFG_EINVAL, "DtrPlan: block_y must be a power of two in [16, min(128, L/2)], got " +
-                                    std::to_string(by));
+    if (by < 16 || by > LFG_KPZ_MAXBY || by % 16 || !is_pow2(by) || h->L % (2 * by))
+        throw Error(LFG_EINVAL, "DtrPlan: block_y must be a power of two in [16, min(" +
+                                    std::to_string(LFG_KPZ_MAXBY) + ", L/2)], got " + std::to_string(by));
     h->bx = bx;
     h->by = by;
 }
@@ -169,7 +169,7 @@ void enqueue_sweeps(lfg_kpz* h, int64_t n) {
     }
     for (int64_t s = 0; s < n; ++s) {
         a.sweep = h->sweep + uint64_t(s);
-        if (sweep_kernel_enabled() && !h->wlog) {
+        if (sweep_kernel_enabled() && !h->wlog && h->by <= 128) {  // its launch bounds stop at 4 warps
             cuda_check(kpz_launch_sweep(a, h->seeds.data(), h->R, h->flags, h->next_job, h->epoch, h->stream),
                        "kpz_dtr_sweep launch");
             continue;

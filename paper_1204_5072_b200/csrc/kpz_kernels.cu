@@ -480,7 +480,8 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
 // begin (programmatic dependent launch), waits (a.chain_wait) for the previous
 // phase's blocks around it, and publishes its own completion in a.dflags.
 template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false, bool CHAIN = false>
-__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : 6) : 12)
+__global__ void __launch_bounds__(MW ? (kNT == 2 && LFG_KPZ_MAXBY >= 256 ? 256 : 256 / kNT) : 32,
+                                  MW ? (kNT == 1 || (kNT == 2 && LFG_KPZ_MAXBY >= 256) ? 3 : 6) : 12)
     kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm_raw[];
     const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
@@ -761,7 +762,7 @@ static cudaError_t attrs_nt(int smem) {
 }
 
 cudaError_t kpz_phase_kernel_attrs() {
-    const int smem = int(kpz_phase_smem_bytes(128));
+    const int smem = int(kpz_phase_smem_bytes(LFG_KPZ_MAXBY));
     cudaError_t e = attrs_nt<1>(smem);
     if (e == cudaSuccess) e = attrs_nt<2>(smem);
     if (e == cudaSuccess && LFG_KPZ_NT >= 4) e = attrs_nt<4>(smem);

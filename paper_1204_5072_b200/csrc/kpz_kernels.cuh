@@ -10,6 +10,10 @@ namespace lfg {
 
 constexpr int kMaxRepPerLaunch = 64;
 
+#ifndef LFG_KPZ_MAXBY
+#define LFG_KPZ_MAXBY 256  // largest DT block height: 256 = 8-warp CTAs, two tiles per lane (the default plan stays 128)
+#endif
+
 // Passed as a __grid_constant__ kernel parameter: everything block-uniform
 // (seeds included) lives in the constant bank -> uniform registers.
 struct KpzPhaseArgs {

@@ -188,6 +188,21 @@ def test_large_lattice_properties(lfg, oracle):
         assert (h.sum(), (h * h).sum()) == k.width_sums()
 
 
+def test_block_height_256_matches_oracle(lfg, oracle):
+    # 8-warp CTAs (block_y = 256): the block-boundary part of the DT deficit is 45 % smaller
+    # than with the default 128 (profiles/stats_r01.md), at 3 % lower throughput
+    for (L, p, q, bx, by, n) in [(2048, 1.0, 0.0, 1024, 256, 2), (2048, 0.95, 0.05, 1024, 256, 2),
+                                 (1024, 0.95, 0.05, 256, 256, 2), (4096, 1.0, 0.5, 1024, 256, 1)]:
+        x, y = oracle.kpz_flat(L)
+        c_ref = oracle.kpz_sweep_dtr(L, x, y, p, q, 17, 0, n, bx, by)
+        with lfg.KpzLattice(L, p, q, 17, block_x=bx, block_y=by) as k:
+            k.make_flat_slopes()
+            c = k.sweep(n)
+            gx, gy = k.download()
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist(), (L, bx, by, p, q)
+        assert (gx == x).all() and (gy == y).all(), (L, bx, by, p, q)
+
+
 def test_large_lattice_matches_oracle_one_sweep(lfg, oracle):
     L = 2048
     # (1, 0.5) and (0, 1): thresholds of exactly 2^32 and 0 on the TMA-staged path, where the
