@@ -468,7 +468,7 @@ def run_b200(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peak_kind, "kernel": "kpz_dtr_phase_kernel",
                     "avg_launch_ms": avg_launch_ms, "alg_bytes_per_launch": bytes_per_launch,
-                    "binding_unit": "SM issue / ALU pipe (profiles/r01d_kpz_ncu.txt: issue 74%, ALU 59%, DRAM 6%)",
+                    "binding_unit": "SM issue / ALU pipe (profiles/r01h_kpz_ncu.txt: issue 74%, ALU 59%, DRAM 6%)",
                     "issue_roofline": issue,
                     "note": "algorithmic bytes = 0.5 B/attempt (two 1-bit slope planes read+written once per MCS, "
                             "SURVEY.md §8(d)); the device keeps 1 spin bit per site; the faithful single-hit "
