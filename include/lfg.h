@@ -176,6 +176,17 @@ LFG_API int lfg_kpz_strip_fill(lfg_kpz* h, void* rows, int32_t row_capacity, int
 LFG_API int lfg_kpz_strip_row0_heights(lfg_kpz* h, const void* rows, int32_t row_capacity, void* H0);
 LFG_API int lfg_kpz_strip_width_partials(lfg_kpz* h, const void* rows, int32_t row_capacity, int32_t row_begin,
                                          int32_t row_count, int32_t seg_rows, void* P1, void* D, void* P2);
+/* Row-order W^2 pieces (the fast readout; the strip must be a piece of a
+ * lattice reached from an integrable state, which every device state is):
+ * for global rows [row_begin, +row_count) (no wrap past L-1) with heights
+ * relative to B = the column-0 height of the row below the piece (B = 0 for
+ * row_begin = 0, which anchors h(0,0) = 0 as kpz.cpp:66 does):
+ * out3[0] = sum h_rel, out3[1] = sum h_rel^2, out3[2] = net column-0 step D.
+ * The ghost row below the piece must be current.  The caller walks the pieces
+ * in global row order: sum h += s1 + n L B, sum h^2 += s2 + 2 B s1 + n L B^2,
+ * B += D (n = row_count).  Synchronous. */
+LFG_API int lfg_kpz_strip_width_rows(lfg_kpz* h, const void* rows, int32_t row_capacity, int32_t row_begin,
+                                     int32_t row_count, int64_t out3[3]);
 /* Combine segments given in global row order (seg_len int32[nseg], device):
  * sum h and sum h^2 - sum p^2 (add the all-reduced P2 to get sum h^2). */
 LFG_API int lfg_kpz_width_combine(lfg_kpz* h, const void* H0, const void* P1, const void* D, const void* seg_len,

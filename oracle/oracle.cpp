@@ -303,13 +303,13 @@ int orc_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, u
     int64_t dep = 0, det = 0;
     for (int32_t s = 0; s < nsweeps; ++s) {
         const uint64_t sweep = sweep0 + uint64_t(s);
-        orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
-            const int o = kpz_attempt(L, x, y, i, j, p, q, [&] {
+        const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
+            return kpz_attempt(L, x, y, i, j, p, q, [&] {
                 return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
             });
-            dep += o == 0;
-            det += o == 1;
         });
+        dep += c.dep;
+        det += c.det;
     }
     counters[0] += int64_t(L) * L * nsweeps;
     counters[1] += dep + det;
@@ -442,13 +442,13 @@ int orc_kmc_sweep_dt(int32_t L, uint64_t* w, double eps, int both, uint64_t seed
     orc::KmcPlan pl{L, bk};
     int64_t succ = 0;
     for (int32_t s = 0; s < nsweeps; ++s) {
-        orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
-                          [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
-                              const int32_t site[3] = {x, y, z};
-                              succ += kmc_attempt(w, L, site, eps, both,
-                                                  [&] { return orc::below(dir_w, 12); },
-                                                  [&] { return acc_w * 0x1p-32; }) == 0;
-                          });
+        succ += orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
+                                  [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
+                                      const int32_t site[3] = {x, y, z};
+                                      return kmc_attempt(w, L, site, eps, both,
+                                                         [&] { return orc::below(dir_w, 12); },
+                                                         [&] { return acc_w * 0x1p-32; });
+                                  });
     }
     counters[0] += int64_t(L) * L * L / 2 * nsweeps;
     counters[1] += succ;
@@ -462,13 +462,19 @@ int orc_kmc_dt_phase_rows(int32_t L, uint64_t* w, double eps, int both, uint64_t
     if (!(eps >= 0.0) || phase < 0 || phase > 7) return -1;
     orc::KmcPlan pl{L, bk};
     const orc::KmcSweepDraw d = orc::kmc_sweep_draw(pl, seed, sweep);
-    int64_t succ = 0, att = 0;
-    orc::kmc_dt_phase(pl, d, seed, sweep, phase, bz0, bz0 + nbz,
+    int64_t att = 0;
+    {
+        const int32_t nb = L / bk;
+        const int set = d.perm[phase], sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
+        for (int32_t bzi = sz; bzi < nb; bzi += 2)
+            if (bzi >= bz0 && bzi < bz0 + nbz) att += int64_t((nb - sy + 1) / 2) * ((nb - sx + 1) / 2);
+        att *= int64_t(bk) * bk * bk / 2;
+    }
+    const int64_t succ = orc::kmc_dt_phase(pl, d, seed, sweep, phase, bz0, bz0 + nbz,
                       [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
                           const int32_t site[3] = {x, y, z};
-                          ++att;
-                          succ += kmc_attempt(w, L, site, eps, both, [&] { return orc::below(dir_w, 12); },
-                                              [&] { return acc_w * 0x1p-32; }) == 0;
+                          return kmc_attempt(w, L, site, eps, both, [&] { return orc::below(dir_w, 12); },
+                                             [&] { return acc_w * 0x1p-32; });
                       });
     counters[0] += att;
     counters[1] += succ;

@@ -29,8 +29,13 @@
 // mismatch between the two shows up as a parity failure.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstddef>
+#include <cstdlib>
+#include <thread>
+#include <vector>
 
 namespace orc {
 
@@ -83,6 +88,48 @@ inline void perm4(uint32_t idx, int out[4]) {
     }
 }
 
+// ---------------------------------------------------------------- threads
+// parallel_rows(n, body): body(row, slot) for row = 0..n-1 on a pool of
+// std::threads (dynamic row claiming; the image has no OpenMP runtime).  Each
+// thread accumulates into its own Counts slot, summed after the join.  Thread
+// count: ORC_THREADS, else hardware_concurrency().
+struct Counts {
+    int64_t dep = 0, det = 0;
+};
+
+inline int oracle_threads() {
+    if (const char* e = std::getenv("ORC_THREADS")) {
+        const int n = std::atoi(e);
+        if (n > 0) return n;
+    }
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? int(h) : 1;
+}
+
+template <class Body>
+Counts parallel_rows(int32_t n, bool allow, Body&& body) {
+    const int nt = allow ? std::min<int>(oracle_threads(), n) : 1;
+    if (nt <= 1) {
+        Counts c;
+        for (int32_t r = 0; r < n; ++r) body(r, c);
+        return c;
+    }
+    std::atomic<int32_t> next{0};
+    std::vector<Counts> part(static_cast<size_t>(nt));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+            for (int32_t r; (r = next.fetch_add(1)) < n;) body(r, part[size_t(t)]);
+        });
+    for (auto& th : pool) th.join();
+    Counts c;
+    for (const auto& p : part) {
+        c.dep += p.dep;
+        c.det += p.det;
+    }
+    return c;
+}
+
 // ---------------------------------------------------------------- KPZ DTr plan
 // Inner geometry is fixed: domains 16 (x) x 8 (y) sites, tiles 32 x 16 (one
 // 32-bit word per tile row), four inner sets (hx, hy), 512 single-hit rounds
@@ -110,23 +157,39 @@ inline KpzSweepDraw kpz_sweep_draw(const KpzPlan& pl, uint64_t seed, uint64_t sw
     return d;
 }
 
+// Outcome codes returned by the attempt functors (kpz_attempt_impl's
+// KpzOutcome, kpz.hpp:31; KMC: 0 = exchanged, anything else = rejected).
+enum : int { OUT_DEPOSIT = 0, OUT_DETACH = 1, OUT_REJECT = 2 };
+
 // One DTr sweep.  attempt(i, j, tile_id, round) performs one KPZ attempt at
-// anchor (i, j); the callee derives the acceptance word from (tile_id, round)
-// via accept_word() when -- and only when -- a pattern matches, mirroring the
-// reference's lazy get_r() (kpz.hpp:87-95).
+// anchor (i, j) and returns its outcome code; the callee derives the
+// acceptance word from (tile_id, round) via accept_word() when -- and only
+// when -- a pattern matches, mirroring the reference's lazy get_r()
+// (kpz.hpp:87-95).
+//
+// Parallel execution (parallel_rows): the active blocks of one phase are one block
+// apart, so their attempts touch disjoint sites (reach +1 < the block gap) and
+// the lattice after the phase does not depend on the order in which blocks run.
+// Block ROWS are distributed over threads: every block row owns whole lattice
+// rows (rows are L bits = whole 64-bit words for L >= 64), so no two threads
+// ever read-modify-write the same word.  Blocks within a row run in order on
+// one thread (neighbouring blocks of a row may share a word at bx = 32).
 template <class Attempt>
-void kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
     const int32_t L = pl.L, mask = L - 1;
     const KpzSweepDraw d = kpz_sweep_draw(pl, seed, sweep);
     const int32_t nbx = L / pl.bx, nby = L / pl.by;
     const int32_t twx = pl.bx / kTileW, thy = pl.by / kTileH;   // tiles per block
     const int32_t tiles_per_row = L / kTileW;
     const int ntiles = twx * thy;
-    uint32_t* anc = new uint32_t[size_t(ntiles) * 4];
+    Counts tot;
     for (int k = 0; k < 4; ++k) {
         const int set = d.perm[k];
         const int sx = set & 1, sy = set >> 1;
-        for (int32_t byi = sy; byi < nby; byi += 2) {
+        const int32_t nrows = (nby - sy + 1) / 2;
+        const Counts c = parallel_rows(nrows, L >= 64, [&](int32_t row, Counts& acc) {
+            const int32_t byi = sy + 2 * row;
+            uint32_t* anc = new uint32_t[size_t(ntiles) * 4];
             for (int32_t bxi = sx; bxi < nbx; bxi += 2) {
                 const uint32_t block_id = uint32_t(byi) * uint32_t(nbx) + uint32_t(bxi);
                 uint32_t sw[4] = {0, 0, 0, 0};
@@ -144,19 +207,24 @@ void kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& a
                             // consumed from the TOP of each Philox word (h = k >> 3, k' = k & 7):
                             //   xd = bits [28-4k', +4) of word h      (words 0, 1)
                             //   yd = bits [29-3k', +3) of word 2 + h  (words 2, 3; low 8 bits unused)
-                            const int k = r & 15, h = k >> 3, kk = k & 7;
+                            const int kb = r & 15, h = kb >> 3, kk = kb & 7;
                             const int32_t xd = int32_t((a4[h] >> (28 - 4 * kk)) & 15u);
                             const int32_t yd = int32_t((a4[2 + h] >> (29 - 3 * kk)) & 7u);
                             const int32_t i = (d.ox + kTileW * gx + kDomW * hx + xd) & mask;
                             const int32_t j = (d.oy + kTileH * gy + kDomH * hy + yd) & mask;
-                            attempt(i, j, tile_id, r);
+                            const int o = attempt(i, j, tile_id, r);
+                            acc.dep += o == OUT_DEPOSIT;
+                            acc.det += o == OUT_DETACH;
                         }
                     }
                 }
             }
-        }
+            delete[] anc;
+        });
+        tot.dep += c.dep;
+        tot.det += c.det;
     }
-    delete[] anc;
+    return tot;
 }
 
 inline uint32_t kpz_accept_word(uint64_t seed, uint64_t sweep, uint32_t tile_id, int round) {
@@ -210,19 +278,28 @@ inline KmcSweepDraw kmc_sweep_draw(const KmcPlan& pl, uint64_t seed, uint64_t sw
 // One phase k (0..7) of a KMC DT sweep, restricted to block z-rows
 // [bz_lo, bz_hi) of the shifted frame (the whole lattice: 0, L/bk -- the
 // z-slab driver runs each rank's rows).  attempt(x, y, z, dir_word,
-// accept_word) performs one exchange attempt at the fcc-valid site (x, y, z).
-// The site draw follows KmcKernel::draw_site (kmc.hpp:154-171) over the
-// domain box: x and y uniform, z uniform over the parity-matched planes.
+// accept_word) performs one exchange attempt at the fcc-valid site (x, y, z)
+// and returns 0 when the pair was exchanged.  The site draw follows
+// KmcKernel::draw_site (kmc.hpp:154-171) over the domain box: x and y
+// uniform, z uniform over the parity-matched planes.  Returns the number of
+// exchanges.
+//
+// Parallel execution (parallel_rows) over the (z, y) block rows of the phase: active
+// blocks are one block apart and the attempt reaches 2 sites (read) / 1 site
+// (write), so concurrent block rows touch disjoint x-rows of the lattice, which
+// are whole 64-bit words for L >= 64.  Blocks along x run in order on one thread.
 template <class Attempt>
-void kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, uint64_t sweep, int k, int32_t bz_lo,
-                  int32_t bz_hi, Attempt&& attempt) {
+int64_t kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, uint64_t sweep, int k, int32_t bz_lo,
+                     int32_t bz_hi, Attempt&& attempt) {
     const int32_t L = pl.L, mask = L - 1;
     const int32_t nb = L / pl.bk, tb = pl.bk / kKmcTile, tl = L / kKmcTile;
     const int set = d.perm[k];
     const int sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
-    for (int32_t bzi = sz; bzi < nb; bzi += 2) {
-        if (bzi < bz_lo || bzi >= bz_hi) continue;
-        for (int32_t byi = sy; byi < nb; byi += 2)
+    const int32_t nh = (nb - sy + 1) / 2;            // active block rows along y
+    const int32_t nrows = ((nb - sz + 1) / 2) * nh;  // (z, y) block rows
+    const Counts c = parallel_rows(nrows, L >= 64, [&](int32_t row, Counts& acc) {
+        const int32_t bzi = sz + 2 * (row / nh), byi = sy + 2 * (row % nh);
+        if (bzi < bz_lo || bzi >= bz_hi) return;
         for (int32_t bxi = sx; bxi < nb; bxi += 2) {
             const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
             uint32_t sw[4] = {0, 0, 0, 0};
@@ -245,18 +322,21 @@ void kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, uint6
                     const int32_t t = (x ^ y) & 1;
                     const int32_t zfirst = z0 + (((z0 & 1) == t) ? 0 : 1);
                     const int32_t z = (zfirst + 2 * int32_t((w[0] >> 4) & 1u)) & mask;
-                    attempt(x, y, z, w[1], w[2]);
+                    acc.dep += attempt(x, y, z, w[1], w[2]) == 0;
                 }
             }
         }
-    }
+    });
+    return c.dep;
 }
 
 // One KMC DT sweep: the eight phases in the sweep's drawn order.
 template <class Attempt>
-void kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
+int64_t kmc_dt_sweep(const KmcPlan& pl, uint64_t seed, uint64_t sweep, Attempt&& attempt) {
     const KmcSweepDraw d = kmc_sweep_draw(pl, seed, sweep);
-    for (int k = 0; k < 8; ++k) kmc_dt_phase(pl, d, seed, sweep, k, 0, pl.L / pl.bk, attempt);
+    int64_t succ = 0;
+    for (int k = 0; k < 8; ++k) succ += kmc_dt_phase(pl, d, seed, sweep, k, 0, pl.L / pl.bk, attempt);
+    return succ;
 }
 
 }  // namespace orc

@@ -248,13 +248,13 @@ int ref_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, u
         int64_t dep = 0, det = 0;
         for (int32_t s = 0; s < nsweeps; ++s) {
             const uint64_t sweep = sweep0 + uint64_t(s);
-            orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
-                const auto o = lf::detail::kpz_attempt_impl<false>(f, i, j, params, [&] {
+            const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
+                return int(lf::detail::kpz_attempt_impl<false>(f, i, j, params, [&] {
                     return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
-                });
-                dep += o == lf::KpzOutcome::deposited;
-                det += o == lf::KpzOutcome::detached;
+                }));
             });
+            dep += c.dep;
+            det += c.det;
         }
         store_field(f, x, y);
         counters[0] += int64_t(L) * L * nsweeps;
@@ -307,22 +307,22 @@ int ref_kmc_sweep_dt(int32_t L, uint64_t* words, double eps, int both, uint64_t 
         orc::KmcPlan pl{L, bk};
         int64_t succ = 0;
         for (int32_t s = 0; s < nsweeps; ++s) {
-            orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
-                              [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
+            succ += orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
+                                      [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
                 const lf::Coord3 site{x, y, z};
                 const bool here_b = lat.is_b(x, y, z);
-                if (!here_b && params.active_mode == lf::ActiveMode::b_only) return;
+                if (!here_b && params.active_mode == lf::ActiveMode::b_only) return 1;
                 const auto& d = lf::kFccOffsets[orc::below(dir_w, 12)];
                 const lf::Coord3 partner{(x + d[0]) & mask, (y + d[1]) & mask, (z + d[2]) & mask};
                 const bool partner_b = lat.is_b(partner[0], partner[1], partner[2]);
-                if (partner_b == here_b) return;
+                if (partner_b == here_b) return 1;
                 const lf::Coord3 b_pos = here_b ? site : partner;
                 const lf::Coord3 a_pos = here_b ? partner : site;
                 const double w = lf::exchange_probability<false>(lat, b_pos, a_pos, params);
-                if (w < 1.0 && !(acc_w * 0x1p-32 < w)) return;
+                if (w < 1.0 && !(acc_w * 0x1p-32 < w)) return 2;
                 lat.set_b(b_pos[0], b_pos[1], b_pos[2], false);
                 lat.set_b(a_pos[0], a_pos[1], a_pos[2], true);
-                ++succ;
+                return 0;
             });
         }
         std::memcpy(words, lat.words(), words3(L) * 8);

@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_strip_row0_heights", P, P, I32, P)
     _sig(L, "lfg_kpz_strip_width_partials", P, P, I32, I32, I32, I32, P, P, P)
     _sig(L, "lfg_kpz_width_combine", P, P, P, P, P, I32, C.POINTER(I64), C.POINTER(I64))
+    _sig(L, "lfg_kpz_strip_width_rows", P, P, I32, I32, I32, C.POINTER(I64))
     _bind_kmc(L)
     _lib = L
     return L

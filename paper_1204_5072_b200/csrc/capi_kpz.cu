@@ -57,6 +57,12 @@ struct lfg_kpz {
     unsigned int* next_job = nullptr;       // whole-sweep kernel claim counter
     uint32_t epoch = 0;
     unsigned long long* hpin = nullptr;     // pinned readback [max(3, 2R)]
+    // Global closure of each replica's field (reconstruct_heights, kpz.cpp:35-47):
+    // dbad[r] != 0 <=> row/column slope sums are not zero.  Set at create (the
+    // all -1 field is not closed), init_flat (closed) and upload; sweeps keep it
+    // (the octahedron move preserves every row and column sum).
+    unsigned long long* dbad = nullptr;     // [R]
+    unsigned long long* dglob = nullptr;    // upload scratch: global-closure violations
 
     size_t words_per_replica() const { return size_t(L) * size_t(L / 32); }
     uint32_t* rep(int r) const { return f + size_t(r) * words_per_replica(); }
@@ -110,19 +116,19 @@ void ensure_slope_scratch(lfg_kpz* h) {
 }
 
 void ensure_width_scratch(lfg_kpz* h) {
-    const int S = kpz_width_segment_rows(h->L), G = h->L / S;
     if (!h->H0) h->H0 = dmalloc<int32_t>(size_t(h->L), "alloc width scratch");
-    if (!h->P1) h->P1 = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
-    if (!h->Dd) h->Dd = dmalloc<int32_t>(size_t(G) * h->L, "alloc width scratch");
     if (!h->wout) h->wout = dmalloc<unsigned long long>(3, "alloc width scratch");
-    if (!h->seglen) {
-        h->seglen = dmalloc<int32_t>(size_t(G), "alloc width scratch");
-        std::vector<int32_t> v(size_t(G), S);
-        cuda_check(cudaMemcpy(h->seglen, v.data(), 4 * size_t(G), cudaMemcpyHostToDevice), "seglen");
-    }
 }
 
 void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel execution"); }
+
+// interface_width sums of replica r into out3 (device): [0] sum h, [1] sum h^2
+// (row-order scan, kpz_width.cu), [2] scratch.
+void enqueue_width(lfg_kpz* h, int32_t r, unsigned long long* out3) {
+    ensure_width_scratch(h);
+    cuda_check(cudaMemsetAsync(out3, 0, 24, h->stream), "memset");
+    cuda_check(kpz_launch_width_rows(h->rep(r), h->L, h->L - 1, 0, h->L, h->H0, out3, h->stream), "width scan");
+}
 
 // LFG_KPZ_SWEEP_KERNEL=1 runs each sweep as one persistent whole-sweep launch
 // (kpz_dtr_sweep_kernel: no wave-quantisation gap between phases; same lattice
@@ -258,6 +264,8 @@ int lfg_kpz_create_batch(lfg_kpz** out, int32_t L, double p, double q, const uin
             cuda_check(cudaMemcpyAsync(h->dseeds, seeds, sizeof(uint64_t) * replicas, cudaMemcpyHostToDevice,
                                        h->stream), "seed upload");
             cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 2 * replicas, h->stream), "memset");
+            h->dbad = dmalloc<unsigned long long>(size_t(replicas), "alloc closure flags");
+            cuda_check(cudaMemsetAsync(h->dbad, 0x01, sizeof(unsigned long long) * replicas, h->stream), "memset");
             // SlopeField(L) starts with every slope -1 (lattice.cpp:20-25): spins f(i,j) = (i + j) & 1.
             cuda_check(kpz_launch_init_zero_slopes(h->f, L, replicas, h->stream), "init");
             cuda_check(cudaStreamSynchronize(h->stream), "create");
@@ -297,6 +305,8 @@ int lfg_kpz_destroy(lfg_kpz* h) {
         dfree(h->hbuf);
         dfree(h->flags);
         dfree(h->next_job);
+        dfree(h->dbad);
+        dfree(h->dglob);
         if (h->hpin) cudaFreeHost(h->hpin);
         if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
         if (prev >= 0) cudaSetDevice(prev);
@@ -319,6 +329,7 @@ int lfg_kpz_init_flat(lfg_kpz* h) {
         check_resident(h);
         DeviceGuard g(h->device);
         cuda_check(kpz_launch_init_flat(h->f, h->L, h->R, h->stream), "init_flat");
+        cuda_check(cudaMemsetAsync(h->dbad, 0, sizeof(unsigned long long) * h->R, h->stream), "memset");
         sync(h);
     });
 }
@@ -328,7 +339,10 @@ int lfg_kpz_init_flat(lfg_kpz* h) {
 namespace {
 
 // H2D of the two slope planes + device conversion to spins (h->fnew) + the
-// closure re-derivation check (mismatches counted into h->dmis).
+// closure checks: a field that is not the slope field of its spin field, or
+// has an elementary plaquette that does not close, is counted into h->dmis
+// (rejected); nonzero row-0 / column-0 sums go to h->dglob (accepted -- the
+// reference sweeps such fields -- but reconstruct_heights refuses them).
 void enqueue_upload(lfg_kpz* h, const uint64_t* x, const uint64_t* y) {
     ensure_slope_scratch(h);
     if (!h->f0) h->f0 = dmalloc<uint8_t>(size_t(h->L), "alloc scratch");
@@ -343,6 +357,16 @@ void enqueue_upload(lfg_kpz* h, const uint64_t* x, const uint64_t* y) {
     cuda_check(kpz_launch_from_slopes(h->sx, h->sy, h->L, h->f0, h->fnew, h->stream), "slopes->spins");
     cuda_check(kpz_launch_to_slopes(h->fnew, h->L, nullptr, nullptr, h->sx, h->sy, h->dmis, h->stream),
                "closure check");
+    if (!h->dglob) h->dglob = dmalloc<unsigned long long>(1, "alloc scratch");
+    cuda_check(cudaMemsetAsync(h->dglob, 0, 8, h->stream), "memset");
+    cuda_check(kpz_launch_closure_check(h->sx, h->sy, h->L, h->dmis, h->dglob, h->stream), "closure check");
+}
+
+// The uploaded field becomes replica r's state: spins and global-closure flag.
+void commit_upload(lfg_kpz* h, int32_t r) {
+    cuda_check(cudaMemcpyAsync(h->rep(r), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice, h->stream),
+               "commit");
+    cuda_check(cudaMemcpyAsync(h->dbad + r, h->dglob, 8, cudaMemcpyDeviceToDevice, h->stream), "commit");
 }
 
 void check_upload_args(lfg_kpz* h, int32_t replica, const void* x, const void* y, size_t nwords) {
@@ -371,8 +395,7 @@ int lfg_kpz_upload(lfg_kpz* h, int32_t replica, const uint64_t* x, const uint64_
         cuda_check(cudaMemcpyAsync(h->hpin, h->dmis, 8, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         if (h->hpin[0] != 0) throw_closure();  // state unchanged
-        cuda_check(cudaMemcpyAsync(h->rep(replica), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice,
-                                   h->stream), "commit");
+        commit_upload(h, replica);
         sync(h);
     });
 }
@@ -382,8 +405,7 @@ int lfg_kpz_upload_async(lfg_kpz* h, int32_t replica, const uint64_t* x, const u
         check_upload_args(h, replica, x, y, nwords);
         DeviceGuard g(h->device);
         enqueue_upload(h, x, y);  // mismatches accumulate in dmis until lfg_kpz_upload_check
-        cuda_check(cudaMemcpyAsync(h->rep(replica), h->fnew, h->words_per_replica() * 4, cudaMemcpyDeviceToDevice,
-                                   h->stream), "commit");
+        commit_upload(h, replica);
     });
 }
 
@@ -510,14 +532,11 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         check_handle(h);
         check_replica(h, replica);
         DeviceGuard g(h->device);
-        ensure_width_scratch(h);
-        cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
-        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->seglen, h->wout, h->stream),
-                   "width scan");
+        enqueue_width(h, replica, h->wout);
         cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         *sum = int64_t(h->hpin[0]);
-        *sum2 = int64_t(h->hpin[1] + h->hpin[2]);
+        *sum2 = int64_t(h->hpin[1]);
     });
 }
 
@@ -543,10 +562,7 @@ int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3) {
         check_replica(h, replica);
         if (!out3) throw Error(LFG_EINVAL, "null output");
         DeviceGuard g(h->device);
-        ensure_width_scratch(h);
-        cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
-        cuda_check(kpz_launch_width(h->rep(replica), h->L, h->H0, h->P1, h->Dd, h->seglen, h->wout, h->stream),
-                   "width scan");
+        enqueue_width(h, replica, h->wout);
         cuda_check(cudaMemcpyAsync(out3, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
     });
 }
@@ -569,6 +585,9 @@ int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n) {
         if (n != need || !heights) throw Error(LFG_EINVAL, "heights: expected L*L entries");
         if (h->L > 16384) throw Error(LFG_EINVAL, "heights: L*L int32 readout limited to L <= 16384");
         DeviceGuard g(h->device);
+        cuda_check(cudaMemcpyAsync(h->hpin, h->dbad + replica, 8, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        if (h->hpin[0] != 0) throw_closure();  // kpz.cpp:37-47: row/column sums must vanish
         ensure_width_scratch(h);
         if (!h->hbuf) h->hbuf = dmalloc<int32_t>(need, "alloc heights");
         cuda_check(kpz_launch_heights(h->rep(replica), h->L, h->H0, h->hbuf, h->stream), "heights");
@@ -770,6 +789,26 @@ int lfg_kpz_strip_width_partials(lfg_kpz* h, const void* rows, int32_t cap, int3
                                              seg_rows, static_cast<int32_t*>(P1), static_cast<int32_t*>(D),
                                              static_cast<unsigned long long*>(P2), h->stream),
                    "width partials");
+    });
+}
+
+int lfg_kpz_strip_width_rows(lfg_kpz* h, const void* rows, int32_t cap, int32_t row_begin, int32_t row_count,
+                             int64_t out3[3]) {
+    return guarded([&] {
+        check_handle(h);
+        check_ring(h, rows, cap);
+        if (row_count < 0 || row_count > h->L || row_begin < 0 || row_begin >= h->L)
+            throw Error(LFG_EINVAL, "width rows: bad row range");
+        if (!out3) throw Error(LFG_EINVAL, "null output");
+        DeviceGuard g(h->device);
+        ensure_width_scratch(h);
+        cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
+        cuda_check(kpz_launch_width_rows(static_cast<const uint32_t*>(rows), h->L, cap - 1, row_begin, row_count,
+                                         h->H0, h->wout, h->stream),
+                   "width rows");
+        cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
+        sync(h);
+        for (int k = 0; k < 3; ++k) out3[k] = int64_t(h->hpin[k]);
     });
 }
 

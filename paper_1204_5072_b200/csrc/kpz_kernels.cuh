@@ -81,6 +81,17 @@ cudaError_t kpz_launch_width_combine(const int32_t* H0, const int32_t* P1, const
                                      int L, int G, unsigned long long* out2, cudaStream_t st);
 cudaError_t kpz_launch_fill_rows(uint32_t* f, int L, int rmask, int row_begin, int row_count, int pattern,
                                  cudaStream_t st);
+// Row-order W^2 sums of a locally closed spin lattice (kpz_width.cu): global
+// rows [row_begin, +row_count) of a ring buffer (slot = row & rmask), heights
+// relative to the column-0 height of the row below the piece (0 at global row
+// 0).  out3[0] += sum h, out3[1] += sum h^2, out3[2] = net column-0 step of
+// the piece (as int64); V: int32[row_count] scratch.
+cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int32_t* V,
+                                  unsigned long long* out3, cudaStream_t st);
+// Closure of two uploaded slope planes: plaquettes that do not close ->
+// *local_bad; row 0 / column 0 sums != 0 -> *global_bad (kpz.cpp:35-47).
+cudaError_t kpz_launch_closure_check(const uint32_t* X, const uint32_t* Y, int L, unsigned long long* local_bad,
+                                     unsigned long long* global_bad, cudaStream_t st);
 cudaError_t kpz_launch_heights(const uint32_t* f, int L, int32_t* H0, int32_t* h, cudaStream_t st);
 
 }  // namespace lfg

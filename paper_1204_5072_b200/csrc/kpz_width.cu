@@ -1,0 +1,264 @@
+// kpz_width.cu -- sm_100a readouts of the KPZ spin lattice: the W^2 sums of
+// interface_width(const SlopeField&) (kpz.cpp:62-81) and the closure checks of
+// reconstruct_heights (kpz.cpp:35-47) applied at upload.
+//
+// W^2 by rows.  interface_width integrates the slopes along row 0 and then up
+// every column (kpz.cpp:66-77).  Every lattice the device holds is locally
+// closed -- each elementary plaquette closes: the init patterns do, an upload
+// whose plaquettes do not is rejected (kpz_plaquette_kernel), and the octahedron
+// move preserves every plaquette sum -- so the height of site (i, j) is the
+// same along any path inside [0, L)^2 from (0, 0): up column 0, then along
+// row j.  That order reads each row contiguously:
+//   V(j)   = sum_{k=1..j} s_y(0, k)                        (kpz_col0_steps_kernel)
+//   h(i,j) = V(j) + sum_{k=1..i} s_x(k, j)                 (kpz_width_rows_kernel)
+// and sum h, sum h^2 are exact int64, finished on the host as kpz.cpp:78-80.
+//
+// Row kernel: one warp per row, 128 words (4096 sites) per step, one 16-byte
+// load per lane.  A lane turns its four spin words into s_x bits, then sums its
+// 128 sites byte by byte from a 256-entry table of per-byte partial sums
+// (S1 = sum of prefix heights, S2 = sum of their squares, D = net step), kept
+// in 32 bank-private copies so the random table reads of a warp are
+// conflict-free.  A warp scan of D gives every lane its start height; the lane
+// partials (relative heights, 32-bit) are then shifted to absolute heights in
+// 64-bit: sum (o + d) = n o + S1, sum (o + d)^2 = n o^2 + 2 o S1 + S2.
+#include <algorithm>
+#include <cstdint>
+
+#include "kpz_kernels.cuh"
+
+namespace lfg {
+
+// Per-byte table entry: byte 0 = S2 (0..204), byte 1 = S1 (signed, -36..36),
+// byte 2 = D (signed, -8..8), for the 8 steps s_t = 2 b_t - 1 of the byte
+// (bit t = +1 step), prefix heights m_t = sum_{u <= t} s_u.
+__device__ __forceinline__ uint32_t width_byte_entry(uint32_t v) {
+    int m = 0, s1 = 0, s2 = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        m += ((v >> t) & 1u) ? 1 : -1;
+        s1 += m;
+        s2 += m * m;
+    }
+    return uint32_t(s2) | (uint32_t(s1 & 0xFF) << 8) | (uint32_t(m & 0xFF) << 16);
+}
+
+__device__ __forceinline__ int32_t prmt_s(uint32_t e, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(e), "r"(sel));
+    return int32_t(r);
+}
+
+// Column-0 heights of global rows row_begin + k (k < n), relative to the row
+// below the piece: V[k] = sum_{m <= k} s_y(0, row_begin + m), where the step
+// into global row 0 is 0 (interface_width anchors h(0, 0) = 0).  One CTA.
+// out_d (may be null): V[n-1], the piece's net column-0 step.
+__global__ void __launch_bounds__(1024) kpz_col0_steps_kernel(const uint32_t* __restrict__ f, int L, int rmask,
+                                                              int row_begin, int n, int32_t* __restrict__ V,
+                                                              long long* __restrict__ out_d) {
+    __shared__ int32_t wsum[32];
+    const int wpr = L >> 5, Lm = L - 1;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int chunk = (n + 1023) / 1024;
+    const int k0 = t * chunk, k1 = min(n, k0 + chunk);
+    auto step = [&](int k) -> int32_t {
+        const int g = (row_begin + k) & Lm;
+        if (g == 0) return 0;
+        const uint32_t a = f[size_t(g & rmask) * wpr] & 1u;
+        const uint32_t b = f[size_t(((g - 1) & Lm) & rmask) * wpr] & 1u;
+        return a == b ? 1 : -1;
+    };
+    int32_t s = 0;
+    for (int k = k0; k < k1; ++k) s += step(k);
+    // block exclusive scan of s
+    int32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = wsum[lane], wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    int32_t acc = wsum[warp] + inc - s;
+    for (int k = k0; k < k1; ++k) {
+        acc += step(k);
+        V[k] = acc;
+    }
+    if (out_d && k1 == n && k0 < k1) *out_d = acc;
+    if (out_d && n == 0 && t == 0) *out_d = 0;
+}
+
+// Sum of heights and of squared heights over global rows row_begin + k (k < n),
+// heights relative to V (see kpz_col0_steps_kernel).  out2[0] += sum h,
+// out2[1] += sum h^2 (two's complement; exact as int64).
+template <bool VEC>
+__global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __restrict__ f, int L, int rmask,
+                                                             int row_begin, int n, const int32_t* __restrict__ V,
+                                                             unsigned long long* __restrict__ out2) {
+    __shared__ uint32_t tab[256 * 32];  // entry v of lane l at word v * 32 + l (bank l)
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+        const uint32_t e = width_byte_entry(uint32_t(v));
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) tab[v * 32 + ((l + v) & 31)] = e;  // rotated: the 32 stores of a warp hit 32 banks
+    }
+    __syncthreads();
+    const int wpr = L >> 5, Lm = L - 1;
+    const int lane = threadIdx.x & 31;
+    const int wpb = int(blockDim.x >> 5);
+    long long s1 = 0, s2 = 0;
+    // grid-stride over rows (the grid is sized to the resident CTAs, so each
+    // CTA builds its table once)
+    for (int k = int(blockIdx.x) * wpb + int(threadIdx.x >> 5); k < n; k += int(gridDim.x) * wpb) {
+        const int g = (row_begin + k) & Lm;
+        const uint32_t* __restrict__ row = f + size_t(g & rmask) * wpr;
+        int32_t base = V[k] - 1;   // site 0 enters as a +1 step from V - 1
+        uint32_t top = 0;          // bit 31 of the previous chunk's last word
+        for (int c = 0; c < wpr; c += 128) {
+            uint32_t F[4];
+            int nw = 4;  // valid words of this lane (all four when VEC)
+            if (VEC) {
+                const uint4 q = *reinterpret_cast<const uint4*>(row + c + 4 * lane);
+                F[0] = q.x; F[1] = q.y; F[2] = q.z; F[3] = q.w;
+            } else {
+                const int w0 = c + 4 * lane;
+                nw = max(0, min(4, wpr - w0));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) F[u] = u < nw ? row[w0 + u] : 0u;
+            }
+            const uint32_t prev_lane = __shfl_up_sync(0xFFFFFFFFu, F[3], 1);
+            uint32_t prev = lane == 0 ? top : prev_lane;
+            top = __shfl_sync(0xFFFFFFFFu, F[3], 31);
+            int32_t o = 0, a1 = 0, a2 = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t X = ~(F[u] ^ ((F[u] << 1) | (prev >> 31)));  // bit b: s_x of site b is +1
+                prev = F[u];
+                if (c == 0 && lane == 0 && u == 0) X |= 1u;
+                if (!VEC && u >= nw) continue;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    uint32_t v;
+                    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(v) : "r"(X), "r"(0x4440u + uint32_t(b)));
+                    const uint32_t e = tab[(v << 5) + uint32_t(lane)];
+                    const int32_t S2 = prmt_s(e, 0x4440u);
+                    const int32_t S1 = prmt_s(e, 0x9991u);
+                    const int32_t D = prmt_s(e, 0xAAA2u);
+                    const int32_t tt = 8 * o + S1;
+                    a1 += tt;
+                    a2 += o * (tt + S1) + S2;
+                    o += D;
+                }
+            }
+            const int32_t nsites = VEC ? 128 : 32 * nw;
+            // lane start heights: exclusive warp scan of o (net step of each lane)
+            int32_t inc = o;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= d) inc += v;
+            }
+            const int32_t O = base + inc - o;
+            base += __shfl_sync(0xFFFFFFFFu, inc, 31);
+            s1 += (long long)nsites * O + a1;
+            s2 += (long long)O * (long long)(nsites * O + 2 * a1) + a2;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        s1 += __shfl_down_sync(0xFFFFFFFFu, s1, d);
+        s2 += __shfl_down_sync(0xFFFFFFFFu, s2, d);
+    }
+    if (lane == 0 && (s1 | s2)) {
+        atomicAdd(out2 + 0, (unsigned long long)s1);
+        atomicAdd(out2 + 1, (unsigned long long)s2);
+    }
+}
+
+cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int32_t* V,
+                                  unsigned long long* out3, cudaStream_t st) {
+    kpz_col0_steps_kernel<<<1, 1024, 0, st>>>(f, L, rmask, row_begin, row_count, V,
+                                              reinterpret_cast<long long*>(out3 + 2));
+    const int wpb = 8;
+    // resident CTAs: 32 KB of table each -> 6 per SM; 148 SMs
+    const unsigned grid = unsigned(std::min((row_count + wpb - 1) / wpb, 148 * 6));
+    if (grid == 0) return cudaGetLastError();
+    if ((L >> 5) % 128 == 0)
+        kpz_width_rows_kernel<true><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, V, out3);
+    else
+        kpz_width_rows_kernel<false><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, V, out3);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- closure
+// Upload check of two slope planes X, Y (uint32 words of the reference layout)
+// against reconstruct_heights' path-independence (kpz.cpp:35-47):
+//   local:  every elementary plaquette closes,
+//           s_x(i, j-1) + s_y(i, j) == s_y(i-1, j) + s_x(i, j)   (periodic indices)
+//           -> bad plaquettes counted into local_bad;
+//   global: row 0's s_x and column 0's s_y sum to zero (with local closure,
+//           every row / column then does) -> deviations counted into global_bad.
+// A locally closed field with nonzero row sums (e.g. the all -1 field of
+// SlopeField(L), lattice.cpp:20-25) is representable and swept exactly, but
+// reconstruct_heights rejects it.
+__global__ void kpz_plaquette_kernel(const uint32_t* __restrict__ X, const uint32_t* __restrict__ Y, int L,
+                                     unsigned long long* __restrict__ local_bad) {
+    const int wpr = L >> 5, wmask = wpr - 1, Lm = L - 1;
+    const size_t n = size_t(L) * wpr;
+    unsigned long long bad = 0;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < n; k += size_t(gridDim.x) * blockDim.x) {
+        const int j = int(k / size_t(wpr)), w = int(k % size_t(wpr));
+        const uint32_t c = X[k];                                              // s_x(i, j)
+        const uint32_t a = X[size_t((j - 1) & Lm) * wpr + w];                 // s_x(i, j-1)
+        const uint32_t b = Y[k];                                              // s_y(i, j)
+        const uint32_t d = (b << 1) | (Y[size_t(j) * wpr + ((w - 1) & wmask)] >> 31);  // s_y(i-1, j)
+        // two-bit sums a + b and c + d must agree
+        bad += __popc(((a ^ b) ^ (c ^ d)) | ((a & b) ^ (c & d)));
+    }
+    bad = __reduce_add_sync(0xFFFFFFFFu, unsigned(bad));
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(local_bad, bad);
+}
+
+__global__ void __launch_bounds__(1024) kpz_closure_sums_kernel(const uint32_t* __restrict__ X,
+                                                                const uint32_t* __restrict__ Y, int L,
+                                                                unsigned long long* __restrict__ global_bad) {
+    __shared__ int part[2][32];
+    const int wpr = L >> 5;
+    int rx = 0, cy = 0;  // ones in row 0 of X, in column 0 of Y
+    for (int w = threadIdx.x; w < wpr; w += blockDim.x) rx += __popc(X[w]);
+    for (int j = threadIdx.x; j < L; j += blockDim.x) cy += int(Y[size_t(j) * wpr] & 1u);
+    rx = __reduce_add_sync(0xFFFFFFFFu, rx);
+    cy = __reduce_add_sync(0xFFFFFFFFu, cy);
+    if ((threadIdx.x & 31) == 0) {
+        part[0][threadIdx.x >> 5] = rx;
+        part[1][threadIdx.x >> 5] = cy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int sx = 0, sy = 0;
+        for (int k = 0; k < int(blockDim.x >> 5); ++k) {
+            sx += part[0][k];
+            sy += part[1][k];
+        }
+        if (2 * sx != L || 2 * sy != L) atomicAdd(global_bad, 1ull);
+    }
+}
+
+cudaError_t kpz_launch_closure_check(const uint32_t* X, const uint32_t* Y, int L, unsigned long long* local_bad,
+                                     unsigned long long* global_bad, cudaStream_t st) {
+    const size_t n = size_t(L) * (L >> 5);
+    const int blocks = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    kpz_plaquette_kernel<<<blocks, 256, 0, st>>>(X, Y, L, local_bad);
+    kpz_closure_sums_kernel<<<1, 1024, 0, st>>>(X, Y, L, global_bad);
+    return cudaGetLastError();
+}
+
+}  // namespace lfg

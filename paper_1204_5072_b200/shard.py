@@ -145,6 +145,8 @@ class CudaStripEngine:
                                                device))
         self.h = h
         self.stream = torch.cuda.Stream(device=device)
+        # the zero fill above ran on torch's current stream; the library works on self.stream
+        self.stream.wait_stream(torch.cuda.current_stream(device))
         _native.check(lib.lfg_kpz_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
 
     def close(self):
@@ -178,36 +180,13 @@ class CudaStripEngine:
         _native.check(_native.lib().lfg_kpz_counters(self.h, 0, C.byref(c)))
         return c
 
-    def width_partials(self, pieces, S):
-        """[(start, n)] -> (P1 [nseg, L] int32, D [nseg, L] int32, seg (start, len) list, P2 int)."""
-        torch = self.torch
-        L = self.plan.L
-        segs = []
-        for (a, n) in pieces:
-            for k in range(0, n, S):
-                segs.append((a + k, min(S, n - k)))
-        P1 = torch.zeros((len(segs), L), dtype=torch.int32, device=self.buf.device)
-        D = torch.zeros_like(P1)
-        P2 = torch.zeros(1, dtype=torch.int64, device=self.buf.device)
-        lib = _native.lib()
-        for gi, (a, n) in enumerate(segs):
-            _native.check(lib.lfg_kpz_strip_width_partials(
-                self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap, a, n, n,
-                C.c_void_p(P1[gi].data_ptr()), C.c_void_p(D[gi].data_ptr()), C.c_void_p(P2.data_ptr())))
-        return P1, D, segs, P2
-
-    def row0_heights(self):
-        H0 = self.torch.zeros(self.plan.L, dtype=self.torch.int32, device=self.buf.device)
-        _native.check(_native.lib().lfg_kpz_strip_row0_heights(self.h, C.c_void_p(self.buf.data_ptr()),
-                                                               self.plan.cap, C.c_void_p(H0.data_ptr())))
-        return H0
-
-    def combine(self, H0, P1, D, seglen):
-        s, s2 = C.c_int64(), C.c_int64()
-        _native.check(_native.lib().lfg_kpz_width_combine(
-            self.h, C.c_void_p(H0.data_ptr()), C.c_void_p(P1.data_ptr()), C.c_void_p(D.data_ptr()),
-            C.c_void_p(seglen.data_ptr()), int(seglen.numel()), C.byref(s), C.byref(s2)))
-        return int(s.value), int(s2.value)
+    def width_rows(self, row_begin: int, count: int):
+        """(sum h_rel, sum h_rel^2, net column-0 step) of global rows
+        [row_begin, +count) (no wrap), heights relative to the row below."""
+        out = (C.c_int64 * 3)()
+        _native.check(_native.lib().lfg_kpz_strip_width_rows(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
+                                                             row_begin, count, out))
+        return int(out[0]), int(out[1]), int(out[2])
 
 
 def sweep_origin(plan: StripPlan, seed: int, sweep: int):
@@ -233,9 +212,14 @@ class LocalComm:
                 if kind != "send":
                     continue
                 src, dst = self.engines[r], self.engines[peer]
-                src.sync()
-                for (slot, m) in src.plan.pieces(b, n):
-                    dst.rows(slot, m).copy_(src.rows(slot, m))
+                torch = dst.torch
+                # on the destination engine's stream, after everything already
+                # queued on both engines' streams
+                with torch.cuda.stream(dst.stream):
+                    dst.stream.wait_stream(src.stream)
+                    for (slot, m) in src.plan.pieces(b, n):
+                        dst.rows(slot, m).copy_(src.rows(slot, m))
+                    src.stream.wait_stream(dst.stream)  # src rows not overwritten before the copy reads them
                 dst.sync()
 
 
@@ -321,6 +305,7 @@ class PeerComm(DistComm):
         self.flags = torch.zeros(2, dtype=torch.int32, device=e.buf.device)  # [from lower, from upper]
         self.err = torch.zeros(1, dtype=torch.int32, device=e.buf.device)
         self.max_spins = int(max_spins)
+        torch.cuda.current_stream(e.buf.device).synchronize()  # zero fills done before peers see the flags
         e.sync()
         mine = []
         for t in (e.buf, self.flags):
@@ -511,64 +496,34 @@ class ShardedKpz:
         return out
 
     def width_sums(self):
-        """interface_width sums (kpz.cpp:62-81) of the sharded lattice: exact int64
-        (sum h, sum h^2), h(0,0) = 0.  Segments of all ranks are combined in
-        global row order; H0 comes from the rank that owns row 0."""
-        import torch
-
+        """interface_width sums (kpz.cpp:62-81) of the sharded lattice: exact
+        (sum h, sum h^2) with h(0,0) = 0.  Every rank scans its owned rows in row
+        order (lfg_kpz_strip_width_rows: heights relative to the column-0 height
+        of the row below each piece) and the pieces are chained in global row
+        order from row 0:  sum h += s1 + n L B,  sum h^2 += s2 + 2 B s1 + n L B^2,
+        B += D.  Only (start, rows, s1, s2, D) per piece crosses ranks."""
         pl = self.plan
-        # each piece's first segment reads the row below it (s_y of its first
-        # row): bring both ghost rows up to date first
+        # each piece reads the row below it (s_y of its first column-0 site)
         for sy in (0, 1):
             self._exchange(lambda r: pl.ghost(self.oy, r, sy))
-        S = 2048 if pl.L >= 4096 else max(1, min(pl.L, 128))
-        local = []
-        H0 = None
-        P2 = 0
+        pieces = []
         for e, r in zip(self.engines, self.ranks):
-            pieces = self.owned_pieces(r)
-            P1, D, segs, p2 = e.width_partials(pieces, S)
-            e.sync()
-            P2 += int(p2.item())
-            local.append((P1, D, segs))
-            if any(a == 0 for (a, _) in pieces):
-                H0 = e.row0_heights()
-                e.sync()
-        e0 = self.engines[0]
-        dev = e0.buf.device
+            for (a, n) in self.owned_pieces(r):
+                s1, s2, d = e.width_rows(a, n)
+                pieces.append((a, n, s1, s2, d))
         if isinstance(self.comm, DistComm):
-            dist = self.comm.dist
-            grp = self.comm.group
-            if self.comm.stage:
-                dev = torch.device("cpu")
-                H0 = H0.cpu() if H0 is not None else None
-            segs_all = [None] * self.comm.world
-            dist.all_gather_object(segs_all, [s for (_, _, segs) in local for s in segs], group=grp)
-            P1l = torch.cat([p for (p, _, _) in local]).to(dev)
-            Dl = torch.cat([d for (_, d, _) in local]).to(dev)
-            nmax = max(len(x) for x in segs_all)
-            pad = lambda t: torch.cat([t, torch.zeros((nmax - t.shape[0], pl.L), dtype=t.dtype, device=dev)])  # noqa: E731
-            P1g = [torch.zeros((nmax, pl.L), dtype=torch.int32, device=dev) for _ in range(self.comm.world)]
-            Dg = [torch.zeros_like(P1g[0]) for _ in range(self.comm.world)]
-            dist.all_gather(P1g, pad(P1l), group=grp)
-            dist.all_gather(Dg, pad(Dl), group=grp)
-            h0 = H0 if H0 is not None else torch.zeros(pl.L, dtype=torch.int32, device=dev)
-            dist.all_reduce(h0, group=grp)
-            H0 = h0
-            p2 = torch.tensor([P2], dtype=torch.int64, device=dev)
-            dist.all_reduce(p2, group=grp)
-            P2 = int(p2.item())
-            entries = [(segs_all[r][i], P1g[r][i], Dg[r][i]) for r in range(self.comm.world)
-                       for i in range(len(segs_all[r]))]
-        else:
-            entries = [(segs[i], P1[i].to(dev), D[i].to(dev)) for (P1, D, segs) in local for i in range(len(segs))]
-        entries.sort(key=lambda t: t[0][0])
-        cdev = e0.buf.device
-        P1c = torch.stack([t[1] for t in entries]).to(cdev).contiguous()
-        Dc = torch.stack([t[2] for t in entries]).to(cdev).contiguous()
-        seglen = torch.tensor([t[0][1] for t in entries], dtype=torch.int32, device=cdev)
-        s, s2 = e0.combine(H0.to(cdev).contiguous(), P1c, Dc, seglen)
-        return s, s2 + P2
+            allp = [None] * self.comm.world
+            self.comm.dist.all_gather_object(allp, pieces, group=self.comm.group)
+            pieces = [t for lst in allp for t in lst]
+        pieces.sort(key=lambda t: t[0])
+        assert pieces and pieces[0][0] == 0 and sum(t[1] for t in pieces) == pl.L
+        S1 = S2 = B = 0
+        for (_, n, s1, s2, d) in pieces:
+            m = n * pl.L
+            S1 += s1 + m * B
+            S2 += s2 + 2 * B * s1 + m * B * B
+            B += d
+        return S1, S2
 
     def interface_width(self) -> float:
         s, s2 = self.width_sums()
@@ -694,6 +649,7 @@ class CudaSlabEngine:
                                               C.byref(kp), device))
         self.h = h
         self.stream = torch.cuda.Stream(device=device)
+        self.stream.wait_stream(torch.cuda.current_stream(device))  # after the zero fill of buf
         _native.check(lib.lfg_kmc_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
 
     def close(self):
@@ -716,10 +672,11 @@ class CudaSlabEngine:
         import numpy as np
 
         full = np.asarray(words_u64).view(np.uint32).view(np.int32).reshape(self.plan.L, self.plan.wpp)
-        for (z, n) in self.plan.plane_pieces_global(z_begin, count):
-            for (slot, m) in self.plan.pieces(z, n):
-                self.buf[slot:slot + m].copy_(self.torch.from_numpy(full[z:z + m].copy()))
-                z += m
+        with self.torch.cuda.stream(self.stream):  # ordered with the library's kernels
+            for (z, n) in self.plan.plane_pieces_global(z_begin, count):
+                for (slot, m) in self.plan.pieces(z, n):
+                    self.buf[slot:slot + m].copy_(self.torch.from_numpy(full[z:z + m].copy()))
+                    z += m
 
     def phase(self, sweep: int, phase: int, bz0: int, nbz: int):
         _native.check(_native.lib().lfg_kmc_slab_phase(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,

@@ -61,6 +61,26 @@ class CpuStripEngine:
         c.deposits, c.detaches = self.dep, self.det
         return c
 
+    def width_rows(self, row_begin, count):
+        """Row-order W^2 piece (the contract of lfg_kpz_strip_width_rows):
+        (sum h_rel, sum h_rel^2, D) over global rows [row_begin, +count), heights
+        relative to the column-0 height of the row below (0 at global row 0)."""
+        L, cap = self.plan.L, self.plan.cap
+        w = self.buf.numpy().view(np.uint32)
+        s1 = s2 = 0
+        V = 0
+        for k in range(count):
+            g = (row_begin + k) % L
+            bits = np.unpackbits(w[g & (cap - 1)].view(np.uint8), bitorder="little").astype(np.int64)
+            if g != 0:
+                below = int(w[((g - 1) % L) & (cap - 1), 0]) & 1
+                V += 1 if int(bits[0]) == below else -1
+            steps = np.where(bits[1:] == bits[:-1], 1, -1)
+            h = V + np.concatenate([[0], np.cumsum(steps)])
+            s1 += int(h.sum())
+            s2 += int((h * h).sum())
+        return s1, s2, V
+
     # ---- one phase -------------------------------------------------------------
     def phase(self, sweep, k, brow0, nbrow):
         pl = self.plan

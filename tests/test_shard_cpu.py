@@ -90,9 +90,11 @@ def _worker(rank, world, port, L, bx, by, p, q, seed, nsweeps, out_path):
     dep, det = sk.counters_local()
     c = torch.tensor([dep, det], dtype=torch.int64)
     dist.all_reduce(c)
+    ws = sk.width_sums()
     if rank == 0:
         np.save(out_path, rows.numpy())
         np.save(out_path + ".cnt.npy", c.numpy())
+        np.save(out_path + ".w.npy", np.array(ws, dtype=np.int64))
     dist.destroy_process_group()
 
 
@@ -110,3 +112,5 @@ def test_gloo_world2_matches_full_lattice_oracle(tmp_path, oracle, p, q):
     px, py = spins_to_slopes(rows, L)
     assert (px == x).all() and (py == y).all()
     assert [int(cnt[0]), int(cnt[1])] == [int(c[2]), int(c[3])]
+    # W^2 sums of the sharded lattice (row pieces chained across ranks) == interface_width's
+    assert tuple(int(v) for v in np.load(out + ".w.npy")) == oracle.kpz_width_sums(L, x, y)
