@@ -157,20 +157,28 @@ Counters kpz_sweep(Field& f, const Params& params, Rng& rng, int sweeps = 1, con
     return c;
 }
 
-// interface_width(const SlopeField&) (kpz.cpp:62-81): exact device scan.
+// interface_width(const SlopeField&) (kpz.cpp:62-81): exact device sums over
+// the caller's slope planes, any L the reference accepts, integrable or not.
 template <class Field>
-double interface_width(const Field& f) {
-    KpzDevice d(f.size(), 1.0, 0.0, 0);
-    d.upload(f);
-    return d.interface_width();
+double interface_width(const Field& f, int device = 0) {
+    const std::int32_t L = f.size();
+    const std::size_t nw = (std::size_t(L) * std::size_t(L) + 63) / 64;
+    std::int64_t s = 0, s2 = 0;
+    check(lfg_kpz_width_sums_host(device, L, f.words_x(), f.words_y(), nw, &s, &s2));
+    const double n = static_cast<double>(std::int64_t(L) * L);  // kpz.cpp:78-80
+    const double mean = static_cast<double>(s) / n;
+    return static_cast<double>(s2) / n - mean * mean;
 }
 
-// reconstruct_heights (kpz.cpp:21-49): h(0,0)=0, row-major j*L+i.
+// reconstruct_heights (kpz.cpp:21-49): h(0,0)=0, row-major j*L+i; throws
+// std::runtime_error (the reference's message) when path-dependent.
 template <class Field>
-std::vector<std::int32_t> reconstruct_heights(const Field& f) {
-    KpzDevice d(f.size(), 1.0, 0.0, 0);
-    d.upload(f);
-    return d.reconstruct_heights();
+std::vector<std::int32_t> reconstruct_heights(const Field& f, int device = 0) {
+    const std::int32_t L = f.size();
+    const std::size_t nw = (std::size_t(L) * std::size_t(L) + 63) / 64;
+    std::vector<std::int32_t> out(std::size_t(L) * std::size_t(L));
+    check(lfg_kpz_heights_host(device, L, f.words_x(), f.words_y(), nw, out.data(), out.size()));
+    return out;
 }
 
 // ------------------------------------------------------------------ KMC
@@ -239,10 +247,13 @@ Counters kmc_mcs(Lattice& lat, const Params& params, Rng& rng, int steps = 1, co
 
 // open_bonds_per_particle (kmc.cpp:20-40); throws std::domain_error without B.
 template <class Lattice>
-double open_bonds_per_particle(const Lattice& lat) {
-    KmcDevice d(lat.size(), 1.5, false, 0);
-    d.upload(lat);
-    return d.open_bonds_per_particle();
+double open_bonds_per_particle(const Lattice& lat, int device = 0) {
+    const std::int32_t L = lat.size();
+    const std::size_t nw = (std::size_t(L) * std::size_t(L) * std::size_t(L) + 63) / 64;
+    std::int64_t np = 0, no = 0;
+    check(lfg_kmc_open_bond_sums_host(device, L, lat.words(), nw, &np, &no));
+    if (np == 0) throw std::domain_error("open_bonds_per_particle: no B particles in lattice");
+    return static_cast<double>(no) / static_cast<double>(np);
 }
 
 }  // namespace gpu

@@ -142,6 +142,23 @@ LFG_API int lfg_kpz_synchronize(lfg_kpz* h);
  * interop (torch.distributed halo exchange on the sharded path). */
 LFG_API int lfg_kpz_device_spins(lfg_kpz* h, int32_t replica, void** dev_ptr, size_t* bytes);
 
+/* ---- readouts of host lattices (no handle) ---------------------------------
+ * The reference's free functions on an arbitrary SlopeField, any power-of-two
+ * L >= 4, integrable or not, computed on `device` in the reference's own index
+ * order (words = SlopeField::words_x()/words_y(), nwords = ceil(L*L/64)):
+ *   interface_width(const SlopeField&) (kpz.cpp:62-81): the int64 sums of
+ *     heights integrated along row 0, then up every column (no closure check,
+ *     as the reference); W2 = sum2/n - (sum/n)^2 on the host (kpz.cpp:78-80);
+ *   reconstruct_heights (kpz.cpp:21-49): heights[j*L+i], LFG_ECLOSURE (the
+ *     reference's std::runtime_error) when they would be path-dependent. */
+LFG_API int lfg_kpz_width_sums_host(int32_t device, int32_t L, const uint64_t* x, const uint64_t* y, size_t nwords,
+                                    int64_t* sum, int64_t* sum2);
+/* interface_width(const HeightField&) (kpz.cpp:51-60): int64 sums of n heights. */
+LFG_API int lfg_heights_width_sums_host(int32_t device, const int32_t* heights, size_t n, int64_t* sum,
+                                        int64_t* sum2);
+LFG_API int lfg_kpz_heights_host(int32_t device, int32_t L, const uint64_t* x, const uint64_t* y, size_t nwords,
+                                 int32_t* heights, size_t n);
+
 /* ---- strip-sharded path (multi-GPU) ----------------------
  * The caller (one process per GPU) owns a device ring buffer of
  * `row_capacity` spin rows (power of two; global row y lives at slot
@@ -169,6 +186,13 @@ LFG_API int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t row_capacity, in
 LFG_API int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t block_row_begin,
                                      int32_t block_rows, uint64_t sweep, int32_t phase, void* peer_dn,
                                      int32_t push_row_dn, void* peer_up, int32_t push_row_up);
+/* Abort flag of the strip step barrier (device uint32, or NULL to clear):
+ * pass the err_flag given to lfg_peer_wait.  Once a neighbour has failed to
+ * arrive (the flag is nonzero), this handle's strip phases return without
+ * touching the rows -- no update against stale ghost rows; the caller then
+ * raises the transport error (the lattice is left as of the last completed
+ * phase). */
+LFG_API int lfg_kpz_set_abort_flag(lfg_kpz* h, const void* dev_flag);
 LFG_API int lfg_kpz_strip_fill(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t row_begin, int32_t row_count,
                                int32_t pattern);
 /* W^2 pieces (kpz.cpp:62-81 split by rows): H0 = row-0 heights (int32[L], needs global row 0);

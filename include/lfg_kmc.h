@@ -45,6 +45,12 @@ LFG_API int lfg_kmc_reset_counters(lfg_kmc* h);
 /* open_bonds_per_particle (kmc.cpp:20-40) as exact sums; LFG_EDOMAIN if no B. */
 LFG_API int lfg_kmc_open_bond_sums(lfg_kmc* h, int64_t* particles, int64_t* open_bonds);
 LFG_API int lfg_kmc_open_bonds_per_particle(lfg_kmc* h, double* out);
+/* open_bonds_per_particle (kmc.cpp:20-40) of a host OccupancyLattice (words(),
+ * nwords = ceil(L^3/64), any power-of-two L >= 4) on `device`, no handle:
+ * the exact int64 sums; the caller divides (and raises std::domain_error when
+ * particles == 0, kmc.cpp:36-38). */
+LFG_API int lfg_kmc_open_bond_sums_host(int32_t device, int32_t L, const uint64_t* words, size_t nwords,
+                                        int64_t* particles, int64_t* open_bonds);
 /* count_b (lattice.cpp:97-101). */
 LFG_API int lfg_kmc_count_b(lfg_kmc* h, int64_t* out);
 LFG_API int lfg_kmc_set_params(lfg_kmc* h, double eps, int32_t both_active);
@@ -87,6 +93,9 @@ LFG_API int lfg_kmc_slab_init_random_alloy(lfg_kmc* h, void* planes, int32_t pla
  * z_begin-1 and z_begin+nz must be current). */
 LFG_API int lfg_kmc_slab_open_bond_sums(lfg_kmc* h, const void* planes, int32_t plane_capacity, int32_t z_begin,
                                         int32_t nz, int64_t* particles, int64_t* open_bonds);
+
+/* Abort flag of the slab step barrier (see lfg_kpz_set_abort_flag). */
+LFG_API int lfg_kmc_set_abort_flag(lfg_kmc* h, const void* dev_flag);
 
 #ifdef __cplusplus
 }

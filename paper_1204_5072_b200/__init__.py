@@ -21,7 +21,8 @@ from ._native import (ClosureError, Counters, CudaError, DeviceOutOfMemory, Doma
                       InvalidArgument, KmcPlan, KpzPlan, LfgError, TransportError, check, device_count)
 
 __all__ = ["KpzLattice", "KmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
-           "DomainError", "CudaError", "device_count", "words2", "words3"]
+           "DomainError", "CudaError", "device_count", "words2", "words3", "interface_width",
+           "width_sums", "reconstruct_heights", "open_bond_sums", "open_bonds_per_particle"]
 
 
 def words2(L: int) -> int:
@@ -35,6 +36,48 @@ def words3(L: int) -> int:
 def _u64(a) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.uint64)
     return a
+
+
+# ---------------------------------------------------------------- host-lattice readouts
+# The reference's free functions on host words (any power-of-two L >= 4,
+# integrable or not), computed on the device (include/lfg.h "readouts of host
+# lattices"; kpz.cpp:21-81, kmc.cpp:20-40).
+def width_sums(L: int, x, y, device: int = 0):
+    """interface_width's exact int64 (sum h, sum h^2) of a host SlopeField."""
+    x, y = _u64(x), _u64(y)
+    s, s2 = C.c_int64(), C.c_int64()
+    check(_native.lib().lfg_kpz_width_sums_host(device, L, x.ctypes.data, y.ctypes.data, x.size, C.byref(s),
+                                                C.byref(s2)))
+    return int(s.value), int(s2.value)
+
+
+def interface_width(L: int, x, y, device: int = 0) -> float:
+    s, s2 = width_sums(L, x, y, device)
+    n = float(L * L)  # kpz.cpp:78-80
+    mean = s / n
+    return s2 / n - mean * mean
+
+
+def reconstruct_heights(L: int, x, y, device: int = 0) -> np.ndarray:
+    """reconstruct_heights (kpz.cpp:21-49); ClosureError when path-dependent."""
+    x, y = _u64(x), _u64(y)
+    h = np.empty(L * L, np.int32)
+    check(_native.lib().lfg_kpz_heights_host(device, L, x.ctypes.data, y.ctypes.data, x.size, h.ctypes.data, h.size))
+    return h
+
+
+def open_bond_sums(L: int, words, device: int = 0):
+    w = _u64(words)
+    a, b = C.c_int64(), C.c_int64()
+    check(_native.lib().lfg_kmc_open_bond_sums_host(device, L, w.ctypes.data, w.size, C.byref(a), C.byref(b)))
+    return int(a.value), int(b.value)
+
+
+def open_bonds_per_particle(L: int, words, device: int = 0) -> float:
+    npart, nopen = open_bond_sums(L, words, device)
+    if npart == 0:
+        raise DomainError("open_bonds_per_particle: no B particles in lattice")
+    return nopen / npart
 
 
 class KpzLattice:

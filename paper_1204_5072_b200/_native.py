@@ -139,6 +139,11 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_strip_width_partials", P, P, I32, I32, I32, I32, P, P, P)
     _sig(L, "lfg_kpz_width_combine", P, P, P, P, P, I32, C.POINTER(I64), C.POINTER(I64))
     _sig(L, "lfg_kpz_strip_width_rows", P, P, I32, I32, I32, C.POINTER(I64))
+    _sig(L, "lfg_kpz_set_abort_flag", P, P)
+    # readouts of host lattices (no handle)
+    _sig(L, "lfg_kpz_width_sums_host", I32, I32, P, P, SZ, C.POINTER(I64), C.POINTER(I64))
+    _sig(L, "lfg_kpz_heights_host", I32, I32, P, P, SZ, P, SZ)
+    _sig(L, "lfg_heights_width_sums_host", I32, P, SZ, C.POINTER(I64), C.POINTER(I64))
     _bind_kmc(L)
     _lib = L
     return L
@@ -161,6 +166,7 @@ def _bind_kmc(L) -> None:
     _sig(L, "lfg_kmc_reset_counters", P)
     _sig(L, "lfg_kmc_open_bond_sums", P, C.POINTER(I64), C.POINTER(I64))
     _sig(L, "lfg_kmc_open_bonds_per_particle", P, C.POINTER(D))
+    _sig(L, "lfg_kmc_open_bond_sums_host", I32, I32, P, SZ, C.POINTER(I64), C.POINTER(I64))
     _sig(L, "lfg_kmc_count_b", P, C.POINTER(I64))
     _sig(L, "lfg_kmc_set_params", P, D, I32)
     _sig(L, "lfg_kmc_set_sweep_index", P, U64)
@@ -168,6 +174,7 @@ def _bind_kmc(L) -> None:
     _sig(L, "lfg_kmc_set_seed", P, U64)
     _sig(L, "lfg_kmc_set_stream", P, P)
     _sig(L, "lfg_kmc_set_concurrency", P, I32)
+    _sig(L, "lfg_kmc_set_abort_flag", P, P)
     _sig(L, "lfg_kmc_synchronize", P)
     _sig(L, "lfg_kmc_device_words", P, C.POINTER(P), C.POINTER(SZ))
     # z-slab sharded path

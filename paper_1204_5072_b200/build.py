@@ -35,7 +35,7 @@ def sources() -> list[str]:
 
 def _inputs() -> list[str]:
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [
-        os.path.join(ROOT, "include", "lfg.h"), os.path.abspath(__file__)]
+        os.path.join(ROOT, "include", "lfg.h"), os.path.join(ROOT, "include", "lfg_kmc.h"), os.path.abspath(__file__)]
 
 
 def up_to_date() -> bool:

@@ -29,6 +29,7 @@ struct lfg_kmc {
     unsigned long long* dtmp = nullptr; // [2] reductions
     unsigned long long* hpin = nullptr; // pinned [2]
     int64_t attempts = 0;
+    const uint32_t* abort_flag = nullptr;  // slab step-barrier abort flag (lfg_kmc_set_abort_flag)
     uint64_t thr[13] = {};
     bool slab_only = false;             // created by lfg_kmc_create_slab: no resident lattice
     int32_t share = 1;                  // lfg_kmc_set_concurrency
@@ -83,6 +84,7 @@ KmcPhaseArgs base_args(const lfg_kmc* h) {
     a.bz0 = 0;
     a.nbz = h->L / h->bk;
     a.share = h->share;
+    a.abort_flag = h->abort_flag;
     return a;
 }
 
@@ -467,6 +469,13 @@ int lfg_kmc_device_words(lfg_kmc* h, void** ptr, size_t* bytes) {
         check_resident(h);
         *ptr = h->w;
         *bytes = h->nwords() * 4;
+    });
+}
+
+int lfg_kmc_set_abort_flag(lfg_kmc* h, const void* dev_flag) {
+    return guarded([&] {
+        check_handle(h);
+        h->abort_flag = static_cast<const uint32_t*>(dev_flag);
     });
 }
 

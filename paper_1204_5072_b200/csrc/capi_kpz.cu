@@ -63,6 +63,7 @@ struct lfg_kpz {
     // (the octahedron move preserves every row and column sum).
     unsigned long long* dbad = nullptr;     // [R]
     unsigned long long* dglob = nullptr;    // upload scratch: global-closure violations
+    const uint32_t* abort_flag = nullptr;   // strip step-barrier abort flag (lfg_kpz_set_abort_flag)
 
     size_t words_per_replica() const { return size_t(L) * size_t(L / 32); }
     uint32_t* rep(int r) const { return f + size_t(r) * words_per_replica(); }
@@ -122,12 +123,13 @@ void ensure_width_scratch(lfg_kpz* h) {
 
 void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel execution"); }
 
-// interface_width sums of replica r into out3 (device): [0] sum h, [1] sum h^2
-// (row-order scan, kpz_width.cu), [2] scratch.
+// interface_width sums of replica r into out3 (device): [0] sum h, [1] sum h^2,
+// [2] = 0 (row-order scan, kpz_width.cu; the ABI's out3[1] + out3[2] = sum h^2).
 void enqueue_width(lfg_kpz* h, int32_t r, unsigned long long* out3) {
     ensure_width_scratch(h);
     cuda_check(cudaMemsetAsync(out3, 0, 24, h->stream), "memset");
     cuda_check(kpz_launch_width_rows(h->rep(r), h->L, h->L - 1, 0, h->L, h->H0, out3, h->stream), "width scan");
+    cuda_check(cudaMemsetAsync(out3 + 2, 0, 8, h->stream), "memset");
 }
 
 // LFG_KPZ_SWEEP_KERNEL=1 runs each sweep as one persistent whole-sweep launch
@@ -536,7 +538,7 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         *sum = int64_t(h->hpin[0]);
-        *sum2 = int64_t(h->hpin[1]);
+        *sum2 = int64_t(h->hpin[1] + h->hpin[2]);
     });
 }
 
@@ -750,8 +752,16 @@ int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0,
         a.peer_up = static_cast<uint32_t*>(peer_up);
         a.push_row_dn = peer_dn ? push_row_dn : -1;
         a.push_row_up = peer_up ? push_row_up : -1;
+        a.abort_flag = h->abort_flag;
         cuda_check(kpz_launch_phase(a, h->seeds.data(), 1, h->stream), "kpz_dtr_phase launch");
         h->attempts[0] += int64_t(nbrow) * h->by * h->L / 4;
+    });
+}
+
+int lfg_kpz_set_abort_flag(lfg_kpz* h, const void* dev_flag) {
+    return guarded([&] {
+        check_handle(h);
+        h->abort_flag = static_cast<const uint32_t*>(dev_flag);
     });
 }
 

@@ -88,6 +88,7 @@ __device__ __forceinline__ void fcc_offset(int dir, int& dx, int& dy, int& dz) {
 // partner, 2 x 8 neighbour rows) is issued before the first use.
 template <bool BOTH, bool WARP_SYNC>
 __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     extern __shared__ __align__(16) unsigned long long smk[];
     __shared__ unsigned long long s_thr[13];
     const int L = a.L, Lm = L - 1, bk = a.bk, E = bk + 4, rows = E * E;
@@ -235,6 +236,7 @@ __device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, 
 
 template <bool BOTH>
 __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     extern __shared__ __align__(16) uint32_t sk16[];
     __shared__ unsigned long long s_thr[13];
     const int L = a.L, Lm = L - 1, t = int(threadIdx.x) & 7, sub = int(threadIdx.x) >> 3;
@@ -335,6 +337,7 @@ __device__ __forceinline__ int k16_count_at(const uint32_t (&f)[4], const uint32
 
 template <bool BOTH>
 __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     extern __shared__ __align__(16) uint32_t sk16[];
     const int L = a.L, Lm = L - 1, lane = int(threadIdx.x), t = lane & 7, j = lane >> 3;
     uint32_t* const cur = sk16;

@@ -20,6 +20,7 @@ struct KmcPhaseArgs {
     int32_t zmask;                 // buffer plane slot = global z & zmask (L-1: whole lattice)
     int32_t bz0, nbz;              // block z-rows [bz0, bz0 + nbz) of the shifted frame (slabs)
     int32_t share;                 // lattices sharing the GPU at once (kernel choice; >= 1)
+    const uint32_t* abort_flag;    // slab step-barrier abort flag (see KpzPhaseArgs), or nullptr
 };
 
 int kmc_blocks_per_cta(int bk);

@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(MW ? (kNT == 2 && LFG_KPZ_MAXBY >= 256 ? 256 :
                                   MW ? (kNT == 1 || (kNT == 2 && LFG_KPZ_MAXBY >= 256) ? 3 : 6) : 12)
     kpz_dtr_phase_kernel(const __grid_constant__ KpzPhaseArgs a) {
     extern __shared__ __align__(16) uint32_t sm_raw[];
+    if (!CHAIN && a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
     const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;  // shared address of line 0
     uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);  // generic pointer to line 0 (lines < 6 unused)

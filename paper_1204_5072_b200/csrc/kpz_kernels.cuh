@@ -31,6 +31,11 @@ struct KpzPhaseArgs {
     // Fused peer push (strip shards over NVLink): blocks writing global row
     // push_row_dn / push_row_up also store it into the lower / upper
     // neighbour's ring buffer (same capacity; peer pointer from CUDA IPC).
+    // Abort flag of the strip step barrier (device memory, or nullptr): when a
+    // neighbour never arrived (peer_wait_kernel timed out and set it), the
+    // phase kernels of this handle return without touching the lattice instead
+    // of updating it against stale ghost rows.
+    const uint32_t* abort_flag;
     uint32_t* peer_dn;
     uint32_t* peer_up;
     int32_t push_row_dn, push_row_up;  // -1: none

@@ -160,6 +160,9 @@ class CudaStripEngine:
     def sync(self):
         self.stream.synchronize()
 
+    def set_abort_flag(self, ptr: int):
+        _native.check(_native.lib().lfg_kpz_set_abort_flag(self.h, C.c_void_p(ptr) if ptr else None))
+
     def fill(self, row_begin: int, count: int, pattern: int):
         _native.check(_native.lib().lfg_kpz_strip_fill(self.h, C.c_void_p(self.buf.data_ptr()), self.plan.cap,
                                                        row_begin, count, pattern))
@@ -307,6 +310,9 @@ class PeerComm(DistComm):
         self.max_spins = int(max_spins)
         torch.cuda.current_stream(e.buf.device).synchronize()  # zero fills done before peers see the flags
         e.sync()
+        # a neighbour that never arrives sets err (peer_wait); the engine's phase
+        # kernels then skip instead of updating against stale ghost rows
+        e.set_abort_flag(self.err.data_ptr())
         mine = []
         for t in (e.buf, self.flags):
             hd, off = (C.c_char * 64)(), C.c_uint64()
@@ -327,6 +333,8 @@ class PeerComm(DistComm):
         self.epoch = 0
 
     def close(self):
+        if getattr(self.engine, "h", None) is not None:
+            self.engine.set_abort_flag(0)  # self.err goes away with this object
         for p in self._bases:
             self.lib.lfg_ipc_close(C.c_void_p(p), self.device)
         self._opened, self._bases = {}, []
@@ -662,6 +670,9 @@ class CudaSlabEngine:
 
     def sync(self):
         self.stream.synchronize()
+
+    def set_abort_flag(self, ptr: int):
+        _native.check(_native.lib().lfg_kmc_set_abort_flag(self.h, C.c_void_p(ptr) if ptr else None))
 
     def init_random_alloy(self, z_begin: int, count: int, c: float, seed: int):
         _native.check(_native.lib().lfg_kmc_slab_init_random_alloy(

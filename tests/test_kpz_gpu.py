@@ -377,3 +377,70 @@ def test_bench_size_properties(lfg, oracle):
     assert np.array_equal(row_ones(x), row_ones(x0))  # sigma_x row sums
     assert np.array_equal(col_ones(y), col_ones(y0))  # sigma_y column sums
     assert oracle.closure_holds(L, x, y)
+
+
+@pytest.mark.parametrize("L", [4, 8, 16, 32, 64, 256])
+def test_host_readouts_any_field(lfg, reflib, L):
+    """interface_width / reconstruct_heights of host SlopeFields through the
+    handle-free device readouts: every power-of-two L >= 4 and fields that are
+    not integrable (random bits), against the unmodified reference."""
+    rs = np.random.RandomState(L)
+    nw = (L * L + 63) // 64
+    for trial in range(3):
+        if trial == 0:
+            x, y = reflib.make_flat(L)
+            for _ in range(2):
+                reflib.kpz_sweep_sequential(L, x, y, 0.9, 0.1, "lcg64", 5 + L, 1)
+        else:
+            x = rs.randint(0, 2**63, size=nw, dtype=np.int64).view(np.uint64)
+            y = rs.randint(0, 2**63, size=nw, dtype=np.int64).view(np.uint64)
+            if L * L < 64:
+                x &= np.uint64((1 << (L * L)) - 1)
+                y &= np.uint64((1 << (L * L)) - 1)
+        assert lfg.interface_width(L, x, y) == reflib.interface_width(L, x, y)
+        try:
+            ref_h = reflib.reconstruct_heights(L, x, y)
+        except Exception:
+            ref_h = None
+        if ref_h is None:
+            with pytest.raises(lfg.ClosureError):
+                lfg.reconstruct_heights(L, x, y)
+        else:
+            assert np.array_equal(lfg.reconstruct_heights(L, x, y), ref_h)
+
+
+def test_heights_readout_refuses_unclosed_state(lfg, reflib):
+    """The device's default state (all slopes -1, SlopeField(L)) is swept like the
+    reference but is not integrable: lfg_kpz_heights raises like
+    reconstruct_heights (kpz.cpp:42-44); after make_flat_slopes it succeeds."""
+    L = 64
+    with lfg.KpzLattice(L) as k:
+        with pytest.raises(lfg.ClosureError):
+            k.reconstruct_heights()
+        x, y = k.download()
+        assert k.interface_width() == reflib.interface_width(L, x, y)
+        k.make_flat_slopes()
+        k.sweep(2)
+        x, y = k.download()
+        assert np.array_equal(k.reconstruct_heights(), reflib.reconstruct_heights(L, x, y))
+
+
+def test_upload_rejects_unclosed_plaquettes(lfg, oracle):
+    """Negating the four slopes around a site that is not a local extremum is a
+    single spin flip -- the spin re-derivation check passes -- but the
+    plaquettes around the site no longer close (heights would be
+    path-dependent): the upload is rejected and the state is unchanged."""
+    L = 64
+    x, y = oracle.kpz_flat(L)
+    i, j = 10, 21  # flat state: s_x(i) = +1, s_x(i+1) = -1, s_y(j) = -1, s_y(j+1) = +1
+    for (plane, ii, jj) in ((x, i, j), (x, i + 1, j), (y, i, j), (y, i, j + 1)):
+        idx = jj * L + ii
+        plane[idx >> 6] ^= np.uint64(1 << (idx & 63))
+    assert not oracle.closure_holds(L, x, y)
+    with lfg.KpzLattice(L) as k:
+        k.make_flat_slopes()
+        before = k.download()
+        with pytest.raises(lfg.ClosureError):
+            k.upload(x, y)
+        after = k.download()
+        assert np.array_equal(before[0], after[0]) and np.array_equal(before[1], after[1])
