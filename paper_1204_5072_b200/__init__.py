@@ -59,11 +59,12 @@ def interface_width(L: int, x, y, device: int = 0) -> float:
 
 
 def reconstruct_heights(L: int, x, y, device: int = 0) -> np.ndarray:
-    """reconstruct_heights (kpz.cpp:21-49); ClosureError when path-dependent."""
+    """reconstruct_heights (kpz.cpp:21-49) -> int32 [L, L] indexed [j, i];
+    ClosureError when path-dependent."""
     x, y = _u64(x), _u64(y)
     h = np.empty(L * L, np.int32)
     check(_native.lib().lfg_kpz_heights_host(device, L, x.ctypes.data, y.ctypes.data, x.size, h.ctypes.data, h.size))
-    return h
+    return h.reshape(L, L)
 
 
 def open_bond_sums(L: int, words, device: int = 0):

@@ -125,8 +125,10 @@ void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel exe
 
 // interface_width sums of replica r into out3 (device): [0] sum h, [1] sum h^2,
 // [2] = 0 (row-order scan, kpz_width.cu; the ABI's out3[1] + out3[2] = sum h^2).
+// out3 == nullptr: the handle's own scratch h->wout (allocated here on first use).
 void enqueue_width(lfg_kpz* h, int32_t r, unsigned long long* out3) {
     ensure_width_scratch(h);
+    if (!out3) out3 = h->wout;
     cuda_check(cudaMemsetAsync(out3, 0, 24, h->stream), "memset");
     cuda_check(kpz_launch_width_rows(h->rep(r), h->L, h->L - 1, 0, h->L, h->H0, out3, h->stream), "width scan");
     cuda_check(cudaMemsetAsync(out3 + 2, 0, 8, h->stream), "memset");
@@ -534,7 +536,7 @@ int lfg_kpz_width_sums(lfg_kpz* h, int32_t replica, int64_t* sum, int64_t* sum2)
         check_handle(h);
         check_replica(h, replica);
         DeviceGuard g(h->device);
-        enqueue_width(h, replica, h->wout);
+        enqueue_width(h, replica, nullptr);
         cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);
         *sum = int64_t(h->hpin[0]);
@@ -564,7 +566,7 @@ int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3) {
         check_replica(h, replica);
         if (!out3) throw Error(LFG_EINVAL, "null output");
         DeviceGuard g(h->device);
-        enqueue_width(h, replica, h->wout);
+        enqueue_width(h, replica, nullptr);
         cuda_check(cudaMemcpyAsync(out3, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
     });
 }
