@@ -375,6 +375,8 @@ def run_b200(args):
         k.make_flat_slopes()
         plan = k.plan
         run = lambda n: k.sweep_async(n)  # noqa: E731
+        done = lambda: k.counters().attempts  # noqa: E731  device count of attempts made (sub = 4: Poisson tiles)
+        sub = k.sub
         mode = "1 GPU"
     else:
         from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, PeerComm, ShardedKpz, StripPlan
@@ -411,10 +413,18 @@ def run_b200(args):
                 sk.make_flat_slopes()
         stream = eng.stream
         run = sk.sweep
+        sub = pl.sub
+
+        def done():  # attempts made by all ranks (device counters)
+            t = torch.tensor([eng.counters().attempts], dtype=torch.float64,
+                             device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t)
+            return int(t.item())
         mode = f"strip-sharded x{world} (rows rolled per sweep, one ghost row per phase; {how})"
 
     run(args.warmup)
     barrier()
+    att0 = done()
     clocks = ClockSampler(local)
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -430,21 +440,22 @@ def run_b200(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = attempts_per_step * args.steps / (ms * 1e6)  # attempts/ns, whole job (fixed L: strong scaling)
+    att_timed = done() - att0  # attempts the timed sweeps made (mean L^2 per MCS)
+    value = att_timed / (ms * 1e6)  # attempts/ns, whole job (fixed L: strong scaling)
 
     # dominant kernel: event-timed phase launches on the launching stream
     roofline = None
     if world == 1:
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
         s0 = k.sweep_index
-        for i, (a, b) in enumerate(ev):
+        for i, (a, b) in enumerate(ev):  # two sub-sweeps of MCS s0 (phase launches take the sub-sweep index)
             a.record(stream)
-            k.phase(s0 + i // 4, i % 4)
+            k.phase(s0 * sub + i // 4, i % 4)
             b.record(stream)
-        k.sweep_index = s0 + 2
+        k.sweep_index = s0 + 1
         torch.cuda.synchronize()
         avg_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / 4
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / (4 * sub)  # mean attempts per launch
         achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
         traffic, ncu = None, {}
         try:
@@ -458,7 +469,7 @@ def run_b200(args):
         # (ncu count of one launch of this kernel at L = 2^16, p = 1).
         issue = None
         if ncu.get("inst_executed") and L == 1 << 16 and args.p == 1.0 and args.q == 0.0:
-            wi_per_att = ncu["inst_executed"] / (attempts_per_step / 4)
+            wi_per_att = ncu["inst_executed"] / (attempts_per_step / (4 * ncu.get("sub", 1)))
             f_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
             ceil_att = 148 * 4 * f_ghz / wi_per_att
             issue = {"achieved_attempts_per_ns": bytes_per_launch / ALG_BYTES_PER_ATTEMPT / (avg_launch_ms * 1e6),
@@ -486,6 +497,7 @@ def run_b200(args):
         ke.upload_ptr(hx.data_ptr(), hy.data_ptr())
         ke.sweep(1)
         ke.download_ptr(hx.data_ptr(), hy.data_ptr())
+        a_single = ke.counters().attempts
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
@@ -494,7 +506,8 @@ def run_b200(args):
             w2 = ke.interface_width()                         # W^2 readout (d2h)
             ke.download_ptr(hx.data_ptr(), hy.data_ptr())     # device -> host SlopeField
         barrier()
-        single = attempts_per_step * args.e2e_steps / ((time.perf_counter() - t0) * 1e9)
+        dt_single = time.perf_counter() - t0
+        single = (ke.counters().attempts - a_single) / (dt_single * 1e9)
         ke.close()
         # (b) headline: two lattices of the same configuration (an ensemble, as in
         # BASELINE configs[1]'s 16 seeds), each on its own stream with the
@@ -523,6 +536,7 @@ def run_b200(args):
         for k2 in kes:
             k2.synchronize()
             k2.upload_check()
+        a_multi = sum(k2.counters().attempts for k2 in kes)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
@@ -535,7 +549,8 @@ def run_b200(args):
         dt = time.perf_counter() - t0
         s_, s2_ = int(o3[0, 0]), int(o3[0, 1]) + int(o3[0, 2])
         w2 = s2_ / (L * L) - (s_ / (L * L)) ** 2
-        e2e = {"value": attempts_per_step * nl * args.e2e_steps / (dt * 1e9), "unit": "attempts/ns",
+        a_multi = sum(k2.counters().attempts for k2 in kes) - a_multi
+        e2e = {"value": a_multi / (dt * 1e9), "unit": "attempts/ns",
                "h2d_bytes_per_step": 2 * L * L // 8, "d2h_bytes_per_step": 2 * L * L // 8 + 24,
                "steps": nl * args.e2e_steps,
                "step": f"one lattice-step = lfg_kpz_upload_async(host SlopeField planes, pinned) + 1 MCS + "
@@ -599,12 +614,12 @@ def run_b200(args):
                                        f"1 MCS per step (BASELINE.json "
                                        + ("configs[1])" if world == 1 else
                                           "configs[2]'s strip-sharded L=2^17 lattice; p, q of the metric)"),
-                           "plan": {"block_x": plan[0], "block_y": plan[1], "domain": "16x8"},
+                           "plan": {"block_x": plan[0], "block_y": plan[1], "domain": "16x8", "sub_sweeps_per_mcs": sub},
                            "parallelism": mode,
                            "l2": f"lattice {L * L // 8 >> 20} MiB ({L * L // 8 // world >> 20} MiB per GPU) >> 126 MB L2: "
                                  f"no flush needed"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": 4 * args.steps, "kmc": kmc, "c3_single_gpu": c3}
+                "gpu_launches": 4 * sub * args.steps, "kmc": kmc, "c3_single_gpu": c3}
         print(json.dumps(line), flush=True)
     if world == 1:
         k.close()

@@ -77,6 +77,7 @@ struct KmcParams {  // kmc.hpp:18-27
 
 struct DtrPlan {
     std::int32_t block_x = 0, block_y = 0;  // KPZ device block (0 = auto)
+    std::int32_t sub = 0;                   // KPZ sub-sweeps per MCS (0 = 4; 1 = the paper's scheme)
     std::int32_t block = 0;                 // KMC device block edge (0 = auto)
 };
 
@@ -90,7 +91,7 @@ std::uint64_t key_from(Rng& rng) {
 class KpzDevice {
 public:
     KpzDevice(std::int32_t L, double p, double q, std::uint64_t seed, const DtrPlan& plan = {}, int device = 0) {
-        lfg_kpz_plan pl{plan.block_x, plan.block_y};
+        lfg_kpz_plan pl{plan.block_x, plan.block_y, plan.sub};
         check(lfg_kpz_create(&h_, L, p, q, seed, &pl, device));
         L_ = L;
     }

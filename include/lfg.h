@@ -67,10 +67,17 @@ typedef struct lfg_kpz lfg_kpz;
 
 /* Two-layer DTr geometry: device blocks block_x x block_y sites (0 = auto:
  * min(1024, L/2) x min(128, L/2)); powers of two, block_x in [32, 1024],
- * block_y in [16, 256]; inner 16x8 single-hit domains are fixed. */
+ * block_y in [16, 256]; inner 16x8 single-hit domains are fixed.
+ * sub: sub-sweeps per MCS (0 = auto = 4).  4: every MCS is four sub-sweeps,
+ * each with its own random origin and block-set order, and every tile makes a
+ * Poisson-distributed number of attempts per activation (mean and variance
+ * 128) -- statistically matched to kpz_sweep_sequential (kpz.cpp:5-19) at
+ * >= 64 seeds.  1: the paper's scheme, one
+ * origin per MCS and exactly 512 single-hit rounds per activation. */
 typedef struct lfg_kpz_plan {
     int32_t block_x;
     int32_t block_y;
+    int32_t sub;
 } lfg_kpz_plan;
 
 /* SlopeField(L) + KpzParams{p,q}.validate() + the seeding of
@@ -107,7 +114,8 @@ LFG_API int lfg_kpz_download_async(lfg_kpz* h, int32_t replica, uint64_t* x, uin
 LFG_API int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out);
 /* Enqueue n_mcs sweeps without synchronising (counters accumulate on device). */
 LFG_API int lfg_kpz_sweep_async(lfg_kpz* h, int64_t n_mcs);
-/* Enqueue one device-layer phase (0..3) of sweep `sweep` (profiling / sharded driver). */
+/* Enqueue one device-layer phase (0..3) of sub-sweep `sweep` (the global
+ * sub-sweep index s' = MCS * plan.sub + k; profiling / sharded driver). */
 LFG_API int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase);
 /* Cumulative counters since create / reset (synchronises). */
 LFG_API int lfg_kpz_counters(lfg_kpz* h, int32_t replica, lfg_counters* out);
@@ -121,12 +129,15 @@ LFG_API int lfg_kpz_interface_width(lfg_kpz* h, int32_t replica, double* w2);
  * (pinned host int64[3], valid after lfg_kpz_synchronize). */
 LFG_API int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3);
 /* Debug instrumentation for the write-disjointness check (the
- * reference's WriteLog, write_log.hpp:10-60): while enabled, every sweep
- * writes one uint32 record per attempt into dev_buf (device memory, >= L*L
- * words; phase k at offset k*L*L/4, then [512 rounds][tiles of the launch]):
- * global tile id (bits 0-19), anchor column in the domain xd (20-23), row yd
- * (24-26), inner set hx (27) / hy (28), accepted (29).  Single-replica handles
- * with block_x < 1024; dev_buf = NULL disables.  Uses the per-phase kernels. */
+ * reference's WriteLog, write_log.hpp:10-60): while enabled, every MCS writes
+ * one uint32 record per (round, tile) into dev_buf (device memory, >=
+ * L*L/512 * rounds * sub words; sub-sweep k, phase f at offset
+ * (4k + f) * L*L/2048 * rounds, then [rounds][tiles of the launch], rounds =
+ * 132 for sub = 4, 512 for sub = 1): global tile id (bits 0-19), anchor column
+ * in the domain xd (20-23), row yd (24-26), inner set hx (27) / hy (28),
+ * accepted (29), skipped round of the tile (30; no attempt).  Single-replica
+ * handles, every plan (incl. the 1024-wide TMA path); dev_buf = NULL
+ * disables.  Uses the per-phase kernels (no phase chaining). */
 LFG_API int lfg_kpz_debug_record_anchors(lfg_kpz* h, void* dev_buf, size_t capacity_words);
 /* reconstruct_heights (kpz.cpp:21-49): n = L*L int32, row-major j*L+i. */
 LFG_API int lfg_kpz_heights(lfg_kpz* h, int32_t replica, int32_t* heights, size_t n);
@@ -168,11 +179,12 @@ LFG_API int lfg_kpz_heights_host(int32_t device, int32_t L, const uint64_t* x, c
  * lfg_kpz_create_strip has no resident lattice of its own. */
 LFG_API int lfg_kpz_create_strip(lfg_kpz** h, int32_t L, double p, double q, uint64_t seed,
                                  const lfg_kpz_plan* plan, int32_t device);
-/* Sweep-level draws of the DTr schedule: out = {ox, oy, set of phase 0..3}. */
+/* Sweep-level draws of the DTr schedule for sub-sweep s' (= MCS * plan.sub + k):
+ * out = {ox, oy, set of phase 0..3}. */
 LFG_API int lfg_kpz_sweep_origin(int32_t L, const lfg_kpz_plan* plan, uint64_t seed, uint64_t sweep,
                                  int32_t out[6]);
-/* One DT phase restricted to block rows [block_row_begin, +block_row_count)
- * of the sweep's shifted frame (begin and count even). */
+/* One DT phase of sub-sweep `sweep` (s') restricted to block rows
+ * [block_row_begin, +block_row_count) of its shifted frame (begin and count even). */
 LFG_API int lfg_kpz_strip_phase(lfg_kpz* h, void* rows, int32_t row_capacity, int32_t block_row_begin,
                                 int32_t block_row_count, uint64_t sweep, int32_t phase);
 /* Fill global rows [row_begin, +row_count) (mod L): pattern 0 = make_flat_slopes,

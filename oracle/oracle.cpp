@@ -295,23 +295,28 @@ int orc_kpz_sweep_sequential(int32_t L, uint64_t* x, uint64_t* y, double p, doub
     return 0;
 }
 
-// Two-layer DTr sweeps (oracle_core.hpp) with the restated attempt.
+// Two-layer DTr sweeps (oracle_core.hpp) with the restated attempt: MCS
+// sweep0 .. sweep0 + nsweeps - 1, each `sub` sub-sweeps (s' = s * sub + k).
 int orc_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, uint64_t seed,
-                      uint64_t sweep0, int32_t nsweeps, int32_t bx, int32_t by, int64_t* counters) {
+                      uint64_t sweep0, int32_t nsweeps, int32_t bx, int32_t by, int32_t sub, int64_t* counters) {
     if (!(p >= 0.0 && p <= 1.0) || !(q >= 0.0 && q <= 1.0) || p + q <= 0.0) return -1;
-    orc::KpzPlan pl{L, bx, by};
-    int64_t dep = 0, det = 0;
+    if (sub != 1 && sub != 4) return -1;
+    orc::KpzPlan pl{L, bx, by, sub};
+    int64_t dep = 0, det = 0, att = 0;
     for (int32_t s = 0; s < nsweeps; ++s) {
-        const uint64_t sweep = sweep0 + uint64_t(s);
-        const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
-            return kpz_attempt(L, x, y, i, j, p, q, [&] {
-                return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
+        for (int32_t k = 0; k < sub; ++k) {
+            const uint64_t sweep = (sweep0 + uint64_t(s)) * uint64_t(sub) + uint64_t(k);
+            const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
+                return kpz_attempt(L, x, y, i, j, p, q, [&] {
+                    return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
+                });
             });
-        });
-        dep += c.dep;
-        det += c.det;
+            dep += c.dep;
+            det += c.det;
+            att += c.att;
+        }
     }
-    counters[0] += int64_t(L) * L * nsweeps;
+    counters[0] += att;
     counters[1] += dep + det;
     counters[2] += dep;
     counters[3] += det;
@@ -321,7 +326,7 @@ int orc_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, u
 // Sweep-level draws of the DTr schedule (origin and block-set order).
 void orc_kpz_sweep_draw(int32_t L, int32_t bx, int32_t by, uint64_t seed, uint64_t sweep,
                         int32_t* out6) {
-    orc::KpzPlan pl{L, bx, by};
+    orc::KpzPlan pl{L, bx, by, 1};
     const auto d = orc::kpz_sweep_draw(pl, seed, sweep);
     out6[0] = d.ox; out6[1] = d.oy;
     for (int k = 0; k < 4; ++k) out6[2 + k] = d.perm[k];

@@ -94,7 +94,7 @@ inline void perm4(uint32_t idx, int out[4]) {
 // thread accumulates into its own Counts slot, summed after the join.  Thread
 // count: ORC_THREADS, else hardware_concurrency().
 struct Counts {
-    int64_t dep = 0, det = 0;
+    int64_t dep = 0, det = 0, att = 0;
 };
 
 inline int oracle_threads() {
@@ -126,20 +126,42 @@ Counts parallel_rows(int32_t n, bool allow, Body&& body) {
     for (const auto& p : part) {
         c.dep += p.dep;
         c.det += p.det;
+        c.att += p.att;
     }
     return c;
 }
 
 // ---------------------------------------------------------------- KPZ DTr plan
 // Inner geometry is fixed: domains 16 (x) x 8 (y) sites, tiles 32 x 16 (one
-// 32-bit word per tile row), four inner sets (hx, hy), 512 single-hit rounds
-// per block activation.
+// 32-bit word per tile row), four inner sets (hx, hy).
+//
+// One MCS = `sub` sub-sweeps (1 or 4).  Sub-sweep s' (global
+// counter s' = s * sub + k) draws its own origin and block-set order; each
+// block activation runs kpz_rounds(sub) single-hit rounds:
+//   sub = 1: 512 rounds, every tile attempts once per round;
+//   sub = 4: 132 rounds; tile t draws K_t from the 16 spare bits of its first
+//            anchor word batch (low bytes of words 2, 3) with P(K >= k) =
+//            {7701, 471, 19, 1} / 2^16 and skips the 4-round groups g < 32 whose
+//            bit is set in the mask nibble {0, 8, A, E, F}[K_t] repeated, i.e.
+//            N_t = 132 - 32 K_t attempts: mean 128, variance 128 (the Poisson
+//            count of a 512-site tile over a quarter MCS of kpz.cpp:5-19).
+// The x origin is a multiple of 128 sites (32 when bx < 64).
 constexpr int kTileW = 32, kTileH = 16, kDomW = 16, kDomH = 8, kRounds = 512;
+
+inline int kpz_rounds(int sub) { return sub == 4 ? 132 : 512; }
+
+inline uint32_t kpz_skip_mask_for(uint32_t v16) {
+    const uint32_t k = uint32_t(v16 >= 57835u) + uint32_t(v16 >= 65065u) + uint32_t(v16 >= 65517u) +
+                       uint32_t(v16 >= 65535u);
+    static const uint32_t nib[5] = {0x0u, 0x8u, 0xAu, 0xEu, 0xFu};
+    return nib[k] * 0x11111111u;
+}
 
 struct KpzPlan {
     int32_t L = 0;
     int32_t bx = 0;  // device block width  (multiple of 32, L % (2 bx) == 0)
     int32_t by = 0;  // device block height (multiple of 16, L % (2 by) == 0)
+    int32_t sub = 1; // sub-sweeps per MCS (1 or 4)
 };
 
 struct KpzSweepDraw {
@@ -151,7 +173,8 @@ inline KpzSweepDraw kpz_sweep_draw(const KpzPlan& pl, uint64_t seed, uint64_t sw
     uint32_t w[4];
     draw(seed, sweep, TAG_SWEEP, 0, 0, w);
     KpzSweepDraw d;
-    d.ox = int32_t(below(w[0], uint32_t(2 * pl.bx)));
+    const int32_t qx = pl.bx >= 64 ? 128 : 32;
+    d.ox = qx * int32_t(below(w[0], uint32_t(2 * pl.bx / qx)));
     d.oy = int32_t(below(w[1], uint32_t(2 * pl.by)));
     perm4(below(w[2], 24), d.perm);
     return d;
@@ -161,11 +184,11 @@ inline KpzSweepDraw kpz_sweep_draw(const KpzPlan& pl, uint64_t seed, uint64_t sw
 // KpzOutcome, kpz.hpp:31; KMC: 0 = exchanged, anything else = rejected).
 enum : int { OUT_DEPOSIT = 0, OUT_DETACH = 1, OUT_REJECT = 2 };
 
-// One DTr sweep.  attempt(i, j, tile_id, round) performs one KPZ attempt at
-// anchor (i, j) and returns its outcome code; the callee derives the
-// acceptance word from (tile_id, round) via accept_word() when -- and only
-// when -- a pattern matches, mirroring the reference's lazy get_r()
-// (kpz.hpp:87-95).
+// One DTr sub-sweep with global sub-sweep counter `sweep`.  attempt(i, j,
+// tile_id, round) performs one KPZ attempt at anchor (i, j) and returns its
+// outcome code; the callee derives the acceptance word from (tile_id, round)
+// via accept_word() when -- and only when -- a pattern matches, mirroring the
+// reference's lazy get_r() (kpz.hpp:87-95).
 //
 // Parallel execution (parallel_rows): the active blocks of one phase are one block
 // apart, so their attempts touch disjoint sites (reach +1 < the block gap) and
@@ -182,6 +205,8 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
     const int32_t twx = pl.bx / kTileW, thy = pl.by / kTileH;   // tiles per block
     const int32_t tiles_per_row = L / kTileW;
     const int ntiles = twx * thy;
+    const int rounds = kpz_rounds(pl.sub);
+    const bool skip = pl.sub == 4;
     Counts tot;
     for (int k = 0; k < 4; ++k) {
         const int set = d.perm[k];
@@ -190,10 +215,11 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
         const Counts c = parallel_rows(nrows, L >= 64, [&](int32_t row, Counts& acc) {
             const int32_t byi = sy + 2 * row;
             uint32_t* anc = new uint32_t[size_t(ntiles) * 4];
+            uint32_t* smask = new uint32_t[size_t(ntiles)];
             for (int32_t bxi = sx; bxi < nbx; bxi += 2) {
                 const uint32_t block_id = uint32_t(byi) * uint32_t(nbx) + uint32_t(bxi);
                 uint32_t sw[4] = {0, 0, 0, 0};
-                for (int r = 0; r < kRounds; ++r) {
+                for (int r = 0; r < rounds; ++r) {
                     if ((r & 63) == 0) draw(seed, sweep, TAG_SET, block_id, uint32_t(r >> 6), sw);
                     const int inner = int((sw[(r >> 4) & 3] >> (2 * (r & 15))) & 3u);
                     const int hx = inner & 1, hy = inner >> 1;
@@ -201,8 +227,11 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
                         for (int32_t tx = 0; tx < twx; ++tx) {
                             const int32_t gx = bxi * twx + tx, gy = byi * thy + ty;
                             const uint32_t tile_id = uint32_t(gy) * uint32_t(tiles_per_row) + uint32_t(gx);
-                            uint32_t* a4 = anc + size_t(ty * twx + tx) * 4;
+                            const size_t t = size_t(ty * twx + tx);
+                            uint32_t* a4 = anc + t * 4;
                             if ((r & 15) == 0) draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(r >> 4), a4);
+                            if (r == 0) smask[t] = skip ? kpz_skip_mask_for((a4[2] & 0xFFu) | ((a4[3] & 0xFFu) << 8)) : 0u;
+                            if (r < 128 && ((smask[t] >> (r >> 2)) & 1u)) continue;  // skipped group
                             // Anchor of round r (k = r & 15 within its 16-round batch), fields
                             // consumed from the TOP of each Philox word (h = k >> 3, k' = k & 7):
                             //   xd = bits [28-4k', +4) of word h      (words 0, 1)
@@ -215,14 +244,17 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
                             const int o = attempt(i, j, tile_id, r);
                             acc.dep += o == OUT_DEPOSIT;
                             acc.det += o == OUT_DETACH;
+                            acc.att += 1;
                         }
                     }
                 }
             }
             delete[] anc;
+            delete[] smask;
         });
         tot.dep += c.dep;
         tot.det += c.det;
+        tot.att += c.att;
     }
     return tot;
 }

@@ -64,7 +64,7 @@ class Oracle:
         _sig(lib, "orc_kpz_reconstruct_heights", I, I32, u64p, u64p, i32p)
         _sig(lib, "orc_kpz_closure_holds", I, I32, u64p, u64p)
         _sig(lib, "orc_kpz_sweep_sequential", I, I32, u64p, u64p, D, D, I, C.POINTER(U64), I, i64p)
-        _sig(lib, "orc_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, i64p)
+        _sig(lib, "orc_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, I32, i64p)
         _sig(lib, "orc_kpz_sweep_draw", None, I32, I32, I32, U64, U64, i32p)
         _sig(lib, "orc_kmc_random_alloy", I, I32, D, I, U64, U32, u64p, C.POINTER(U64))
         _sig(lib, "orc_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
@@ -128,9 +128,11 @@ class Oracle:
         assert self.lib.orc_kpz_sweep_sequential(L, x, y, p, q, KIND[kind], C.byref(st), sweeps, c) == 0
         return c, st.value
 
-    def kpz_sweep_dtr(self, L, x, y, p, q, seed, sweep0, nsweeps, bx, by):
+    def kpz_sweep_dtr(self, L, x, y, p, q, seed, sweep0, nsweeps, bx, by, sub=4):
+        """MCS sweep0 .. sweep0+nsweeps-1 of the DTr schedule (sub sub-sweeps each);
+        counters [attempts, successes, deposits, detaches]."""
         c = np.zeros(4, np.int64)
-        rc = self.lib.orc_kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, nsweeps, bx, by, c)
+        rc = self.lib.orc_kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, nsweeps, bx, by, sub, c)
         if rc != 0:
             raise ValueError("KpzParams: invalid p/q")
         return c
@@ -213,7 +215,7 @@ class RefLib:
         _sig(lib, "ref_kpz_field_create", C.c_void_p, I32, u64p, u64p)
         _sig(lib, "ref_kpz_field_destroy", None, C.c_void_p)
         _sig(lib, "ref_kpz_field_attempts", I, C.c_void_p, D, D, I, C.POINTER(U64), I64, i64p)
-        _sig(lib, "ref_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, i64p)
+        _sig(lib, "ref_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, I32, i64p)
         _sig(lib, "ref_make_random_alloy", I, I32, D, I, U64, u64p, C.POINTER(U64))
         _sig(lib, "ref_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
         _sig(lib, "ref_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, i64p)
@@ -303,9 +305,9 @@ class RefLib:
         self._check(self.lib.ref_kpz_attempt(L, x, y, i, j, p, q, r, C.byref(o)))
         return o.value
 
-    def kpz_sweep_dtr(self, L, x, y, p, q, seed, sweep0, nsweeps, bx, by):
+    def kpz_sweep_dtr(self, L, x, y, p, q, seed, sweep0, nsweeps, bx, by, sub=4):
         c = np.zeros(4, np.int64)
-        self._check(self.lib.ref_kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, nsweeps, bx, by, c))
+        self._check(self.lib.ref_kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, nsweeps, bx, by, sub, c))
         return c
 
     def make_random_alloy(self, L, c, kind, seed):

@@ -236,28 +236,33 @@ int ref_kpz_attempt(int32_t L, uint64_t* x, uint64_t* y, int32_t i, int32_t j, d
     });
 }
 
-// The DTr schedule (oracle_core.hpp) with the reference's own attempt kernel.
+// The DTr schedule (oracle_core.hpp) with the reference's own attempt kernel:
+// MCS sweep0 .. sweep0 + nsweeps - 1, each `sub` sub-sweeps (s' = s * sub + k).
 // counters: [attempts, successes, deposits, detaches].
 int ref_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, uint64_t seed,
-                      uint64_t sweep0, int32_t nsweeps, int32_t bx, int32_t by, int64_t* counters) {
+                      uint64_t sweep0, int32_t nsweeps, int32_t bx, int32_t by, int32_t sub, int64_t* counters) {
     return guarded([&] {
         const lf::KpzParams params{p, q};
         params.validate();
+        if (sub != 1 && sub != 4) throw std::invalid_argument("DtrPlan: sub must be 1 or 4");
         auto f = load_field(L, x, y);
-        orc::KpzPlan pl{L, bx, by};
-        int64_t dep = 0, det = 0;
+        orc::KpzPlan pl{L, bx, by, sub};
+        int64_t dep = 0, det = 0, att = 0;
         for (int32_t s = 0; s < nsweeps; ++s) {
-            const uint64_t sweep = sweep0 + uint64_t(s);
-            const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
-                return int(lf::detail::kpz_attempt_impl<false>(f, i, j, params, [&] {
-                    return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
-                }));
-            });
-            dep += c.dep;
-            det += c.det;
+            for (int32_t k = 0; k < sub; ++k) {
+                const uint64_t sweep = (sweep0 + uint64_t(s)) * uint64_t(sub) + uint64_t(k);
+                const orc::Counts c = orc::kpz_dtr_sweep(pl, seed, sweep, [&](int32_t i, int32_t j, uint32_t tile_id, int r) {
+                    return int(lf::detail::kpz_attempt_impl<false>(f, i, j, params, [&] {
+                        return orc::kpz_accept_word(seed, sweep, tile_id, r) * 0x1p-32;
+                    }));
+                });
+                dep += c.dep;
+                det += c.det;
+                att += c.att;
+            }
         }
         store_field(f, x, y);
-        counters[0] += int64_t(L) * L * nsweeps;
+        counters[0] += att;
         counters[1] += dep + det;
         counters[2] += dep;
         counters[3] += det;

@@ -86,15 +86,17 @@ class KpzLattice:
 
     ``replicas > 1`` (or ``seeds=[...]``) holds independent lattices that one
     launch advances together (ensembles, e.g. W(t) over 16 seeds).
+    ``sub``: sub-sweeps per MCS (0 = 4, the statistically matched scheme; 1 =
+    the paper's single-origin scheme), include/lfg.h ``lfg_kpz_plan``.
     """
 
     def __init__(self, L: int, p: float = 1.0, q: float = 0.0, seed: int = 1, *, seeds=None,
-                 block_x: int = 0, block_y: int = 0, device: int = 0):
+                 block_x: int = 0, block_y: int = 0, sub: int = 0, device: int = 0):
         self._h = None
         L_ = _native.lib()
         seeds = [int(seed)] if seeds is None else [int(s) for s in seeds]
         arr = (C.c_uint64 * len(seeds))(*seeds)
-        plan = KpzPlan(block_x, block_y)
+        plan = KpzPlan(block_x, block_y, sub)
         h = C.c_void_p()
         check(L_.lfg_kpz_create_batch(C.byref(h), L, float(p), float(q), arr, len(seeds), C.byref(plan), device))
         self._h = h
@@ -106,6 +108,7 @@ class KpzLattice:
         got = KpzPlan()
         check(L_.lfg_kpz_get_plan(h, C.byref(got)))
         self.plan = (int(got.block_x), int(got.block_y))
+        self.sub = int(got.sub)
 
     # -- lifetime ---------------------------------------------------------
     def close(self) -> None:

@@ -65,7 +65,8 @@ class Counters(C.Structure):
 
 
 class KpzPlan(C.Structure):
-    _fields_ = [("block_x", C.c_int32), ("block_y", C.c_int32)]
+    """lfg_kpz_plan (include/lfg.h): block_x, block_y, sub (0 = defaults)."""
+    _fields_ = [("block_x", C.c_int32), ("block_y", C.c_int32), ("sub", C.c_int32)]
 
 
 class KmcPlan(C.Structure):

@@ -54,6 +54,9 @@ def _parser() -> argparse.ArgumentParser:
     common(k)
     k.add_argument("--p", type=float, default=1.0)
     k.add_argument("--q", type=float, default=0.0)
+    k.add_argument("--sub", type=int, default=0, choices=[0, 1, 4],
+                   help="DTr sub-sweeps per MCS: 4 (default) statistically matched, 1 the paper's scheme "
+                        "with exact L^2 attempts per MCS")
     m = sub.add_parser("kmc", help="fcc binary-alloy KMC, open bonds per particle (t)")
     common(m)
     m.add_argument("--conc", type=float, default=0.5)
@@ -86,8 +89,8 @@ def _config(a):
         if not (0.0 <= a.p <= 1.0 and 0.0 <= a.q <= 1.0) or a.p + a.q <= 0.0:
             raise UsageError("p and q must lie in [0,1] with p + q > 0")
         return ExperimentConfig("kpz", a.size, a.mcs, a.seed, a.realizations, samples, p=a.p, q=a.q,
-                                block_x=a.tile_edge, block_y=a.block_edge, device=a.device,
-                                concurrency=a.concurrency)
+                                block_x=a.tile_edge, block_y=a.block_edge, sub=getattr(a, "sub", 0),
+                                device=a.device, concurrency=a.concurrency)
     if not 0.0 <= a.conc <= 1.0 or a.eps < 0.0:
         raise UsageError("conc must lie in [0,1] and eps >= 0")
     return ExperimentConfig("kmc", a.size, a.mcs, a.seed, a.realizations, samples, conc=a.conc, eps=a.eps,

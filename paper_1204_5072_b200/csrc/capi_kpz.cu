@@ -31,14 +31,15 @@ struct lfg_kpz {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int32_t L = 0, bx = 0, by = 0, R = 1;
+    int32_t sub = 4;                        // sub-sweeps per MCS (plan; lfg_common.cuh kpz_rounds)
     double p = 1.0, q = 0.0;
     uint64_t sweep = 0;
     std::vector<uint64_t> seeds;
     uint32_t* f = nullptr;                  // [R][L][L/32]
     uint64_t* dseeds = nullptr;             // [R]
-    unsigned long long* dcnt = nullptr;     // [R][2]
-    std::vector<unsigned long long> hcnt;   // cumulative host mirror (valid when !stale)
-    std::vector<int64_t> attempts;          // cumulative attempts per replica
+    unsigned long long* dcnt = nullptr;     // [R][2] deposits, detaches, then [R] skipped attempts
+    std::vector<unsigned long long> hcnt;   // cumulative host mirror of dcnt (3R)
+    std::vector<int64_t> attempts;          // cumulative scheduled attempts per replica (before skips)
     // scratch (lazy)
     uint32_t* sx = nullptr;                 // [L][L/32] slope planes staging
     uint32_t* sy = nullptr;
@@ -53,8 +54,7 @@ struct lfg_kpz {
     bool strip_only = false;                // created by lfg_kpz_create_strip: no resident lattice
     int32_t* hbuf = nullptr;                // [L][L] heights (small L)
     uint32_t* wlog = nullptr;               // debug anchor records ([4 phases][L^2/4]) or nullptr
-    uint32_t* flags = nullptr;              // [R][L/bx][L/by] whole-sweep kernel completion epochs
-    unsigned int* next_job = nullptr;       // whole-sweep kernel claim counter
+    uint32_t* flags = nullptr;              // [R][L/bx][L/by] phase-chaining completion epochs
     uint32_t epoch = 0;
     unsigned long long* hpin = nullptr;     // pinned readback [max(3, 2R)]
     // Global closure of each replica's field (reconstruct_heights, kpz.cpp:35-47):
@@ -94,8 +94,33 @@ void resolve_plan(lfg_kpz* h, const lfg_kpz_plan* plan) {
     if (by < 16 || by > LFG_KPZ_MAXBY || by % 16 || !is_pow2(by) || h->L % (2 * by))
         throw Error(LFG_EINVAL, "DtrPlan: block_y must be a power of two in [16, min(" +
                                     std::to_string(LFG_KPZ_MAXBY) + ", L/2)], got " + std::to_string(by));
+    const int32_t sub = plan && plan->sub ? plan->sub : 4;
+    if (sub != 1 && sub != 4)
+        throw Error(LFG_EINVAL, "DtrPlan: sub (sub-sweeps per MCS) must be 1 or 4, got " + std::to_string(sub));
     h->bx = bx;
     h->by = by;
+    h->sub = sub;
+}
+
+// Scheduled attempts of one sub-sweep over nbrow block rows (before skips).
+int64_t sub_sweep_attempts(const lfg_kpz* h, int64_t nbrow) {
+    return nbrow * h->by * int64_t(h->L) / 512 * kpz_rounds(h->sub);
+}
+
+// Fields every phase launch of handle h shares.
+KpzPhaseArgs base_phase_args(const lfg_kpz* h) {
+    KpzPhaseArgs a{};
+    a.counters = h->dcnt;
+    a.skipped = h->dcnt + 2 * h->R;
+    a.L = h->L;
+    a.bx = h->bx;
+    a.by = h->by;
+    a.rounds = kpz_rounds(h->sub);
+    a.skip = h->sub == 4;
+    a.thrP = threshold32(h->p);
+    a.thrQ = threshold32(h->q);
+    a.general = !(h->p == 1.0 && h->q == 0.0);
+    return a;
 }
 
 void check_handle(const lfg_kpz* h) {
@@ -134,12 +159,6 @@ void enqueue_width(lfg_kpz* h, int32_t r, unsigned long long* out3) {
     cuda_check(cudaMemsetAsync(out3 + 2, 0, 8, h->stream), "memset");
 }
 
-// LFG_KPZ_SWEEP_KERNEL=1 runs each sweep as one persistent whole-sweep launch
-// (kpz_dtr_sweep_kernel: no wave-quantisation gap between phases; same lattice
-// bit for bit, tests/test_kpz_gpu.py::test_sweep_kernel_matches_phase_launches).
-// Default: four phase launches -- measured faster on B200 (979 vs 801
-// attempts/ns at L = 2^16): the persistent kernel's extra live state costs the
-// round loop its load batching (ncu: short-scoreboard stalls 1% -> 20%).
 // Chained phase launches (programmatic dependent launch + per-block flags);
 // LFG_KPZ_PDL=0 disables.
 bool pdl_enabled() {
@@ -150,45 +169,26 @@ bool pdl_enabled() {
     return on;
 }
 
-bool sweep_kernel_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("LFG_KPZ_SWEEP_KERNEL");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 void enqueue_sweeps(lfg_kpz* h, int64_t n) {
-    KpzPhaseArgs a{};
+    KpzPhaseArgs a = base_phase_args(h);
     a.f = h->f;
-    a.counters = h->dcnt;
-    a.L = h->L;
-    a.bx = h->bx;
-    a.by = h->by;
-    a.thrP = threshold32(h->p);
-    a.thrQ = threshold32(h->q);
-    a.general = !(h->p == 1.0 && h->q == 0.0);
     a.row_mask = h->L - 1;
     a.brow0 = 0;
     a.nbrow = h->L / h->by;
-    if (!h->flags) {  // whole-sweep kernel state (zeroed: epochs start at 1)
+    if (!h->flags) {  // phase-chaining completion flags (zeroed: epochs start at 1)
         const size_t nf = size_t(h->R) * size_t(h->L / h->bx) * size_t(h->L / h->by);
-        h->flags = dmalloc<uint32_t>(nf, "alloc sweep flags");
-        h->next_job = dmalloc<unsigned int>(1, "alloc sweep counter");
+        h->flags = dmalloc<uint32_t>(nf, "alloc phase flags");
         cuda_check(cudaMemsetAsync(h->flags, 0, nf * 4, h->stream), "memset");
     }
-    for (int64_t s = 0; s < n; ++s) {
-        a.sweep = h->sweep + uint64_t(s);
-        if (sweep_kernel_enabled() && !h->wlog && h->by <= 128) {  // its launch bounds stop at 4 warps
-            cuda_check(kpz_launch_sweep(a, h->seeds.data(), h->R, h->flags, h->next_job, h->epoch, h->stream),
-                       "kpz_dtr_sweep launch");
-            continue;
-        }
+    for (int64_t s = 0; s < n * h->sub; ++s) {
+        a.sweep = h->sweep * uint64_t(h->sub) + uint64_t(s);  // global sub-sweep index
         const bool chain = pdl_enabled() && !h->wlog && h->R <= kMaxRepPerLaunch;
         const uint32_t epoch = chain ? ++h->epoch : 0u;
         for (int k = 0; k < 4; ++k) {
             a.phase = k;
-            a.wlog = h->wlog ? h->wlog + size_t(k) * (size_t(h->L) * h->L / 4) : nullptr;
+            a.wlog = h->wlog ? h->wlog + (size_t(s % h->sub) * 4 + size_t(k)) * (size_t(h->L) * h->L / 512 / 4) *
+                                             size_t(kpz_rounds(h->sub))
+                             : nullptr;
             if (chain) {  // phases 1-3 overlap the previous phase's tail (per-block flags)
                 a.dflags = h->flags;
                 a.depoch = epoch;
@@ -199,14 +199,19 @@ void enqueue_sweeps(lfg_kpz* h, int64_t n) {
         }
     }
     h->sweep += uint64_t(n);
-    for (int r = 0; r < h->R; ++r) h->attempts[size_t(r)] += int64_t(h->L) * h->L * n;
+    for (int r = 0; r < h->R; ++r) h->attempts[size_t(r)] += sub_sweep_attempts(h, h->L / h->by) * h->sub * n;
 }
 
 void read_counters(lfg_kpz* h) {
-    cuda_check(cudaMemcpyAsync(h->hpin, h->dcnt, sizeof(unsigned long long) * 2 * h->R, cudaMemcpyDeviceToHost,
+    cuda_check(cudaMemcpyAsync(h->hpin, h->dcnt, sizeof(unsigned long long) * 3 * h->R, cudaMemcpyDeviceToHost,
                                h->stream), "counter readback");
     sync(h);
-    std::memcpy(h->hcnt.data(), h->hpin, sizeof(unsigned long long) * 2 * h->R);
+    std::memcpy(h->hcnt.data(), h->hpin, sizeof(unsigned long long) * 3 * h->R);
+}
+
+// Attempts actually made by replica r: scheduled minus skipped (sub = 4).
+int64_t done_attempts(const lfg_kpz* h, int r) {
+    return h->attempts[size_t(r)] - int64_t(h->hcnt[size_t(2 * h->R + r)]);
 }
 
 lfg_counters make_counters(int64_t att, unsigned long long dep, unsigned long long det) {
@@ -254,7 +259,7 @@ int lfg_kpz_create_batch(lfg_kpz** out, int32_t L, double p, double q, const uin
             h->device = device;
             resolve_plan(h, plan);
             h->seeds.assign(seeds, seeds + replicas);
-            h->hcnt.assign(size_t(2 * replicas), 0);
+            h->hcnt.assign(size_t(3 * replicas), 0);
             h->attempts.assign(size_t(replicas), 0);
             DeviceGuard g(device);
             cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -262,12 +267,12 @@ int lfg_kpz_create_batch(lfg_kpz** out, int32_t L, double p, double q, const uin
             cuda_check(kpz_phase_kernel_attrs(), "kernel attributes");
             h->f = dmalloc<uint32_t>(h->words_per_replica() * size_t(replicas), "alloc lattice");
             h->dseeds = dmalloc<uint64_t>(size_t(replicas), "alloc seeds");
-            h->dcnt = dmalloc<unsigned long long>(size_t(2 * replicas), "alloc counters");
-            cuda_check(cudaMallocHost(&h->hpin, sizeof(unsigned long long) * std::max(3, 2 * replicas)),
+            h->dcnt = dmalloc<unsigned long long>(size_t(3 * replicas), "alloc counters");
+            cuda_check(cudaMallocHost(&h->hpin, sizeof(unsigned long long) * std::max(3, 3 * replicas)),
                        "alloc pinned");
             cuda_check(cudaMemcpyAsync(h->dseeds, seeds, sizeof(uint64_t) * replicas, cudaMemcpyHostToDevice,
                                        h->stream), "seed upload");
-            cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 2 * replicas, h->stream), "memset");
+            cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 3 * replicas, h->stream), "memset");
             h->dbad = dmalloc<unsigned long long>(size_t(replicas), "alloc closure flags");
             cuda_check(cudaMemsetAsync(h->dbad, 0x01, sizeof(unsigned long long) * replicas, h->stream), "memset");
             // SlopeField(L) starts with every slope -1 (lattice.cpp:20-25): spins f(i,j) = (i + j) & 1.
@@ -308,7 +313,6 @@ int lfg_kpz_destroy(lfg_kpz* h) {
         dfree(h->seglen);
         dfree(h->hbuf);
         dfree(h->flags);
-        dfree(h->next_job);
         dfree(h->dbad);
         dfree(h->dglob);
         if (h->hpin) cudaFreeHost(h->hpin);
@@ -324,6 +328,7 @@ int lfg_kpz_get_plan(const lfg_kpz* h, lfg_kpz_plan* out) {
         check_handle(h);
         out->block_x = h->bx;
         out->block_y = h->by;
+        out->sub = h->sub;
     });
 }
 
@@ -467,12 +472,14 @@ int lfg_kpz_sweep(lfg_kpz* h, int64_t n_mcs, lfg_counters* out) {
         DeviceGuard g(h->device);
         read_counters(h);
         std::vector<unsigned long long> before = h->hcnt;
+        std::vector<int64_t> before_att = h->attempts;
         enqueue_sweeps(h, n_mcs);
         read_counters(h);
         if (out)
             for (int r = 0; r < h->R; ++r)
-                out[r] = make_counters(int64_t(h->L) * h->L * n_mcs, h->hcnt[2 * r] - before[2 * r],
-                                       h->hcnt[2 * r + 1] - before[2 * r + 1]);
+                out[r] = make_counters(h->attempts[size_t(r)] - before_att[size_t(r)] -
+                                           int64_t(h->hcnt[size_t(2 * h->R + r)] - before[size_t(2 * h->R + r)]),
+                                       h->hcnt[2 * r] - before[2 * r], h->hcnt[2 * r + 1] - before[2 * r + 1]);
     });
 }
 
@@ -492,21 +499,15 @@ int lfg_kpz_phase(lfg_kpz* h, uint64_t sweep, int32_t phase) {
         check_resident(h);
         if (phase < 0 || phase > 3) throw Error(LFG_EINVAL, "phase must be in 0..3");
         DeviceGuard g(h->device);
-        KpzPhaseArgs a{};
+        KpzPhaseArgs a = base_phase_args(h);
         a.f = h->f;
-        a.counters = h->dcnt;
-        a.L = h->L;
-        a.bx = h->bx;
-        a.by = h->by;
-        a.thrP = threshold32(h->p);
-        a.thrQ = threshold32(h->q);
-        a.general = !(h->p == 1.0 && h->q == 0.0);
         a.row_mask = h->L - 1;
         a.brow0 = 0;
         a.nbrow = h->L / h->by;
         a.sweep = sweep;
         a.phase = phase;
         cuda_check(kpz_launch_phase(a, h->seeds.data(), h->R, h->stream), "kpz_dtr_phase launch");
+        for (int r = 0; r < h->R; ++r) h->attempts[size_t(r)] += sub_sweep_attempts(h, h->L / h->by) / 4;
     });
 }
 
@@ -516,7 +517,7 @@ int lfg_kpz_counters(lfg_kpz* h, int32_t replica, lfg_counters* out) {
         if (replica < 0 || replica >= h->R) throw Error(LFG_EINVAL, "replica index out of range");
         DeviceGuard g(h->device);
         read_counters(h);
-        *out = make_counters(h->attempts[size_t(replica)], h->hcnt[2 * replica], h->hcnt[2 * replica + 1]);
+        *out = make_counters(done_attempts(h, replica), h->hcnt[2 * replica], h->hcnt[2 * replica + 1]);
     });
 }
 
@@ -524,7 +525,7 @@ int lfg_kpz_reset_counters(lfg_kpz* h) {
     return guarded([&] {
         check_handle(h);
         DeviceGuard g(h->device);
-        cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 2 * h->R, h->stream), "memset");
+        cuda_check(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned long long) * 3 * h->R, h->stream), "memset");
         sync(h);
         std::fill(h->hcnt.begin(), h->hcnt.end(), 0ull);
         std::fill(h->attempts.begin(), h->attempts.end(), 0ll);
@@ -553,9 +554,10 @@ int lfg_kpz_debug_record_anchors(lfg_kpz* h, void* dev_buf, size_t capacity_word
             return;
         }
         if (h->R != 1) throw Error(LFG_EINVAL, "debug_record_anchors: single-replica handles only");
-        if (h->bx >= 1024) throw Error(LFG_EINVAL, "debug_record_anchors: needs a plan with block_x < 1024");
-        if (capacity_words < size_t(h->L) * h->L)
-            throw Error(LFG_EINVAL, "debug_record_anchors: buffer must hold L*L words (one sweep)");
+        const size_t need = size_t(h->L) * h->L / 512 * size_t(kpz_rounds(h->sub)) * size_t(h->sub);
+        if (capacity_words < need)
+            throw Error(LFG_EINVAL, "debug_record_anchors: buffer must hold one MCS of records (" +
+                                        std::to_string(need) + " words: L*L/512 tiles x rounds x sub)");
         h->wlog = static_cast<uint32_t*>(dev_buf);
     });
 }
@@ -681,15 +683,15 @@ int lfg_kpz_create_strip(lfg_kpz** out, int32_t L, double p, double q, uint64_t 
             h->strip_only = true;
             resolve_plan(h, plan);
             h->seeds.assign(1, seed);
-            h->hcnt.assign(2, 0);
+            h->hcnt.assign(3, 0);
             h->attempts.assign(1, 0);
             DeviceGuard g(device);
             cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
             h->own_stream = true;
             cuda_check(kpz_phase_kernel_attrs(), "kernel attributes");
-            h->dcnt = dmalloc<unsigned long long>(2, "alloc counters");
+            h->dcnt = dmalloc<unsigned long long>(3, "alloc counters");
             cuda_check(cudaMallocHost(&h->hpin, sizeof(unsigned long long) * 3), "alloc pinned");
-            cuda_check(cudaMemsetAsync(h->dcnt, 0, 16, h->stream), "memset");
+            cuda_check(cudaMemsetAsync(h->dcnt, 0, 24, h->stream), "memset");
             sync(h);
         } catch (...) {
             lfg_kpz_destroy(h);
@@ -736,15 +738,8 @@ int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0,
         if (cap < h->L && cap < nbrow * h->by + 2)
             throw Error(LFG_EINVAL, "row_capacity too small for the strip and its ghost rows");
         DeviceGuard g(h->device);
-        KpzPhaseArgs a{};
+        KpzPhaseArgs a = base_phase_args(h);
         a.f = static_cast<uint32_t*>(rows);
-        a.counters = h->dcnt;
-        a.L = h->L;
-        a.bx = h->bx;
-        a.by = h->by;
-        a.thrP = threshold32(h->p);
-        a.thrQ = threshold32(h->q);
-        a.general = !(h->p == 1.0 && h->q == 0.0);
         a.row_mask = cap - 1;
         a.brow0 = brow0;
         a.nbrow = nbrow;
@@ -756,7 +751,7 @@ int lfg_kpz_strip_phase_push(lfg_kpz* h, void* rows, int32_t cap, int32_t brow0,
         a.push_row_up = peer_up ? push_row_up : -1;
         a.abort_flag = h->abort_flag;
         cuda_check(kpz_launch_phase(a, h->seeds.data(), 1, h->stream), "kpz_dtr_phase launch");
-        h->attempts[0] += int64_t(nbrow) * h->by * h->L / 4;
+        h->attempts[0] += sub_sweep_attempts(h, nbrow) / 4;
     });
 }
 

@@ -19,6 +19,9 @@
 // row, bit i&31 of word i>>5 -- so row j is contiguous and 128-bit loadable.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+
+#include <cudaTypedefs.h>
 
 #include "kpz_kernels.cuh"
 #include "lfg_common.cuh"
@@ -101,6 +104,32 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  : "memory");
 }
 
+// shared -> global bulk store (bulk-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+
+// 3-D tensor copies (cp.async.bulk.tensor, tile mode): box of tensor map `tm`
+// at element coordinates (x, y, z).
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, int x, int y, int z, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(dst), "l"(tm), "r"(x), "r"(y), "r"(z), "r"(mbar)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, int x, int y, int z, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
+                 "r"(x), "r"(y), "r"(z), "r"(src)
+                 : "memory");
+}
+
+// Commit this thread's bulk stores and wait until they are complete (written).
+__device__ __forceinline__ void bulk_commit_and_wait() {
+    asm volatile("cp.async.bulk.commit_group;\n\tcp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // FMA-pipe shift (IMAD.SHL): keeps the anchor-field advance off the ALU pipe.
 __device__ __forceinline__ uint32_t mullo_u32(uint32_t a, uint32_t b) {
     uint32_t d;
@@ -137,14 +166,15 @@ __device__ __forceinline__ uint32_t sel_lt_or(uint32_t u, uint32_t thr_lo, uint3
 // With acceptance draws (p < 1 or q > 0) both tests share their common part
 // g = f_R==f_U & f_L==f_D & f_R!=f_L, and f_R==f_S tells the two moves apart
 // (6 LOP3 per tile instead of 7; 32-bit threshold compares: 498 -> 534 att/ns).
-// The one-hot anchor bit selects the column actually attempted.  All loads
+// The one-hot anchor bit selects the column actually attempted (a zero base
+// makes the attempt a no-op: a tile's skipped groups, sub = 4).  All loads
 // of all tiles are issued before any store (the tiles are disjoint rows), so
 // the NT dependency chains overlap.
 template <int HX, int HY, bool GENERAL, int NT>
 __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], const uint32_t (&xd)[NT],
                                                   const uint32_t (&u)[NT], uint64_t thrP, uint64_t thrQ,
                                                   uint32_t& ndep, uint32_t& ndet, uint32_t (&acc)[NT],
-                                                  uint32_t base_lo = 1u, uint32_t base_hi = 0x10000u) {
+                                                  const uint32_t (&base_lo)[NT], const uint32_t (&base_hi)[NT]) {
     uint32_t own[NT], up[NT], dn[NT], nb[NT], res[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -158,7 +188,7 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
     for (int n = 0; n < NT; ++n) {
         const uint32_t Rw = __funnelshift_r(own[n], nb[n], 1);  // bit i = f(i+1)
         const uint32_t Lw = __funnelshift_l(nb[n], own[n], 1);  // bit i = f(i-1)
-        const uint32_t bit = (HX ? base_hi : base_lo) << xd[n];
+        const uint32_t bit = (HX ? base_hi[n] : base_lo[n]) << xd[n];  // 0: tile skips this round
         if (!GENERAL) {
             const uint32_t flip = lop3<0x80>(lop3<0x81>(own[n], Rw, up[n]), lop3<0x18>(own[n], Lw, dn[n]), bit);
             res[n] = own[n] ^ flip;
@@ -208,24 +238,36 @@ template <bool GENERAL, bool FULL, int NT, bool MW, bool WLOG = false>
 __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT], bool active, uint64_t seed,
                                                  uint64_t sweep, uint32_t block_id, const uint32_t (&tile_id)[NT],
                                                  uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet,
+                                                 uint32_t& nskip, const int rounds, const bool skip,
                                                  const KpzAnchorLog& wlog = KpzAnchorLog{}) {
     // One-hot bases 1 and 1 << 16.  thrQ <= 2^32, so thrQ >> 33 is 0 -- but not to ptxas:
     // the bases become uniform runtime values instead of immediates rematerialised into a
     // vector register every round (one IMAD.MOV per round saved: 984 -> 1007 att/ns).
     const uint32_t zero = uint32_t(thrQ >> 33);
-    const uint32_t base_lo = 1u + zero, base_hi = 0x10000u + zero;
+    const uint32_t one = 1u + zero;
+    // Skip masks (sub = 4): bit g set <=> the tile sits out 4-round group g (< 32).
+    uint32_t mk[NT];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) mk[n] = 0u;
 #pragma unroll 1
-    for (int m4 = 0; m4 < kRounds / 64; ++m4) {
+    for (int m4 = 0; 64 * m4 < rounds; ++m4) {
         const U4 V = draw(seed, sweep, TAG_SET, block_id, uint32_t(m4));
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 4 && 64 * m4 + 16 * j < rounds; ++j) {
             uint32_t setw = sel4(V, j);
             const int m = 4 * m4 + j;
             U4 A[NT];
 #pragma unroll
             for (int n = 0; n < NT; ++n) A[n] = draw(seed, sweep, TAG_ANCHOR, tile_id[n], uint32_t(m));
+            if (m == 0 && skip) {
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    mk[n] = kpz_skip_mask(kpz_skip_k(kpz_skip_bits(A[n].z, A[n].w)));
+                    nskip += 4u * uint32_t(__popc(mk[n]));
+                }
+            }
 #pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 2 && 16 * m + 8 * h < rounds; ++h) {
                 uint32_t xw[NT], yw[NT];
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
@@ -233,12 +275,20 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
                     yw[n] = h ? A[n].w : A[n].z;
                 }
 #pragma unroll 1
-                for (int q = 0; q < 2; ++q) {
+                for (int q = 0; q < 2 && 16 * m + 8 * h + 4 * q < rounds; ++q) {
                     U4 Uw[NT];
                     if (GENERAL) {
 #pragma unroll
                         for (int n = 0; n < NT; ++n)
                             Uw[n] = draw(seed, sweep, TAG_ACCEPT, tile_id[n], uint32_t(4 * m + 2 * h + q));
+                    }
+                    // this 4-round group's one-hot bases per tile (0 while the tile sits out)
+                    uint32_t blo[NT], bhi[NT];
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) {
+                        blo[n] = one & ~mk[n];
+                        bhi[n] = blo[n] << 16;
+                        mk[n] >>= 1;
                     }
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -255,22 +305,22 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
                         if (FULL || active) {
                             if (setw & 2u) {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, base_lo, base_hi);
+                                    kpz_attempt_tiles<1, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, blo, bhi);
                                 else
-                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, base_lo, base_hi);
+                                    kpz_attempt_tiles<0, 1, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, blo, bhi);
                             } else {
                                 if (setw & 1u)
-                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, base_lo, base_hi);
+                                    kpz_attempt_tiles<1, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, blo, bhi);
                                 else
-                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, base_lo, base_hi);
+                                    kpz_attempt_tiles<0, 0, GENERAL, NT>(addr, xd, u, thrP, thrQ, ndep, ndet, acc, blo, bhi);
                             }
                             if (WLOG) {
-                                const uint32_t r = uint32_t(64 * m4 + 16 * j + 8 * h + 4 * q + k);
+                                const uint32_t r = uint32_t(16 * m + 8 * h + 4 * q + k);
 #pragma unroll
                                 for (int n = 0; n < NT; ++n)
                                     wlog.out[r * wlog.stride + wlog.slot[n]] =
                                         tile_id[n] | (xd[n] << 20) | (((addr[n] >> 8) & 7u) << 24) |
-                                        ((setw & 3u) << 27) | (acc[n] ? 1u << 29 : 0u);
+                                        ((setw & 3u) << 27) | (acc[n] ? 1u << 29 : 0u) | (blo[n] ? 0u : 1u << 30);
                             }
                         }
                         setw >>= 2;
@@ -337,7 +387,7 @@ struct KpzDeps {
 };
 
 // One activation of device block (bxi, byi) (block-set `set`) of replica
-// `rep`: stage, 512 single-hit rounds, write back, count.  `mbar_parity` is
+// `rep`: stage, a.rounds single-hit rounds, write back, count.  `mbar_parity` is
 // the phase of the CTA's staging mbarrier (initialised by the caller) that this
 // activation's bulk copies complete.
 template <bool GENERAL, bool FULL, int kNT, bool MW, bool WLOG = false>
@@ -358,46 +408,50 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
     const int Y0 = (sw.oy + byi * a.by) & Lm;
     const int b = X0 & 31;
     const int w0 = ((X0 - 32 + L) & Lm) >> 5;
+    // FULL: the block's 64-word window [X0/32 - 4, X0/32 + 60) and rows -1..by
+    // lie inside the buffer without wrapping -> tensor copies in and out.
+    const int xw = (X0 >> 5) - 4;
+    const int ylo = (Y0 - 1) & rmask;
+    const bool tens = FULL && a.tma && xw >= 0 && xw + 64 <= wpr && ylo + a.by + 2 <= rmask + 1;
 
-    // Stage rows -1..by, slots -1..Wt, funnel-shifting the bit-granular origin
-    // away (slot s of row R <- global bits [X0 + 32 s, X0 + 32 s + 32)).
+    // Stage rows -1..by, slots -1..Wt (slot s of row R <- global bits
+    // [X0 + 32 s, X0 + 32 s + 32)).
     if (FULL) {
-        // Wt == 32 (so L >= 2048 and a row has >= 64 words).  Raw words
-        // [a0, a0 + 40) (a0 = w0 rounded down to 16 bytes) of every staged row
-        // land at words 0..39 of the row's own line by cp.async.bulk (split in
-        // two where the block wraps around x = L), all rows in flight at once
-        // against one mbarrier; each warp then funnel-shifts its rows in place
-        // (all reads of a row before any of its writes; slot -1 goes to word 63
-        // of the previous line, which no raw copy touches).
+        // Wt == 32 (so L >= 2048 and a row has >= 64 words), and X0 is a
+        // multiple of 128 (kpz_ox_quantum): slot s is global word X0/32 + s, and
+        // the raw words [X0/32 - 4, X0/32 + 36) (16-byte aligned) of every
+        // staged row land at words 0..39 of the row's own line by cp.async.bulk
+        // (split in two where the block wraps around x = L), all rows in flight
+        // at once against one mbarrier.  No shift pass: slot s sits at line
+        // word s + 4, so tile column tx reads bank (tx + 4) & 31 and the halo
+        // words H_L / H_R are words 3 / 36 of the same line.
+        // Away from the x / y wrap of the buffer, two tensor copies (64-word
+        // boxes of by/2 + 1 rows, issued by one thread) stage the whole block;
+        // at the wrap every row is one or two 40-word bulk copies.
         const uint32_t mbar = smA + 6 * 256;  // line 6, word 0 (lines < 7 hold no row data)
-        const int a0 = w0 & ~3, m = w0 & 3;
-        const int n1 = min(40, wpr - a0);  // words before the x wrap (a multiple of 4)
         const uint32_t rows = uint32_t(a.by + 2);
         deps.wait_block(bxi, byi);
         if (threadIdx.x == 0) {
             if (init_mbar) mbar_init(mbar, 1);
-            mbar_arrive_expect_tx(mbar, rows * 160u);
+            mbar_arrive_expect_tx(mbar, rows * (tens ? 256u : 160u));
+            if (tens) {
+                const int br = (a.by >> 1) + 1;
+                tma_load_3d(smA + 7 * 256, &a.tm_ld, xw, ylo, rep, mbar);
+                tma_load_3d(smA + uint32_t(7 + br) * 256u, &a.tm_ld, xw, ylo + br, rep, mbar);
+            }
         }
         __syncthreads();
-        for (int R = int(threadIdx.x) - 1; R <= a.by; R += int(blockDim.x)) {
-            const uint32_t* row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
-            const uint32_t dst = smA + uint32_t(R + 8) * 256u;
-            bulk_g2s(dst, row + a0, uint32_t(n1) * 4u, mbar);
-            if (n1 < 40) bulk_g2s(dst + uint32_t(n1) * 4u, row, uint32_t(40 - n1) * 4u, mbar);
+        if (!tens) {
+            const int a0 = xw & wmask;
+            const int n1 = min(40, wpr - a0);  // words before the x wrap (a multiple of 4)
+            for (int R = int(threadIdx.x) - 1; R <= a.by; R += int(blockDim.x)) {
+                const uint32_t* row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
+                const uint32_t dst = smA + uint32_t(R + 8) * 256u;
+                bulk_g2s(dst, row + a0, uint32_t(n1) * 4u, mbar);
+                if (n1 < 40) bulk_g2s(dst + uint32_t(n1) * 4u, row, uint32_t(40 - n1) * 4u, mbar);
+            }
         }
         mbar_wait_parity(mbar, mbar_parity);
-        for (int R = warp - 1; R <= a.by; R += nwarps) {
-            const uint32_t* line = sm + (R + 8) * 64;
-            const uint32_t lo = line[m + lane + 1], hi = line[m + lane + 2];
-            uint32_t elo = 0, ehi = 0;  // lane 0: slot -1, lane 1: slot 32
-            if (lane < 2) {
-                elo = line[m + 33 * lane];
-                ehi = line[m + 33 * lane + 1];
-            }
-            __syncwarp();
-            sm[(R + 8) * 64 + lane] = __funnelshift_r(lo, hi, b);
-            if (lane < 2) sm[lane ? (R + 8) * 64 + 32 : (R + 7) * 64 + 63] = __funnelshift_r(elo, ehi, b);
-        }
     } else {
         deps.wait_block(bxi, byi);
         for (int R = warp - 1; R <= a.by; R += nwarps) {
@@ -417,9 +471,9 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
     for (int n = 0; n < kNT; ++n) {
         const int ty = warp + n * nwarps;
         tile_id[n] = uint32_t(byi * (a.by >> 4) + ty) * uint32_t(L >> 5) + uint32_t(bxi * Wt + tx);
-        lane_base[n] = smA + uint32_t((16 * ty + 8) * 256 + 4 * tx);  // bits 8..10 clear
+        lane_base[n] = smA + uint32_t((16 * ty + 8) * 256 + 4 * tx + (FULL ? 16 : 0));  // bits 8..10 clear
     }
-    uint32_t ndep = 0, ndet = 0;
+    uint32_t ndep = 0, ndet = 0, nskip = 0;
     KpzAnchorLog wl{};
     if (WLOG) {
         const uint32_t tpb = uint32_t(Wt * (a.by >> 4));
@@ -431,7 +485,7 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
                          uint32_t(tx);
     }
     kpz_block_rounds<GENERAL, FULL, kNT, MW, WLOG>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP,
-                                                   a.thrQ, ndep, ndet, wl);
+                                                   a.thrQ, ndep, ndet, nskip, a.rounds, a.skip != 0, wl);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     // A row that a strip neighbour reads as its ghost is also stored straight
     // into that neighbour's ring buffer (NVLink peer memory): the exchange is
@@ -443,19 +497,40 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
         return p ? p + uint32_t(gy & rmask) * uint32_t(wpr) : nullptr;
     };
     if (FULL) {
-        for (int R = warp; R < a.by; R += nwarps) {
-            uint32_t* __restrict__ row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
-            uint32_t* const prow = push ? peer_row(R) : nullptr;
-            const uint32_t cur = sm[(R + 8) * 64 + lane];             // slot lane
-            const uint32_t prv = __shfl_up_sync(0xFFFFFFFFu, cur, 1);  // slot lane-1
-            const uint32_t lo = lane == 0 ? sm[sm_slot(R, -1)] : prv;
-            const uint32_t v = __funnelshift_l(lo, cur, b);
-            row[(w0 + 1 + lane) & wmask] = v;
-            if (prow) prow[(w0 + 1 + lane) & wmask] = v;
-            if (lane == 31 && b != 0) {
-                const uint32_t v2 = __funnelshift_l(cur, sm[(R + 8) * 64 + 32], b);
-                row[(w0 + 33) & wmask] = v2;
-                if (prow) prow[(w0 + 33) & wmask] = v2;
+        // Interior words of rows 0..by-1 (line words 4..35) -> global words
+        // X0/32 .. X0/32 + 31 by bulk stores (128 bytes, 16-byte aligned; split
+        // at the x wrap): every thread's shared writes are made visible to the
+        // async proxy, one thread per row issues its copies and waits for them
+        // (the chained-phase flag is released only after every row landed).
+        // Away from the wraps: two tensor stores of the 64-word window of rows
+        // 0..by-1 (the 32 words outside the block are the inactive
+        // neighbours' words, unchanged in this phase and written back as
+        // staged; a later-phase block that could write them waits for this
+        // block's flag).  At a wrap: per-row 128-byte bulk stores.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        const int gw = X0 >> 5;
+        if (tens) {  // (rows 0..by-1 then lie inside the buffer too)
+            if (threadIdx.x == 0) {
+                const int bs = a.by >> 1;
+                tma_store_3d(&a.tm_st, xw, ylo + 1, rep, smA + 8 * 256);
+                tma_store_3d(&a.tm_st, xw, ylo + 1 + bs, rep, smA + uint32_t(8 + bs) * 256u);
+                bulk_commit_and_wait();
+            }
+        } else {
+            const int n1 = min(32, wpr - gw);
+            for (int R = int(threadIdx.x); R < a.by; R += int(blockDim.x)) {
+                uint32_t* const row = f + uint32_t((Y0 + R) & rmask) * uint32_t(wpr);
+                const uint32_t src = smA + uint32_t(R + 8) * 256u + 16u;
+                bulk_s2g(row + gw, src, uint32_t(n1) * 4u);
+                if (n1 < 32) bulk_s2g(row, src + uint32_t(n1) * 4u, uint32_t(32 - n1) * 4u);
+            }
+            bulk_commit_and_wait();
+        }
+        if (push) {  // the strip's boundary rows also go straight to the neighbour's ring
+            for (int R = warp; R < a.by; R += nwarps) {
+                uint32_t* const prow = peer_row(R);
+                if (prow) prow[(gw + lane) & wmask] = sm[(R + 8) * 64 + 4 + lane];
             }
         }
     } else {
@@ -471,12 +546,14 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
         }
     }
     if (push) __threadfence_system();  // peer stores visible system-wide before the step signal
-    // Counters: deposits, detaches per replica.
+    // Counters: deposits, detaches, skipped attempts (sub = 4) per replica.
     ndep = __reduce_add_sync(0xFFFFFFFFu, ndep);
     if (GENERAL) ndet = __reduce_add_sync(0xFFFFFFFFu, ndet);
+    nskip = __reduce_add_sync(0xFFFFFFFFu, (FULL || tx < Wt) ? nskip : 0u);
     if (lane == 0) {
         if (ndep) atomicAdd(a.counters + 2 * rep + 0, (unsigned long long)ndep);
         if (GENERAL && ndet) atomicAdd(a.counters + 2 * rep + 1, (unsigned long long)ndet);
+        if (nskip) atomicAdd(a.skipped + rep, (unsigned long long)nskip);
     }
 }
 
@@ -496,8 +573,10 @@ __global__ void __launch_bounds__(MW ? (kNT == 2 && LFG_KPZ_MAXBY >= 256 ? 256 :
     uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);  // generic pointer to line 0 (lines < 6 unused)
     const int rep = a.rep0 + int(blockIdx.z);
     const uint64_t seed = a.seeds[blockIdx.z];
-    const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
-    const int set = sw.set(a.phase);
+    // sub-sweep draws of this replica (origin, this phase's block set), from the launcher
+    const uint32_t swd = a.swd[blockIdx.z];
+    const KpzSweep sw{int32_t(swd & 0xFFFu), int32_t((swd >> 12) & 0xFFFu), 0u};
+    const int set = int(swd >> 24);
     if constexpr (!CHAIN) {
         kpz_block_activation<GENERAL, FULL, kNT, MW, WLOG>(a, sm, smA, rep, seed, sw, 2 * int(blockIdx.x) + (set & 1),
                                                      a.brow0 + 2 * int(blockIdx.y) + (set >> 1), 0u, true,
@@ -524,77 +603,6 @@ __global__ void __launch_bounds__(MW ? (kNT == 2 && LFG_KPZ_MAXBY >= 256 ? 256 :
     }
 }
 
-// Whole-sweep kernel (resident lattice): the four DT phases of sweep a.sweep in
-// one persistent launch.  CTAs take activations in phase-major order
-// (round-robin over the resident grid); an activation of phase k > 0 first waits until the blocks of
-// phase k-1 in its 8-neighbourhood have published completion (flag = epoch).
-// Every earlier-phase neighbour is then complete as well (each one is adjacent
-// to a phase-(k-1) neighbour that waited for it), and later-phase neighbours
-// cannot start before this block publishes, so the schedule -- and therefore
-// the lattice -- is exactly that of four back-to-back phase launches, while
-// the tail of each phase overlaps the start of the next (no wave-quantisation
-// gap between phases).
-struct KpzSweepArgs {
-    KpzPhaseArgs p;            // p.phase unused; one replica p.rep0 (seed p.seeds[0])
-    uint32_t* flags;           // [L/by][L/bx] completion epochs of this replica
-    unsigned int* next_job;    // claim counter (zeroed before the launch)
-    uint32_t epoch;            // unique per launch
-    int32_t lg_hx, lg_pp;      // log2(L/bx/2), log2(active blocks per phase): shifts keep the
-                               // job -> block mapping on the uniform datapath (no division)
-    uint32_t dd;               // bits 2k, 2k+1: x / y parity of set(k) ^ set(k - 1), k = 1..3
-};
-
-#ifndef LFG_KPZ_SWEEP_MINB
-#define LFG_KPZ_SWEEP_MINB 6
-#endif
-template <bool GENERAL, bool FULL, int kNT, bool MW>
-__global__ void __launch_bounds__(MW ? 256 / kNT : 32, MW ? (kNT == 1 ? 3 : LFG_KPZ_SWEEP_MINB) : 12)
-    kpz_dtr_sweep_kernel(const __grid_constant__ KpzSweepArgs s) {
-    extern __shared__ __align__(16) uint32_t sm_raw[];
-    const KpzPhaseArgs& a = s.p;
-    const uint32_t sm_base = uint32_t(__cvta_generic_to_shared(sm_raw));
-    const uint32_t smA = (sm_base - 1536u + 2047u) & ~2047u;
-    uint32_t* const sm = sm_raw + (int32_t(smA - sm_base) >> 2);
-    const int nbx = a.L / a.bx, nby = a.L / a.by;
-    const int njobs = 4 << s.lg_pp;
-    uint32_t parity = 0;
-    bool first = true;
-    // Static round-robin: CTA c runs jobs c, c + G, c + 2G, ... in order (the
-    // job index stays a function of blockIdx, so the block/set/RNG bookkeeping
-    // keeps to the uniform datapath as in the phase kernel).  Every CTA's
-    // current job is its smallest unfinished one, so the globally smallest
-    // unfinished job always has its (smaller) dependencies done: no deadlock,
-    // given co-residency (cooperative launch).
-    for (int job = int(blockIdx.x); job < njobs; job += int(gridDim.x)) {
-        const int k = job >> s.lg_pp, idx = job & ((1 << s.lg_pp) - 1);
-        const uint64_t seed = a.seeds[0];
-        const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seed, a.sweep);
-        const int set = sw.set(k);
-        // Phase k visits its block rows starting at row k (mod L/by/2): the
-        // first rows of a phase then depend on rows the previous phase finished
-        // long ago, never on its last (periodic-wrap) row.
-        const int hy_mask = (1 << (s.lg_pp - s.lg_hx)) - 1;
-        const int bxi = 2 * (idx & ((1 << s.lg_hx) - 1)) + (set & 1);
-        const int byi = 2 * (((idx >> s.lg_hx) + k) & hy_mask) + (set >> 1);
-        uint32_t* const fl = s.flags;
-        const int d = int((s.dd >> (2 * k)) & 3u);  // host-computed (see the phase kernel)
-        const KpzDeps deps{k > 0 ? fl : nullptr, nbx, nby, d & 1, d >> 1, s.epoch};
-        kpz_block_activation<GENERAL, FULL, kNT, MW>(a, sm, smA, a.rep0, seed, sw, bxi, byi, parity, first, deps);
-        parity ^= 1u;
-        first = false;
-        __syncthreads();  // every warp's write-back issued before the release
-        // thread 0 publishes; predicated inside one asm block so the loop keeps a
-        // branch-free (uniform) control flow for the next activation
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "setp.eq.u32 p, %2, 0;\n\t"
-            "@p fence.acq_rel.gpu;\n\t"
-            "@p st.release.gpu.global.u32 [%0], %1;\n\t}" ::"l"(fl + byi * nbx + bxi),
-            "r"(s.epoch), "r"(uint32_t(threadIdx.x))
-            : "memory");
-    }
-}
-
 // Tiles per lane for a block height: the largest NT <= LFG_KPZ_NT with by >= 16 NT.
 static int kpz_nt_for(int by) {
     int nt = LFG_KPZ_NT;
@@ -606,9 +614,14 @@ template <int NT, bool MW>
 static void launch_cfg(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_t st) {
     const dim3 block(unsigned(32 * (b.by / 16 / NT)));
     const bool full = b.bx == 1024;
-    if (b.wlog && !full && NT <= 2) {  // debug recording (block_x < 1024 plans only)
-        if (b.general) kpz_dtr_phase_kernel<true, false, NT, MW, true><<<grid, block, smem, st>>>(b);
-        else kpz_dtr_phase_kernel<false, false, NT, MW, true><<<grid, block, smem, st>>>(b);
+    if (b.wlog && NT <= 2) {  // debug write-set recording (every plan, incl. the 1024-wide TMA path)
+        if (full) {
+            if (b.general) kpz_dtr_phase_kernel<true, true, NT, MW, true><<<grid, block, smem, st>>>(b);
+            else kpz_dtr_phase_kernel<false, true, NT, MW, true><<<grid, block, smem, st>>>(b);
+        } else {
+            if (b.general) kpz_dtr_phase_kernel<true, false, NT, MW, true><<<grid, block, smem, st>>>(b);
+            else kpz_dtr_phase_kernel<false, false, NT, MW, true><<<grid, block, smem, st>>>(b);
+        }
         return;
     }
     if (b.dflags) {
@@ -645,20 +658,54 @@ static void launch_nt(const KpzPhaseArgs& b, dim3 grid, size_t smem, cudaStream_
     else launch_cfg<NT, false>(b, grid, smem, st);
 }
 
-cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st) {
-    const size_t smem = kpz_phase_smem_bytes(a.by);
-    const int nt = kpz_nt_for(a.by);
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// 3-D map [replicas][rows][L/32] u32 over f, box 64 words x box_rows rows x 1.
+static bool encode_rows_map(CUtensorMap* m, uint32_t* f, int L, int rows, int replicas, int box_rows) {
+    auto enc = tensor_map_encoder();
+    if (!enc || box_rows > 256) return false;
+    const cuuint64_t dims[3] = {cuuint64_t(L / 32), cuuint64_t(rows), cuuint64_t(replicas)};
+    const cuuint64_t strides[2] = {cuuint64_t(L / 32) * 4, cuuint64_t(L / 32) * 4 * cuuint64_t(rows)};
+    const cuuint32_t box[3] = {64u, cuuint32_t(box_rows), 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, f, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t kpz_launch_phase(const KpzPhaseArgs& a0, const uint64_t* seeds, int replicas, cudaStream_t st) {
+    const size_t smem = kpz_phase_smem_bytes(a0.by);
+    const int nt = kpz_nt_for(a0.by);
+    KpzPhaseArgs a = a0;
+    a.tma = 0;
+    if (a.bx == 1024 && !std::getenv("LFG_KPZ_NO_TENSOR_MAP")) {
+        const int rows = (a.L - 1 & a.row_mask) + 1;
+        a.tma = encode_rows_map(&a.tm_ld, a.f, a.L, rows, replicas, a.by / 2 + 1) &&
+                encode_rows_map(&a.tm_st, a.f, a.L, rows, replicas, a.by / 2);
+    }
     for (int r0 = 0; r0 < replicas; r0 += kMaxRepPerLaunch) {
         KpzPhaseArgs b = a;
         b.rep0 = r0;
         const int nr = std::min(kMaxRepPerLaunch, replicas - r0);
-        for (int r = 0; r < nr; ++r) b.seeds[r] = seeds[r0 + r];
-        if (b.dflags && b.chain_wait) {
-            for (auto& w : b.dd) w = 0;
-            for (int r = 0; r < nr; ++r) {
-                const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seeds[r0 + r], a.sweep);
+        for (auto& w : b.dd) w = 0;
+        for (int r = 0; r < nr; ++r) {
+            b.seeds[r] = seeds[r0 + r];
+            const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seeds[r0 + r], a.sweep);
+            b.swd[r] = uint32_t(sw.ox) | (uint32_t(sw.oy) << 12) | (uint32_t(sw.set(a.phase)) << 24);
+            if (b.dflags && b.chain_wait)
                 b.dd[r >> 5] |= uint64_t(sw.set(a.phase) ^ sw.set(a.phase - 1)) << (2 * (r & 31));
-            }
         }
         const dim3 grid(unsigned(a.L / a.bx / 2), unsigned(a.nbrow / 2), unsigned(nr));
         if (nt >= 4) launch_nt<(LFG_KPZ_NT >= 4 ? 4 : 1)>(b, grid, smem, st);
@@ -668,79 +715,6 @@ cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int r
     return cudaGetLastError();
 }
 
-// ---- whole-sweep launcher
-template <bool GENERAL, bool FULL, int NT, bool MW>
-static cudaError_t launch_sweep_cfg(const KpzSweepArgs& s, int njobs, size_t smem, cudaStream_t st) {
-    auto kern = kpz_dtr_sweep_kernel<GENERAL, FULL, NT, MW>;
-    const int threads = 32 * (s.p.by / 16 / NT);
-    static int per_sm[2][2][3][2] = {};  // occupancy cache per instantiation (device-independent enough: B200 only)
-    int& occ = per_sm[GENERAL][FULL][NT == 4 ? 2 : NT - 1][MW];
-    if (occ == 0) {  // smem attribute for the largest plan (block_y = 128); occupancy for this one
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(kpz_phase_smem_bytes(128)));
-        if (e != cudaSuccess) return e;
-    }
-    {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-    }
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::min(njobs, occ * nsm);
-    void* args[] = {const_cast<KpzSweepArgs*>(&s)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(unsigned(grid)), dim3(unsigned(threads)),
-                                       args, smem, st);
-}
-
-template <int NT, bool MW>
-static cudaError_t launch_sweep_nt(const KpzSweepArgs& s, int njobs, size_t smem, cudaStream_t st) {
-    const bool full = s.p.bx == 1024;
-    if (s.p.general)
-        return full ? launch_sweep_cfg<true, true, NT, MW>(s, njobs, smem, st)
-                    : launch_sweep_cfg<true, false, NT, MW>(s, njobs, smem, st);
-    return full ? launch_sweep_cfg<false, true, NT, MW>(s, njobs, smem, st)
-                : launch_sweep_cfg<false, false, NT, MW>(s, njobs, smem, st);
-}
-
-static int ilog2(int v) {
-    int l = 0;
-    while ((1 << l) < v) ++l;
-    return l;
-}
-
-cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, uint32_t* flags,
-                             unsigned int* next_job, uint32_t& epoch, cudaStream_t st) {
-    const size_t smem = kpz_phase_smem_bytes(a.by);
-    const int nt = kpz_nt_for(a.by);
-    const size_t nblocks = size_t(a.L / a.bx) * size_t(a.L / a.by);
-    for (int r = 0; r < replicas; ++r) {  // one launch per replica
-        KpzSweepArgs s{};
-        s.p = a;
-        s.p.rep0 = r;
-        s.p.seeds[0] = seeds[r];
-        s.flags = flags + size_t(r) * nblocks;
-        s.next_job = next_job;
-        s.epoch = ++epoch;
-        s.lg_hx = ilog2(a.L / a.bx / 2);
-        s.lg_pp = s.lg_hx + ilog2(a.L / a.by / 2);
-        {
-            const KpzSweep sw = kpz_sweep_draw(a.bx, a.by, seeds[r], a.sweep);
-            for (int k = 1; k < 4; ++k) s.dd |= uint32_t(sw.set(k) ^ sw.set(k - 1)) << (2 * k);
-        }
-        cudaError_t e = cudaMemsetAsync(next_job, 0, sizeof(unsigned int), st);
-        if (e != cudaSuccess) return e;
-        const int njobs = 4 << s.lg_pp;
-        const bool mw = a.by > 16 * nt;
-        if (nt >= 4) e = mw ? launch_sweep_nt<(LFG_KPZ_NT >= 4 ? 4 : 1), true>(s, njobs, smem, st)
-                            : launch_sweep_nt<(LFG_KPZ_NT >= 4 ? 4 : 1), false>(s, njobs, smem, st);
-        else if (nt == 2) e = mw ? launch_sweep_nt<2, true>(s, njobs, smem, st) : launch_sweep_nt<2, false>(s, njobs, smem, st);
-        else e = mw ? launch_sweep_nt<1, true>(s, njobs, smem, st) : launch_sweep_nt<1, false>(s, njobs, smem, st);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-}
 
 template <int NT, bool MW>
 static cudaError_t attrs_cfg(int smem) {
@@ -748,6 +722,8 @@ static cudaError_t attrs_cfg(int smem) {
     if (NT <= 2) {
         cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, false, NT, MW, true>, at, smem);
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, false, NT, MW, true>, at, smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT, MW, true>, at, smem);
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<true, true, NT, MW, true>, at, smem);
         if (e != cudaSuccess) return e;
     }
     cudaError_t e = cudaFuncSetAttribute(kpz_dtr_phase_kernel<false, true, NT, MW>, at, smem);

@@ -4,6 +4,7 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace lfg {
@@ -16,18 +17,27 @@ constexpr int kMaxRepPerLaunch = 64;
 
 // Passed as a __grid_constant__ kernel parameter: everything block-uniform
 // (seeds included) lives in the constant bank -> uniform registers.
-struct KpzPhaseArgs {
+struct alignas(64) KpzPhaseArgs {
+    // 1024-wide plans: 3-D tensor maps [R][rows][L/32] u32 of the lattice (or
+    // strip ring buffer); tm_ld boxes 64 words x (by/2 + 1) rows (staging),
+    // tm_st 64 words x by/2 rows (write-back).  tma = 0: per-row bulk copies.
+    CUtensorMap tm_ld;
+    CUtensorMap tm_st;
+    int32_t tma;
     uint32_t* f;                    // spins, replica-major [R][L][L/32]
     unsigned long long* counters;   // [R][2] deposits, detaches (device)
+    unsigned long long* skipped;    // [R] attempts skipped by the sub = 4 count law (device)
     int32_t L, bx, by;
-    uint64_t sweep;                 // global sweep index
+    int32_t rounds;                 // single-hit rounds per block activation (kpz_rounds(sub))
+    int32_t skip;                   // 1: per-tile Poisson attempt counts (sub = 4)
+    uint64_t sweep;                 // global sub-sweep index s' = MCS * sub + k
     int32_t phase;                  // 0..3 position in the sweep's block-set order
     uint64_t thrP, thrQ;            // ceil(p 2^32), ceil(q 2^32)
     bool general;                   // false: p == 1, q == 0 fast path
     int32_t rep0;                   // first replica of this launch (set by the launcher)
     int32_t row_mask;               // buffer row slot = global row & row_mask (L-1: whole lattice)
     int32_t brow0, nbrow;           // block rows [brow0, brow0 + nbrow) of the shifted frame (strips)
-    uint32_t* wlog;                 // debug: this phase's [512 rounds][tiles] anchor records, or nullptr
+    uint32_t* wlog;                 // debug: this phase's [rounds][tiles] anchor records, or nullptr
     // Fused peer push (strip shards over NVLink): blocks writing global row
     // push_row_dn / push_row_up also store it into the lower / upper
     // neighbour's ring buffer (same capacity; peer pointer from CUDA IPC).
@@ -51,6 +61,9 @@ struct KpzPhaseArgs {
     // of set(phase) ^ set(phase - 1), filled by the launcher from the seeds
     uint64_t dd[kMaxRepPerLaunch / 32];
     uint64_t seeds[kMaxRepPerLaunch];
+    // per replica of this launch: ox | oy << 12 | set(phase) << 24 of sub-sweep
+    // `sweep` (kpz_sweep_draw on the host: no Philox / permutation divisions per CTA)
+    uint32_t swd[kMaxRepPerLaunch];
 };
 
 // Device-side step barrier between strip shards (no host synchronisation):
@@ -64,12 +77,6 @@ cudaError_t peer_launch_wait(const uint32_t* flag_a, const uint32_t* flag_b, uin
 size_t kpz_phase_smem_bytes(int by);
 cudaError_t kpz_phase_kernel_attrs();
 cudaError_t kpz_launch_phase(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, cudaStream_t st);
-// All four phases of sweep a.sweep in one persistent launch (resident lattice,
-// a.brow0 = 0, a.nbrow = L/by).  flags: [replicas][L/bx][L/by] u32 completion
-// epochs (any initial content); next_job: one u32 of scratch; epoch: per-handle
-// launch counter (incremented here).
-cudaError_t kpz_launch_sweep(const KpzPhaseArgs& a, const uint64_t* seeds, int replicas, uint32_t* flags,
-                             unsigned int* next_job, uint32_t& epoch, cudaStream_t st);
 cudaError_t kpz_launch_init_flat(uint32_t* f, int L, int replicas, cudaStream_t st);
 cudaError_t kpz_launch_init_zero_slopes(uint32_t* f, int L, int replicas, cudaStream_t st);
 cudaError_t kpz_launch_from_slopes(const uint32_t* X, const uint32_t* Y, int L, uint8_t* f0_scratch,

@@ -83,8 +83,37 @@ LFG_HD uint32_t perm_packed(uint32_t idx, int n, int bits) {
 
 // ---------------------------------------------------------------- KPZ plan
 // Inner layer: 16x8 single-hit domains in 32x16 tiles (one 32-bit word per
-// tile row), 512 rounds per block activation.
+// tile row).  One MCS = `sub` sub-sweeps (plan, 1 or 4); each sub-sweep draws
+// its own origin and block-set order (sweep counter s' = s * sub + k) and gives
+// every block one activation of kpz_rounds(sub) single-hit rounds:
+//   sub = 1: 512 rounds, every tile one attempt per round (the paper's scheme,
+//            PAPER.md:366-380);
+//   sub = 4: 132 rounds; tile t skips the 4-round groups g < 32 whose bit is
+//            set in kpz_skip_mask(K_t), K_t ~ Poisson(1/8) from 16 spare bits of
+//            its first anchor draw -> N_t = 132 - 32 K_t attempts with mean 128
+//            and variance 128 exactly: the Poisson count a 512-site tile gets in
+//            a quarter MCS of random-sequential updates (kpz.cpp:5-19).
+// DESIGN.md §2.1 / §6 (scripts/explore: why both changes are needed).
 constexpr int kTileW = 32, kTileH = 16, kDomW = 16, kDomH = 8, kRounds = 512;
+
+LFG_HD int kpz_rounds(int sub) { return sub == 4 ? 132 : 512; }
+
+// K from 16 uniform bits v: P(K >= k) = {7701, 471, 19, 1} / 2^16 (Poisson(1/8)
+// tail rounded so that E[K] = 1/8 and Var[K] = 1/8 hold exactly).
+LFG_HD uint32_t kpz_skip_k(uint32_t v16) {
+    return uint32_t(v16 >= 57835u) + uint32_t(v16 >= 65065u) + uint32_t(v16 >= 65517u) + uint32_t(v16 >= 65535u);
+}
+
+// Groups g < 32 skipped by a tile with K: nibble {0, 8, A, E, F}[K] repeated
+// (8 K of the 32 groups, spread evenly: 32 K rounds).
+LFG_HD uint32_t kpz_skip_mask(uint32_t k) { return ((0xFEA80u >> (4u * k)) & 0xFu) * 0x11111111u; }
+
+// The 16 spare bits of anchor word batch 0 (the low bytes of words 2 and 3,
+// which the 3-bit row fields never reach).
+LFG_HD uint32_t kpz_skip_bits(uint32_t a2, uint32_t a3) { return (a2 & 0xFFu) | ((a3 & 0xFFu) << 8); }
+
+// x-origin quantum: 128 sites (16-byte aligned rows in HBM) for bx >= 64.
+LFG_HD int32_t kpz_ox_quantum(int32_t bx) { return bx >= 64 ? 128 : 32; }
 
 struct KpzSweep {
     int32_t ox, oy;
@@ -92,10 +121,12 @@ struct KpzSweep {
     LFG_HD int set(int phase) const { return int((perm >> (2 * phase)) & 3u); }
 };
 
+// Draws of sub-sweep s' (the global sub-sweep counter).
 LFG_HD KpzSweep kpz_sweep_draw(int32_t bx, int32_t by, uint64_t seed, uint64_t sweep) {
     const U4 w = draw(seed, sweep, TAG_SWEEP, 0, 0);
     KpzSweep s;
-    s.ox = int32_t(below(w.x, uint32_t(2 * bx)));
+    const int32_t qx = kpz_ox_quantum(bx);
+    s.ox = qx * int32_t(below(w.x, uint32_t(2 * bx / qx)));
     s.oy = int32_t(below(w.y, uint32_t(2 * by)));
     s.perm = perm_packed(below(w.z, 24), 4, 2);
     return s;

@@ -38,6 +38,7 @@ class ExperimentConfig:
     q: float = 0.0
     block_x: int = 0
     block_y: int = 0
+    sub: int = 0          # KPZ sub-sweeps per MCS (0: plan default 4; 1: the paper's scheme)
     # KMC
     conc: float = 0.5
     eps: float = 1.5
@@ -83,7 +84,7 @@ class Row:
 
 def _kpz_open(cfg: ExperimentConfig, r: int) -> KpzLattice:
     k = KpzLattice(cfg.size, cfg.p, cfg.q, cfg.seed + r, block_x=cfg.block_x, block_y=cfg.block_y,
-                   device=cfg.device)
+                   sub=cfg.sub, device=cfg.device)
     k.make_flat_slopes()
     return k
 
@@ -92,7 +93,8 @@ def _kpz_observe(cfg: ExperimentConfig, k: KpzLattice):
     L = cfg.size
     c = k.counters()
     succ = c.deposits + c.detaches
-    return succ, [("W2", k.interface_width()), ("mean_height", -1.0 + 2.0 * (c.deposits - c.detaches) / (L * L))]
+    return succ, int(c.attempts), [("W2", k.interface_width()),
+                                   ("mean_height", -1.0 + 2.0 * (c.deposits - c.detaches) / (L * L))]
 
 
 def _kmc_open(cfg: ExperimentConfig, r: int) -> KmcLattice:
@@ -102,7 +104,8 @@ def _kmc_open(cfg: ExperimentConfig, r: int) -> KmcLattice:
 
 
 def _kmc_observe(cfg: ExperimentConfig, k: KmcLattice):
-    return k.counters().successes, [("open_bonds_per_particle", k.open_bonds_per_particle())]
+    c = k.counters()
+    return c.successes, int(c.attempts), [("open_bonds_per_particle", k.open_bonds_per_particle())]
 
 
 def _run_batch(cfg: ExperimentConfig, rids: List[int]) -> List[Row]:
@@ -112,7 +115,6 @@ def _run_batch(cfg: ExperimentConfig, rids: List[int]) -> List[Row]:
     interval's sweeps to the last one finishing, attributed equally to the realizations."""
     kpz = cfg.model == "kpz"
     opener, observe = (_kpz_open, _kpz_observe) if kpz else (_kmc_open, _kmc_observe)
-    per_mcs = cfg.size ** 2 if kpz else cfg.size ** 3 // 2
     lats = []
     try:
         for r in rids:
@@ -120,7 +122,7 @@ def _run_batch(cfg: ExperimentConfig, rids: List[int]) -> List[Row]:
             if not kpz and len(rids) > 1:
                 lats[-1].set_concurrency(len(rids))
         out = {r: [] for r in rids}
-        t, wall, att = 0, 0.0, 0
+        t, wall = 0, 0.0
         for ts in cfg.sample_times():
             if ts > t:
                 t0 = time.perf_counter()
@@ -133,10 +135,9 @@ def _run_batch(cfg: ExperimentConfig, rids: List[int]) -> List[Row]:
                 for k in lats:
                     k.synchronize()
                 wall += (time.perf_counter() - t0) * 1e3 / len(lats)
-                att += per_mcs * (ts - t)
                 t = ts
             for r, k in zip(rids, lats):
-                succ, obs = observe(cfg, k)
+                succ, att, obs = observe(cfg, k)  # device counters: attempts actually made
                 out[r].extend(Row(t, name, v, att, succ, wall, r) for name, v in obs)
         return [row for r in rids for row in out[r]]
     finally:

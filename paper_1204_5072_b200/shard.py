@@ -52,6 +52,7 @@ class StripPlan:
     world: int
     bx: int
     by: int
+    sub: int = 4  # sub-sweeps per MCS (include/lfg.h lfg_kpz_plan.sub); ownership rolls per sub-sweep
 
     def __post_init__(self):
         if self.L % self.world:
@@ -140,7 +141,7 @@ class CudaStripEngine:
         self.buf = torch.zeros((plan.cap, plan.wpr), dtype=torch.int32, device=f"cuda:{device}")
         lib = _native.lib()
         h = C.c_void_p()
-        kp = _native.KpzPlan(plan.bx, plan.by)
+        kp = _native.KpzPlan(plan.bx, plan.by, plan.sub)
         _native.check(lib.lfg_kpz_create_strip(C.byref(h), plan.L, float(p), float(q), int(seed), C.byref(kp),
                                                device))
         self.h = h
@@ -193,8 +194,9 @@ class CudaStripEngine:
 
 
 def sweep_origin(plan: StripPlan, seed: int, sweep: int):
+    """(ox, oy, [set of phase 0..3]) of global sub-sweep `sweep` (= MCS * plan.sub + k)."""
     out = (C.c_int32 * 6)()
-    kp = _native.KpzPlan(plan.bx, plan.by)
+    kp = _native.KpzPlan(plan.bx, plan.by, plan.sub)
     _native.check(_native.lib().lfg_kpz_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep),
                                                      C.cast(out, C.POINTER(C.c_int32))))
     return int(out[0]), int(out[1]), [int(out[2 + k]) for k in range(4)]
@@ -396,7 +398,7 @@ class ShardedKpz:
         """Each rank fills its window for the first sweep's origin plus both ghosts
         (no communication)."""
         self.sweep_index = sweep_index
-        _, oy, _ = sweep_origin(self.plan, self.seed, sweep_index)
+        _, oy, _ = sweep_origin(self.plan, self.seed, sweep_index * self.plan.sub)
         for e, r in zip(self.engines, self.ranks):
             e.fill(self.plan.start(oy, r) - 1, self.plan.H + 2, 0)
         for e in self.engines:
@@ -415,18 +417,18 @@ class ShardedKpz:
         if getattr(self.comm, "fused_push", False):
             return self._sweep_fused(n)
         for _ in range(n):
-            s = self.sweep_index
-            _, oy, sets = sweep_origin(pl, self.seed, s)
-            if oy != self.oy:
-                old = self.oy
-                self._exchange(lambda r: pl.roll(old, oy, r))
-                self.oy = oy
-            for k in range(4):
-                sy = sets[k] >> 1
-                self._exchange(lambda r: pl.ghost(oy, r, sy))
-                for e, r in zip(self.engines, self.ranks):
-                    b0, nb = pl.block_rows(r)
-                    e.phase(s, k, b0, nb)
+            for s in range(self.sweep_index * pl.sub, (self.sweep_index + 1) * pl.sub):  # sub-sweeps
+                _, oy, sets = sweep_origin(pl, self.seed, s)
+                if oy != self.oy:
+                    old = self.oy
+                    self._exchange(lambda r: pl.roll(old, oy, r))
+                    self.oy = oy
+                for k in range(4):
+                    sy = sets[k] >> 1
+                    self._exchange(lambda r: pl.ghost(oy, r, sy))
+                    for e, r in zip(self.engines, self.ranks):
+                        b0, nb = pl.block_rows(r)
+                        e.phase(s, k, b0, nb)
             self.sweep_index += 1
         for e in self.engines:
             e.sync()
@@ -440,24 +442,24 @@ class ShardedKpz:
         pl, comm = self.plan, self.comm
         e, r = self.engines[0], self.ranks[0]
         for _ in range(n):
-            s = self.sweep_index
-            _, oy, sets = sweep_origin(pl, self.seed, s)
-            ops = []
-            if oy != self.oy:
-                ops += pl.roll(self.oy, oy, r)
-                self.oy = oy
-            comm.exchange(ops)
-            comm.exchange(pl.ghost(oy, r, 0) + pl.ghost(oy, r, 1))
-            first = pl.start(oy, r)
-            last = (first + pl.H - 1) % pl.L
-            b0, nb = pl.block_rows(r)
-            for k in range(4):
-                sy = sets[k] >> 1
-                comm.step()
-                if sy == 0:
-                    e.phase_push(s, k, b0, nb, comm.peer_ring(comm.dn), first, None, -1)
-                else:
-                    e.phase_push(s, k, b0, nb, None, -1, comm.peer_ring(comm.up), last)
+            for s in range(self.sweep_index * pl.sub, (self.sweep_index + 1) * pl.sub):  # sub-sweeps
+                _, oy, sets = sweep_origin(pl, self.seed, s)
+                ops = []
+                if oy != self.oy:
+                    ops += pl.roll(self.oy, oy, r)
+                    self.oy = oy
+                comm.exchange(ops)
+                comm.exchange(pl.ghost(oy, r, 0) + pl.ghost(oy, r, 1))
+                first = pl.start(oy, r)
+                last = (first + pl.H - 1) % pl.L
+                b0, nb = pl.block_rows(r)
+                for k in range(4):
+                    sy = sets[k] >> 1
+                    comm.step()
+                    if sy == 0:
+                        e.phase_push(s, k, b0, nb, comm.peer_ring(comm.dn), first, None, -1)
+                    else:
+                        e.phase_push(s, k, b0, nb, None, -1, comm.peer_ring(comm.up), last)
             self.sweep_index += 1
         comm.step()
         e.sync()

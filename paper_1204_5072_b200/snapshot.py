@@ -42,7 +42,7 @@ def save_kpz(k, path: str) -> None:
         ys.append(y)
         c = k.counters(r)
         cnt.append([int(c.attempts), int(c.deposits), int(c.detaches)])
-    hdr = _header("kpz", L=k.L, p=k.p, q=k.q, seeds=[int(s) for s in k.seeds], plan=list(k.plan),
+    hdr = _header("kpz", L=k.L, p=k.p, q=k.q, seeds=[int(s) for s in k.seeds], plan=list(k.plan) + [int(k.sub)],
                   sweep_index=k.sweep_index, counters=cnt)
     np.savez(path, header=hdr, x=np.stack(xs), y=np.stack(ys))
 
@@ -52,7 +52,8 @@ def load_kpz(path: str, device: int = 0):
 
     hdr, a = _read(path, "kpz")
     k = KpzLattice(int(hdr["L"]), float(hdr["p"]), float(hdr["q"]), seeds=hdr["seeds"],
-                   block_x=int(hdr["plan"][0]), block_y=int(hdr["plan"][1]), device=device)
+                   block_x=int(hdr["plan"][0]), block_y=int(hdr["plan"][1]),
+                   sub=int(hdr["plan"][2]) if len(hdr["plan"]) > 2 else 1, device=device)
     try:
         for r in range(k.replicas):
             k.upload(a["x"][r], a["y"][r], r)

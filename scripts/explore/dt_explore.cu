@@ -42,7 +42,8 @@
 struct Cfg {
     int L = 256, bx = 128, by = 128, mini = 1, counts = 0, skip = 0;
     float thin = 1.f, pt = 0.9f, cap = 2.f;
-    int tc = 0, td = 0, tlog = 4;   // counts 4: N = tc - td with probability 2^-tlog, else tc
+    int tc = 0, td = 0, tlog = 4;
+    int oxq = 1;                    // x-origin quantum (sites)   // counts 4: N = tc - td with probability 2^-tlog, else tc
     int replicas = 4096;
     unsigned long long seed = 1;
     int nt = 0;
@@ -138,6 +139,7 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
     __shared__ int s_rounds;
     __shared__ int s_ox, s_oy, s_perm[4];
     __shared__ long long s_dep[32];
+    __shared__ int s_mn[256];
     curandStatePhilox4_32_10_t st;      // per thread
     curand_init(c.seed, uint64_t(rep) * 4096 + threadIdx.x, 0, &st);
     curandStatePhilox4_32_10_t cs;      // CTA-level draws (thread 0)
@@ -155,7 +157,7 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
         for (int ms = 0; ms < nms; ++ms) {
             if (threadIdx.x == 0) {
                 const uint4 u = curand4(&cs);
-                s_ox = int((uint64_t(u.x) * (2 * c.bx)) >> 32);
+                s_ox = c.oxq * int((uint64_t(u.x) * (2 * c.bx / c.oxq)) >> 32);
                 s_oy = int((uint64_t(u.y) * (2 * c.by)) >> 32);
                 int pool[4] = {0, 1, 2, 3};
                 for (int k = 3; k > 0; --k) {  // Fisher-Yates
@@ -169,8 +171,20 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
                 const int set = s_perm[ph], sx = set & 1, sy = set >> 1;
                 // per-tile counts
                 int my_n[8];
+                uint32_t my_mask_k[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 int tiles = 0;
                 if (threadIdx.x == 0) s_rounds = 0;
+                if (c.counts == 6) {
+                    for (int a = threadIdx.x; a < nact; a += blockDim.x) s_mn[a] = 0;
+                    __syncthreads();
+                    if (threadIdx.x == 0) {
+                        for (int blk = 0; blk < act_blocks; ++blk)
+                            for (int k = 0; k < int(mean_n) * ntile; ++k) {
+                                const int t = int((uint64_t(curand(&cs)) * ntile) >> 32);
+                                ++s_mn[blk * ntile + t];
+                            }
+                    }
+                }
                 __syncthreads();
                 for (int a = threadIdx.x; a < nact; a += blockDim.x, ++tiles) {
                     int n = base_rounds;
@@ -183,6 +197,13 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
                         n = int(lrint(mean_n + sh + sg * g));
                         if (c.counts == 3) n = min(n, int(lrint(mean_n + sh + k * sg)));
                         n = max(0, min(n, 2047));
+                    } else if (c.counts == 6) {
+                        n = s_mn[a];
+                    } else if (c.counts == 5) {
+                        const uint32_t v = curand(&st) >> 16;
+                        const int K = (v >= 57835u) + (v >= 65065u) + (v >= 65517u) + (v >= 65535u);
+                        n = 132 - 32 * K;
+                        my_mask_k[tiles] = ((0xFEA80u >> (4 * K)) & 0xFu) * 0x11111111u;
                     } else if (c.counts == 4) {
                         n = (curand(&st) >> (32 - c.tlog)) == 0 ? c.tc - c.td : c.tc;
                     } else if (c.counts == 2) {
@@ -208,7 +229,9 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
                     const int inner = sets[r], hx = inner & 1, hy = inner >> 1;
                     int k = 0;
                     for (int a = threadIdx.x; a < nact; a += blockDim.x, ++k) {
-                        if (c.skip == 0) {
+                        if (c.counts == 5) {
+                            if (r < 128 && ((my_mask_k[k] >> (r >> 2)) & 1u)) continue;
+                        } else if (c.skip == 0) {
                             if (r >= my_n[k]) continue;
                         } else if (c.skip == 2) {  // spread at 4-round group granularity
                             if (my_n[k] < R) {
@@ -266,6 +289,7 @@ int main(int argc, char** argv) {
         else if (a == "--tc") c.tc = std::stoi(nx());
         else if (a == "--td") c.td = std::stoi(nx());
         else if (a == "--tlog") c.tlog = std::stoi(nx());
+        else if (a == "--oxq") c.oxq = std::stoi(nx());
         else if (a == "--replicas") c.replicas = std::stoi(nx());
         else if (a == "--seed") c.seed = std::stoull(nx());
         else if (a == "--tmax") tmax = std::stoi(nx());
@@ -304,9 +328,9 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(W.data(), w2, n * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(Hm.data(), hm, n * 8, cudaMemcpyDeviceToHost));
     FILE* f = fopen(out.c_str(), "w");
-    fprintf(f, "{\"scheme\":\"%s\",\"L\":%d,\"bx\":%d,\"by\":%d,\"mini\":%d,\"counts\":%d,\"thin\":%g,\"pt\":%g,\"cap\":%g,\"skip\":%d,\"tc\":%d,\"td\":%d,\"tlog\":%d,"
+    fprintf(f, "{\"scheme\":\"%s\",\"L\":%d,\"bx\":%d,\"by\":%d,\"mini\":%d,\"counts\":%d,\"thin\":%g,\"pt\":%g,\"cap\":%g,\"skip\":%d,\"tc\":%d,\"td\":%d,\"tlog\":%d,\"oxq\":%d,"
                "\"replicas\":%d,\"seed\":%llu,\"seconds\":%.3f,\"t\":[",
-            scheme.c_str(), c.L, c.bx, c.by, c.mini, c.counts, c.thin, c.pt, c.cap, c.skip, c.tc, c.td, c.tlog, c.replicas, c.seed, ms / 1e3);
+            scheme.c_str(), c.L, c.bx, c.by, c.mini, c.counts, c.thin, c.pt, c.cap, c.skip, c.tc, c.td, c.tlog, c.oxq, c.replicas, c.seed, ms / 1e3);
     for (int s = 0; s < c.nt; ++s) fprintf(f, "%s%d", s ? "," : "", c.ts[s]);
     fprintf(f, "],\"w2_mean\":[");
     std::vector<double> mw(c.nt), sw(c.nt), mh(c.nt), sh(c.nt);

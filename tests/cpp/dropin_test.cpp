@@ -86,7 +86,8 @@ int main() {
 #endif
     REQUIRE(lf::gpu::interface_width(f) == 0.5);
     const auto c = lf::gpu::kpz_sweep(f, params, rng, 5);
-    REQUIRE(c.attempts == 5LL * 256 * 256);
+    // default plan (sub = 4): Poisson tile counts, mean L^2 and sd L per MCS
+    REQUIRE(std::llabs(c.attempts - 5LL * 256 * 256) < 6LL * 256 * 3);
     REQUIRE(c.successes > 0);
     const double w2 = lf::gpu::interface_width(f);
     REQUIRE(w2 > 0.5);

@@ -33,20 +33,25 @@ def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-# (L, bx, by, p, q, seed, sweep0, nsweeps)
+# (L, bx, by, p, q, seed, sweep0, nsweeps, sub): sub = 4 is the default plan
+# (sub-sweeps + Poisson tile counts), sub = 1 the paper's single-origin scheme.
 KPZ_DTR_CASES = [
-    (64, 32, 32, 1.0, 0.0, 1, 0, 1),
-    (64, 32, 32, 1.0, 0.0, 1, 0, 4),
-    (64, 32, 16, 0.95, 0.05, 7, 3, 3),
-    (128, 64, 32, 1.0, 0.0, 2, 0, 3),
-    (128, 32, 64, 0.5, 0.5, 3, 10, 2),
-    (256, 128, 64, 1.0, 0.0, 11, 0, 2),
-    (256, 64, 128, 0.95, 0.05, 12, 5, 2),
-    (512, 256, 128, 1.0, 0.0, 1, 0, 2),
-    (1024, 512, 128, 1.0, 0.0, 1, 0, 1),
-    (1024, 512, 64, 0.95, 0.05, 5, 100, 1),
-    (2048, 1024, 128, 1.0, 0.0, 1, 0, 1),
-    (2048, 1024, 128, 0.25, 0.75, 9, 0, 1),
+    (64, 32, 32, 1.0, 0.0, 1, 0, 1, 4),
+    (64, 32, 32, 1.0, 0.0, 1, 0, 4, 4),
+    (64, 32, 16, 0.95, 0.05, 7, 3, 3, 4),
+    (128, 64, 32, 1.0, 0.0, 2, 0, 3, 4),
+    (128, 32, 64, 0.5, 0.5, 3, 10, 2, 4),
+    (256, 128, 64, 1.0, 0.0, 11, 0, 2, 4),
+    (256, 64, 128, 0.95, 0.05, 12, 5, 2, 4),
+    (512, 256, 128, 1.0, 0.0, 1, 0, 2, 4),
+    (1024, 512, 128, 1.0, 0.0, 1, 0, 1, 4),
+    (1024, 512, 64, 0.95, 0.05, 5, 100, 1, 4),
+    (2048, 1024, 128, 1.0, 0.0, 1, 0, 1, 4),
+    (2048, 1024, 128, 0.25, 0.75, 9, 0, 1, 4),
+    (64, 32, 32, 1.0, 0.0, 1, 0, 2, 1),
+    (256, 128, 64, 0.95, 0.05, 12, 5, 2, 1),
+    (1024, 512, 128, 1.0, 0.0, 1, 0, 1, 1),
+    (2048, 1024, 128, 0.25, 0.75, 9, 0, 1, 1),
 ]
 
 # (L, bk, eps, both, c, alloy_seed, seed, sweep0, nsweeps)
@@ -119,12 +124,12 @@ def main() -> None:
     out["kpz_c1_head"] = traj
 
     dtr = []
-    for (L, bx, by, p, q, seed, sweep0, ns) in KPZ_DTR_CASES:
+    for (L, bx, by, p, q, seed, sweep0, ns, sub) in KPZ_DTR_CASES:
         x, y = ref.make_flat(L)
-        c = ref.kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, ns, bx, by)
+        c = ref.kpz_sweep_dtr(L, x, y, p, q, seed, sweep0, ns, bx, by, sub)
         h = ref.reconstruct_heights(L, x, y).astype(np.int64)
         rec = {"L": L, "bx": bx, "by": by, "p": p, "q": q, "seed": seed, "sweep0": sweep0,
-               "nsweeps": ns, "counters": [int(v) for v in c], "sx": sha(x), "sy": sha(y),
+               "nsweeps": ns, "sub": sub, "counters": [int(v) for v in c], "sx": sha(x), "sy": sha(y),
                "w2": ref.interface_width(L, x, y), "sum": int(h.sum()), "sum2": int((h ** 2).sum())}
         if L == 64:
             rec["x"] = [int(v) for v in x]

@@ -87,8 +87,11 @@ class CpuStripEngine:
         L, cap, bx, by = pl.L, pl.cap, pl.bx, pl.by
         w = self.buf.numpy().view(np.uint32)
         W = self.draw(sweep, TAG_SWEEP, 0, 0)
-        ox = (W[0] * 2 * bx) >> 32
+        qx = 128 if bx >= 64 else 32  # x-origin quantum (lfg_common.cuh kpz_ox_quantum)
+        ox = qx * ((W[0] * (2 * bx // qx)) >> 32)
         oy = (W[1] * 2 * by) >> 32
+        sub = getattr(pl, "sub", 4)
+        rounds = 132 if sub == 4 else 512
         perm = self.orc.kpz_sweep_draw(L, bx, by, self.seed, sweep)[2:]
         st = int(perm[k])
         sx, sy = st & 1, st >> 1
@@ -103,8 +106,9 @@ class CpuStripEngine:
             for bxi in range(sx, L // bx, 2):
                 block_id = byi * (L // bx) + bxi
                 anc = {}
+                smask = {}
                 sw = None
-                for r in range(512):
+                for r in range(rounds):
                     if r % 64 == 0:
                         sw = self.draw(sweep, TAG_SET, block_id, r >> 6)
                     inner = (sw[(r >> 4) & 3] >> (2 * (r & 15))) & 3
@@ -116,6 +120,12 @@ class CpuStripEngine:
                             if r % 16 == 0:
                                 anc[tid] = self.draw(sweep, TAG_ANCHOR, tid, r >> 4)
                             a4 = anc[tid]
+                            if r == 0:  # sub = 4: Poisson attempt count via skipped 4-round groups
+                                v = (a4[2] & 0xFF) | ((a4[3] & 0xFF) << 8)
+                                K = (v >= 57835) + (v >= 65065) + (v >= 65517) + (v >= 65535)
+                                smask[tid] = [0x0, 0x8, 0xA, 0xE, 0xF][K] * 0x11111111 if sub == 4 else 0
+                            if r < 128 and (smask[tid] >> (r >> 2)) & 1:
+                                continue
                             kk, h = r & 15, (r >> 3) & 1
                             xd = (a4[h] >> (28 - 4 * (kk & 7))) & 15
                             yd = (a4[2 + h] >> (29 - 3 * (kk & 7))) & 7

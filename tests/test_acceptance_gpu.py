@@ -80,7 +80,8 @@ def test_acceptance6_conservation_1e4_mcs(lfg, oracle):
         k.make_flat_slopes()
         x0, y0 = k.download()
         c = k.sweep(10000)
-        assert c.attempts == 10000 * L * L
+        # sub = 4: Poisson tile counts, mean L^2 per MCS, sd L per MCS (tests/test_oracle.py)
+        assert abs(c.attempts - 10000 * L * L) < 6 * L * 100
         x, y = k.download()
 
     def row_sums_x(words):  # sum_i sigma_x(i, j) for every row j (bit 1 <=> +1)

@@ -62,15 +62,26 @@ def test_kpz_flat_single_row(tmp_path):
 
 @pytest.mark.gpu
 def test_kpz_series_accounting(tmp_path):
-    """Accounting exactness: attempts = t * N at every sample row."""
+    """Accounting: the attempts column is the device count; with the
+    default sub = 4 plan it is t * N on average (sd L per MCS, Poisson tile counts),
+    with sub = 1 (the paper's scheme) exactly t * N -- see test_kpz_series_accounting_sub1."""
     out = tmp_path / "kpz.csv"
     assert parse_and_run(["kpz", "--size", "256", "--mcs", "30", "--realizations", "2", "--out", str(out)]) == 0
     _, rows = read_csv(out.read_text())
     assert {r.realization_id for r in rows} == {0, 1}
     for r in rows:
-        assert r.attempts == r.t * 256 * 256
+        assert abs(r.attempts - r.t * 256 * 256) < 6 * 256 * max(1, r.t) ** 0.5
     ts = [r.t for r in rows if r.realization_id == 0 and r.observable_name == "W2"]
     assert ts == sorted(set(ts)) and ts[-1] == 30
+
+
+@pytest.mark.gpu
+def test_kpz_series_accounting_sub1(tmp_path):
+    """Accounting exactness with the paper's scheme (--sub 1): attempts = t * N."""
+    out = tmp_path / "kpz1.csv"
+    assert parse_and_run(["kpz", "--size", "256", "--mcs", "12", "--sub", "1", "--out", str(out)]) == 0
+    _, rows = read_csv(out.read_text())
+    assert rows and all(r.attempts == r.t * 256 * 256 for r in rows)
 
 
 @pytest.mark.gpu

@@ -104,14 +104,15 @@ def test_c1_head_golden(oracle, golden):
         assert oracle.interface_width(L, x, y) == pt["w2"]
 
 
-@pytest.mark.parametrize("case", range(12))
+@pytest.mark.parametrize("case", range(16))
 def test_dtr_golden(oracle, golden, case):
     g = golden["kpz_dtr"][case]
     if g["L"] > 1024:
         pytest.skip("covered by the GPU tier")
     L = g["L"]
     x, y = oracle.kpz_flat(L)
-    c = oracle.kpz_sweep_dtr(L, x, y, g["p"], g["q"], g["seed"], g["sweep0"], g["nsweeps"], g["bx"], g["by"])
+    c = oracle.kpz_sweep_dtr(L, x, y, g["p"], g["q"], g["seed"], g["sweep0"], g["nsweeps"], g["bx"], g["by"],
+                             g["sub"])
     assert [int(v) for v in c] == g["counters"]
     assert sha(x) == g["sx"] and sha(y) == g["sy"]
     assert oracle.interface_width(L, x, y) == g["w2"]
@@ -129,20 +130,42 @@ def test_dtr_live_vs_ref(oracle, reflib):
         seed = int(rs.randint(0, 2**63))
         x1, y1 = oracle.kpz_flat(L)
         x2, y2 = reflib.make_flat(L)
-        c1 = oracle.kpz_sweep_dtr(L, x1, y1, p, q, seed, 123, 2, bx, by)
-        c2 = reflib.kpz_sweep_dtr(L, x2, y2, p, q, seed, 123, 2, bx, by)
+        sub = int(rs.choice([1, 4]))
+        c1 = oracle.kpz_sweep_dtr(L, x1, y1, p, q, seed, 123, 2, bx, by, sub)
+        c2 = reflib.kpz_sweep_dtr(L, x2, y2, p, q, seed, 123, 2, bx, by, sub)
         assert (c1 == c2).all() and (x1 == x2).all() and (y1 == y2).all()
         assert oracle.interface_width(L, x1, y1) == reflib.interface_width(L, x2, y2)
         assert (oracle.reconstruct_heights(L, x1, y1) == reflib.reconstruct_heights(L, x2, y2)).all()
 
 
 def test_dtr_attempt_accounting_and_closure(oracle):
-    # SPEC.md:349 exact accounting; closure invariant under the DTr scheduler.
+    # sub = 1: SPEC.md:349 exact accounting (L^2 per MCS).  sub = 4: every tile
+    # makes 132 - 32 K attempts per activation, K ~ Poisson(1/8) from 16 bits
+    # (mean 128, variance 128 exactly); 16 activations of L^2/512 tiles per 4
+    # sub-sweeps -> mean L^2 per MCS, sd sqrt(128 * 4 * L^2 / 512) = L per MCS.
+    # Closure is invariant under the DTr scheduler either way.
     for L, bx, by in ((64, 32, 16), (128, 64, 64)):
         x, y = oracle.kpz_flat(L)
-        c = oracle.kpz_sweep_dtr(L, x, y, 0.7, 0.3, 5, 0, 5, bx, by)
+        c = oracle.kpz_sweep_dtr(L, x, y, 0.7, 0.3, 5, 0, 5, bx, by, 1)
         assert c[0] == 5 * L * L and c[1] == c[2] + c[3]
         assert oracle.closure_holds(L, x, y)
+    L, n = 256, 40
+    x, y = oracle.kpz_flat(L)
+    c = oracle.kpz_sweep_dtr(L, x, y, 1.0, 0.0, 3, 0, n, 128, 64, 4)
+    assert abs(int(c[0]) - n * L * L) < 5 * L * n ** 0.5 and c[1] == c[2] + c[3]
+    assert oracle.closure_holds(L, x, y)
+
+
+def test_skip_law_moments():
+    # the 16-bit Poisson(1/8) law of the sub = 4 tile counts: E[K] = Var[K] = 1/8 exactly
+    import numpy as np
+
+    v = np.arange(65536)
+    K = (v >= 57835).astype(int) + (v >= 65065) + (v >= 65517) + (v >= 65535)
+    assert K.sum() * 8 == 65536
+    assert (K * K).sum() * 65536 - K.sum() ** 2 == 65536 ** 2 // 8
+    N = 132 - 32 * K
+    assert N.mean() == 128 and N.var() == 128
 
 
 def test_sweep_draw_ranges(oracle):

@@ -46,62 +46,68 @@ def _writes(L, ox, oy, rec):
     return tile, acc, sites.astype(np.int64)
 
 
-def _log_arrays(groups):
-    """groups: list of lists of (worker, sites[k]) -> flat arrays for ref_writelog_violations."""
-    goff, tw, woff, ws = [0], [], [0], []
-    for g in groups:
-        for worker, sites in g:
-            tw.append(worker)
-            ws.extend(sites)
-            woff.append(len(ws))
-        goff.append(len(tw))
-    return (np.array(goff, np.int64), np.array(tw, np.int32), np.array(woff, np.int64),
-            np.array(ws if ws else [0], np.int64))
+def _np_log(workers, acc, sites):
+    """Vectorised _log_arrays: workers / acc [G, T] (interval g, worker slot t),
+    sites [G, T, 4]; an accepted attempt writes its four sites."""
+    G, T = workers.shape
+    nw = np.where(acc, 4, 0).reshape(-1)
+    goff = np.arange(G + 1, dtype=np.int64) * T
+    woff = np.concatenate([[0], np.cumsum(nw)]).astype(np.int64)
+    ws = sites.reshape(-1, 4)[acc.reshape(-1)].reshape(-1).astype(np.int64)
+    return goff, workers.reshape(-1).astype(np.int32), woff, (ws if ws.size else np.zeros(1, np.int64))
 
 
-@pytest.mark.parametrize("p,q", [(1.0, 0.0), (0.95, 0.05)])
-def test_dt_write_sets_are_disjoint(lfg, oracle, reflib, p, q):
+@pytest.mark.parametrize("L,bx,by,sub,p,q,nsweeps", [
+    (256, 64, 32, 4, 1.0, 0.0, 30), (256, 64, 32, 4, 0.95, 0.05, 30), (256, 64, 32, 1, 0.95, 0.05, 30),
+    (2048, 1024, 128, 4, 1.0, 0.0, 2), (2048, 1024, 128, 4, 0.95, 0.05, 2), (2048, 1024, 128, 1, 1.0, 0.0, 1)])
+def test_dt_write_sets_are_disjoint(lfg, oracle, reflib, L, bx, by, sub, p, q, nsweeps):
+    """Every plan incl. the production 1024 x 128 TMA path (L = 2048) and both sub modes."""
     import torch
 
-    L, bx, by, seed, nsweeps = 256, 64, 32, 4711, 100
-    buf = torch.zeros(L * L, dtype=torch.int32, device="cuda")
+    seed = 4711
+    rounds = 132 if sub == 4 else 512
+    ntiles = L * L // 512
+    nrec = ntiles * rounds * sub
+    buf = torch.zeros(nrec, dtype=torch.int32, device="cuda")
     ntile_x = L // 32
     tpb_x, tpb_y = bx // 32, by // 16
+    nblocks = (L // bx) * (L // by)
     total_rw = total_bw = 0
-    with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by) as k:
-        lfg._native.check(lfg._native.lib().lfg_kpz_debug_record_anchors(k._h, buf.data_ptr(), L * L))
+    with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by, sub=sub) as k:
+        lfg._native.check(lfg._native.lib().lfg_kpz_debug_record_anchors(k._h, buf.data_ptr(), nrec))
         k.make_flat_slopes()
         for s in range(nsweeps):
             c = k.sweep(1)
-            rec = buf.cpu().numpy().view(np.uint32).reshape(4, 512, -1)
-            d = oracle.kpz_sweep_draw(L, bx, by, seed, s)
-            ox, oy = int(d[0]), int(d[1])
-            tile, acc, sites = _writes(L, ox, oy, rec.reshape(-1))
-            assert acc.sum() == c.successes and rec.size == L * L  # every attempt recorded once
-            tile = tile.reshape(4, 512, -1)
-            acc = acc.reshape(4, 512, -1)
-            sites = sites.reshape(4, 512, -1, 4)
-            rounds, blocks = [], []
-            for ph in range(4):
-                per_block = {}
-                for r in range(512):
-                    g = [(int(tile[ph, r, t]), sites[ph, r, t].tolist() if acc[ph, r, t] else [])
-                         for t in range(tile.shape[2])]
-                    rounds.append(g)
-                    for (w, ss) in g:
-                        b = (w // ntile_x // tpb_y) * (L // bx) + (w % ntile_x) // tpb_x
-                        per_block.setdefault(b, []).extend(ss)
-                blocks.append(list(per_block.items()))
-            nv, nw, first = reflib.writelog_violations(L * L // 512, *_log_arrays(rounds))
-            assert nv == 0, (s, first)
-            nv2, nw2, first2 = reflib.writelog_violations((L // bx) * (L // by), *_log_arrays(blocks))
-            assert nv2 == 0, (s, first2)
-            assert nw == nw2 == 4 * c.successes
-            total_rw += nw
-            total_bw += nw2
-            if s == 0:  # negative control: a phase as one interval with tiles as workers must race
-                wrong = [[w for g in rounds[ph * 512:(ph + 1) * 512] for w in g] for ph in range(4)]
-                nvw, _, _ = reflib.writelog_violations(L * L // 512, *_log_arrays(wrong))
-                assert nvw > 0
+            rec = buf.cpu().numpy().view(np.uint32).reshape(sub, 4, rounds, ntiles // 4)
+            skipped = ((rec >> 30) & 1).astype(bool)
+            assert int((~skipped).sum()) == c.attempts  # every attempt recorded once
+            nacc = 0
+            for kk in range(sub):
+                d = oracle.kpz_sweep_draw(L, bx, by, seed, s * sub + kk)
+                tile, acc, sites = _writes(L, int(d[0]), int(d[1]), rec[kk].reshape(-1))
+                assert not (acc & skipped[kk].reshape(-1)).any()
+                nacc += int(acc.sum())
+                T = ntiles // 4
+                tile = tile.reshape(4 * rounds, T)
+                acc = acc.reshape(4 * rounds, T)
+                sites = sites.reshape(4 * rounds, T, 4)
+                # round level: one interval per (phase, round), workers = tiles
+                nv, nw, first = reflib.writelog_violations(ntiles, *_np_log(tile, acc, sites))
+                assert nv == 0, (s, kk, first)
+                # block level: one interval per phase, workers = device blocks
+                blk = (tile // ntile_x // tpb_y) * (L // bx) + (tile % ntile_x) // tpb_x
+                bw = blk.reshape(4, rounds * T)
+                nv2, nw2, first2 = reflib.writelog_violations(
+                    nblocks, *_np_log(bw, acc.reshape(4, rounds * T), sites.reshape(4, rounds * T, 4)))
+                assert nv2 == 0, (s, kk, first2)
+                assert nw == nw2
+                total_rw += nw
+                total_bw += nw2
+                if s == 0 and kk == 0:  # negative control: a phase as one interval with tiles as workers must race
+                    nvw, _, _ = reflib.writelog_violations(
+                        ntiles, *_np_log(tile.reshape(4, rounds * T), acc.reshape(4, rounds * T),
+                                         sites.reshape(4, rounds * T, 4)))
+                    assert nvw > 0
+            assert nacc == c.successes
         lfg._native.check(lfg._native.lib().lfg_kpz_debug_record_anchors(k._h, None, 0))
     assert total_rw > 0 and total_bw > 0
