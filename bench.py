@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--L", type=int, default=0,
-                    help="lattice edge (0: 2^16 = configs[1] at N=1; 2^17 = configs[2]'s strip-sharded lattice at N>1)")
+                    help="lattice edge (0: 2^16, the metric's configs[1] lattice, at every N)")
     ap.add_argument("--p", type=float, default=1.0)
     ap.add_argument("--q", type=float, default=0.0)
     ap.add_argument("--seed", type=int, default=1)
@@ -51,10 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kmc", action="store_true")
-    ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] single-GPU sub-measurement")
+    ap.add_argument("--no-c3", action="store_true", help="skip the configs[2] (L=2^17, p=0.95, q=0.05) sub-measurement")
     a = ap.parse_args()
-    if a.L == 0:
-        a.L = (1 << 16) if int(os.environ.get("WORLD_SIZE", "1")) == 1 else (1 << 17)
+    a.L = a.L or (1 << 16)
     return a
 
 
@@ -320,26 +319,122 @@ def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
     return out
 
 
-def c3_measure(lfg, torch, stream, steps, warmup, L=1 << 17):
-    """BASELINE configs[2]'s lattice and parameters (L = 2^17, p = 0.95, q = 0.05, flat
-    start) on this one GPU: the denominator of its strong-scaling runs at N > 1."""
-    k = lfg.KpzLattice(L, 0.95, 0.05, 1)
-    try:
-        k.set_stream(stream.cuda_stream)
-        k.make_flat_slopes()
-        k.sweep_async(warmup)
+class KpzRun:
+    """One KPZ lattice of the bench with the same interface at every N: the resident
+    lattice on this GPU (N = 1) or the strip-sharded lattice across the ranks (N > 1,
+    one strip per GPU; peer memory over NVLink, torch.distributed as the fallback)."""
+
+    def __init__(self, lfg, torch, dist, L, p, q, seed, rank, world, local, stream, block_x=0, block_y=0):
+        self.torch, self.dist, self.world, self.L = torch, dist, world, L
+        if world == 1:
+            self.k = k = lfg.KpzLattice(L, p, q, seed, block_x=block_x, block_y=block_y, device=local)
+            k.set_stream(stream.cuda_stream)
+            k.make_flat_slopes()
+            self.stream, self.plan, self.sub = stream, k.plan, k.sub
+            self.mode = "1 GPU"
+            return
+        from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, PeerComm, ShardedKpz, StripPlan
+
+        bx, by = block_x or min(1024, L // 2), block_y or min(128, L // 2)
+        self.plan = (bx, by)
+        pl = StripPlan(L, world, bx, by)
+        self.sub = pl.sub
+        eng = CudaStripEngine(pl, p, q, seed, local)
+        # Default: peer memory (CUDA IPC over NVLink; ghost rows pushed by the phase
+        # kernel's write-back, device-side step barriers).  LFG_COMM=nccl selects
+        # torch.distributed P2P; a peer setup failure falls back to it.
+        comm, how = None, "torch.distributed " + dist.get_backend()
+        if os.environ.get("LFG_COMM", "peer") == "peer":
+            try:
+                comm, how = PeerComm(eng), "peer memory (CUDA IPC / NVLink), fused write-back push"
+            except Exception as ex:  # reported in the JSON line
+                how = f"torch.distributed {dist.get_backend()} (peer setup failed: {ex})"
+        if comm is None:
+            comm = DistComm(eng)
+        sk = ShardedKpz(pl, seed, [eng], [rank], comm)
+        sk.make_flat_slopes()
+        if isinstance(comm, PeerComm):  # a peer barrier that times out anywhere -> everyone falls back
+            try:
+                sk.sweep(1)
+                bad = 0
+            except Exception:
+                bad = 1
+            t = torch.tensor([bad], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(t)
+            if int(t.item()):
+                comm.close()
+                comm, how = DistComm(eng), f"torch.distributed {dist.get_backend()} (peer barrier timed out)"
+                sk = ShardedKpz(pl, seed, [eng], [rank], comm)
+                sk.make_flat_slopes()
+        self.eng, self.sk, self.rank = eng, sk, rank
+        self.stream = eng.stream
+        self.mode = (f"strip-sharded x{world} (rows rolled per sub-sweep, one ghost row per phase; {how})")
+
+    def run(self, n):
+        if self.world == 1:
+            self.k.sweep_async(n)
+        else:
+            self.sk.sweep(n)
+
+    def done(self):
+        """Attempts made so far by the whole job (device counters; sub = 4: Poisson tiles)."""
+        if self.world == 1:
+            return self.k.counters().attempts
+        t = self.torch.tensor([float(self.eng.counters().attempts)], dtype=self.torch.float64,
+                              device="cuda" if self.dist.get_backend() == "nccl" else "cpu")
+        self.dist.all_reduce(t)
+        return int(t.item())
+
+    def launch_ms(self, n=8):
+        """Mean duration of this rank's dominant-kernel launch (one DT phase), CUDA events on
+        the launching stream; the phases are timed after the timed region (no trajectory)."""
+        torch = self.torch
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        if self.world == 1:
+            s0 = self.k.sweep_index
+        else:
+            s0 = self.sk.sweep_index
+            b0, nb = self.sk.plan.block_rows(self.rank)
+        for i, (a, b) in enumerate(ev):
+            a.record(self.stream)
+            if self.world == 1:
+                self.k.phase(s0 * self.sub + i // 4, i % 4)
+            else:
+                self.eng.phase(s0 * self.sub + i // 4, i % 4, b0, nb)
+            b.record(self.stream)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        k.sweep_async(steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        return {"value": L * L * steps / (ms * 1e6), "unit": "attempts/ns", "ms_per_mcs": ms / steps,
-                "steps": steps, "config": f"KPZ DTr L={L}, p=0.95, q=0.05, flat start, plan {k.plan} "
-                                         f"(BASELINE.json configs[2] on 1 GPU)"}
-    finally:
-        k.close()
+        if self.world == 1:
+            self.k.sweep_index = s0 + 1
+        return statistics.mean(a.elapsed_time(b) for a, b in ev)
+
+    def close(self):
+        if self.world == 1:
+            self.k.close()
+
+
+def timed(torch, dist, lat, steps, warmup, barrier, clocks=None):
+    """W warm-up MCS, then K MCS between CUDA events on the launching stream with a
+    barrier + synchronize on both sides; max over ranks.  -> (attempts/ns, ms, clocks)."""
+    lat.run(warmup)
+    barrier()
+    att0 = lat.done()
+    if clocks is not None:
+        clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(lat.stream)
+    lat.run(steps)
+    e1.record(lat.stream)
+    barrier()
+    clk = clocks.stop() if clocks is not None else None
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    att = lat.done() - att0
+    return att / (ms * 1e6), ms, clk
 
 
 def run_b200(args):
@@ -369,93 +464,26 @@ def run_b200(args):
         torch.cuda.synchronize()
 
     peak, peak_kind = measured_peaks()
+    lat = KpzRun(lfg, torch, dist, L, args.p, args.q, args.seed, rank, world, local, stream, args.block_x,
+                 args.block_y)
+    plan, sub, mode = lat.plan, lat.sub, lat.mode
+    stream = lat.stream
     if world == 1:
-        k = lfg.KpzLattice(L, args.p, args.q, args.seed, block_x=args.block_x, block_y=args.block_y, device=local)
-        k.set_stream(stream.cuda_stream)
-        k.make_flat_slopes()
-        plan = k.plan
-        run = lambda n: k.sweep_async(n)  # noqa: E731
-        done = lambda: k.counters().attempts  # noqa: E731  device count of attempts made (sub = 4: Poisson tiles)
-        sub = k.sub
-        mode = "1 GPU"
+        k = lat.k
     else:
-        from paper_1204_5072_b200.shard import CudaStripEngine, DistComm, PeerComm, ShardedKpz, StripPlan
+        eng, sk = lat.eng, lat.sk
+    value, ms, clk = timed(torch, dist, lat, args.steps, args.warmup, barrier, ClockSampler(local))
 
-        bx, by = min(1024, L // 2), min(128, L // 2)
-        plan = (bx, by)
-        pl = StripPlan(L, world, bx, by)
-        eng = CudaStripEngine(pl, args.p, args.q, args.seed, local)
-        # Default: peer memory (CUDA IPC over NVLink; ghost rows pushed by the phase
-        # kernel's write-back, device-side step barriers).  LFG_COMM=nccl selects
-        # torch.distributed P2P; a peer setup failure falls back to it.
-        comm, how = None, "torch.distributed " + dist.get_backend()
-        if os.environ.get("LFG_COMM", "peer") == "peer":
-            try:
-                comm, how = PeerComm(eng), "peer memory (CUDA IPC / NVLink), fused write-back push"
-            except Exception as ex:  # reported in the JSON line
-                how = f"torch.distributed {dist.get_backend()} (peer setup failed: {ex})"
-        if comm is None:
-            comm = DistComm(eng)
-        sk = ShardedKpz(pl, args.seed, [eng], [rank], comm)
-        sk.make_flat_slopes()
-        if isinstance(comm, PeerComm):  # a peer barrier that times out anywhere -> everyone falls back
-            try:
-                sk.sweep(1)
-                bad = 0
-            except Exception:
-                bad = 1
-            t = torch.tensor([bad], device="cuda" if dist.get_backend() == "nccl" else "cpu")
-            dist.all_reduce(t)
-            if int(t.item()):
-                comm.close()
-                comm, how = DistComm(eng), f"torch.distributed {dist.get_backend()} (peer barrier timed out)"
-                sk = ShardedKpz(pl, args.seed, [eng], [rank], comm)
-                sk.make_flat_slopes()
-        stream = eng.stream
-        run = sk.sweep
-        sub = pl.sub
-
-        def done():  # attempts made by all ranks (device counters)
-            t = torch.tensor([eng.counters().attempts], dtype=torch.float64,
-                             device="cuda" if dist.get_backend() == "nccl" else "cpu")
-            dist.all_reduce(t)
-            return int(t.item())
-        mode = f"strip-sharded x{world} (rows rolled per sweep, one ghost row per phase; {how})"
-
-    run(args.warmup)
-    barrier()
-    att0 = done()
-    clocks = ClockSampler(local)
-    clocks.start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    run(args.steps)
-    e1.record(stream)
-    barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    att_timed = done() - att0  # attempts the timed sweeps made (mean L^2 per MCS)
-    value = att_timed / (ms * 1e6)  # attempts/ns, whole job (fixed L: strong scaling)
-
-    # dominant kernel: event-timed phase launches on the launching stream
+    # dominant kernel: event-timed phase launches on the launching stream (this rank's
+    # strip phases at N > 1: per-GPU bytes / per-GPU launch time)
     roofline = None
-    if world == 1:
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(8)]
-        s0 = k.sweep_index
-        for i, (a, b) in enumerate(ev):  # two sub-sweeps of MCS s0 (phase launches take the sub-sweep index)
-            a.record(stream)
-            k.phase(s0 * sub + i // 4, i % 4)
-            b.record(stream)
-        k.sweep_index = s0 + 1
-        torch.cuda.synchronize()
-        avg_launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / (4 * sub)  # mean attempts per launch
+    if True:
+        avg_launch_ms = lat.launch_ms()
+        if dist is not None:
+            t = torch.tensor([avg_launch_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            avg_launch_ms = float(t.item())
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * attempts_per_step / world / (4 * sub)  # mean, per GPU
         achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
         traffic, ncu = None, {}
         try:
@@ -468,7 +496,7 @@ def run_b200(args):
         # SMSPs at the clock sampled during the timed region / warp-instructions per attempt
         # (ncu count of one launch of this kernel at L = 2^16, p = 1).
         issue = None
-        if ncu.get("inst_executed") and L == 1 << 16 and args.p == 1.0 and args.q == 0.0:
+        if ncu.get("inst_executed") and world == 1 and L == 1 << 16 and args.p == 1.0 and args.q == 0.0:
             wi_per_att = ncu["inst_executed"] / (attempts_per_step / (4 * ncu.get("sub", 1)))
             f_ghz = (clk.get("sm_mhz") or 1965.0) / 1000.0
             ceil_att = 148 * 4 * f_ghz / wi_per_att
@@ -479,7 +507,7 @@ def run_b200(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": traffic, "peak_source": peak_kind, "kernel": "kpz_dtr_phase_kernel",
                     "avg_launch_ms": avg_launch_ms, "alg_bytes_per_launch": bytes_per_launch,
-                    "binding_unit": "SM issue / ALU pipe (profiles/r01h_kpz_ncu.txt: issue 74%, ALU 59%, DRAM 6%)",
+                    "binding_unit": ncu.get("binding", "SM issue (profiles/ncu_summary.json)"),
                     "issue_roofline": issue,
                     "note": "algorithmic bytes = 0.5 B/attempt (two 1-bit slope planes read+written once per MCS, "
                             "SURVEY.md §8(d)); the device keeps 1 spin bit per site; the faithful single-hit "
@@ -603,23 +631,29 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_kmc:
         kmc = kmc_measure(lfg, torch, stream, steps=20, warmup=3)
     c3 = None
-    if rank == 0 and world == 1 and not args.no_c3:
-        c3 = c3_measure(lfg, torch, stream, steps=10, warmup=3)
+    if not args.no_c3:  # BASELINE configs[2]: L = 2^17, p = 0.95, q = 0.05, at every N (strips at N > 1)
+        l3 = KpzRun(lfg, torch, dist, 1 << 17, 0.95, 0.05, 1, rank, world, local, torch.cuda.current_stream())
+        v3, ms3, _ = timed(torch, dist, l3, 10, 3, barrier)
+        c3 = {"value": v3, "unit": "attempts/ns", "ms_per_mcs": ms3 / 10, "steps": 10, "n_gpus": world,
+              "config": f"KPZ DTr L=131072, p=0.95, q=0.05, flat start, plan {l3.plan} sub={l3.sub} "
+                        f"(BASELINE.json configs[2]; {l3.mode})"}
+        l3.close()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "attempts/ns", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (flat start)",
                 "config": {"workload": f"KPZ octahedron DTr, L={L}x{L}, p={args.p}, q={args.q}, flat start, "
-                                       f"1 MCS per step (BASELINE.json "
-                                       + ("configs[1])" if world == 1 else
-                                          "configs[2]'s strip-sharded L=2^17 lattice; p, q of the metric)"),
+                                       f"1 MCS per step (BASELINE.json configs[1]; the same lattice at every N: "
+                                       f"strong scaling)",
                            "plan": {"block_x": plan[0], "block_y": plan[1], "domain": "16x8", "sub_sweeps_per_mcs": sub},
                            "parallelism": mode,
                            "l2": f"lattice {L * L // 8 >> 20} MiB ({L * L // 8 // world >> 20} MiB per GPU) >> 126 MB L2: "
                                  f"no flush needed"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-                "gpu_launches": 4 * sub * args.steps, "kmc": kmc, "c3_single_gpu": c3}
+                "gpu_launches": 4 * sub * args.steps, "kmc": kmc, "c3": c3}
+        if world == 1:
+            line["c3_single_gpu"] = c3
         print(json.dumps(line), flush=True)
     if world == 1:
         k.close()

@@ -228,6 +228,34 @@ LFG_API int lfg_kpz_strip_width_rows(lfg_kpz* h, const void* rows, int32_t row_c
 LFG_API int lfg_kpz_width_combine(lfg_kpz* h, const void* H0, const void* P1, const void* D, const void* seg_len,
                                   int32_t nseg, int64_t* sum, int64_t* sum2_without_p2);
 
+/* ------------------------------------------------------------ sharded lattice (one process, N GPUs)
+ * BASELINE configs[2]: the lattice split into N y-strips, strip g on
+ * devices[g] (NULL: devices 0..N-1; a device may repeat), driven by ONE host
+ * thread: the caller of the reference's kpz_sweep_sequential / interface_width
+ * (kpz.hpp:119-120) gets the same lattice, bit for bit, as lfg_kpz_create's
+ * single-GPU handle.  Per sub-sweep the row ownership rolls
+ * with the DTr origin and the ghost rows are peer copies (NVLink); per phase the
+ * ghost row a neighbour needs is stored into its ring by the phase kernel's
+ * write-back and neighbouring strips are ordered by CUDA events.  L/N must be a
+ * multiple of 2 * block_y.  Error codes as the single-GPU calls. */
+typedef struct lfg_kpz_sharded lfg_kpz_sharded;
+LFG_API int lfg_kpz_create_sharded(lfg_kpz_sharded** h, int32_t L, double p, double q, uint64_t seed,
+                                   const lfg_kpz_plan* plan, int32_t n_shards, const int32_t* devices);
+LFG_API int lfg_kpz_sharded_destroy(lfg_kpz_sharded* h);
+/* make_flat_slopes (lattice.cpp:71-82) / a host SlopeField (closure-checked). */
+LFG_API int lfg_kpz_sharded_init_flat(lfg_kpz_sharded* h);
+LFG_API int lfg_kpz_sharded_upload(lfg_kpz_sharded* h, const uint64_t* x, const uint64_t* y, size_t nwords);
+LFG_API int lfg_kpz_sharded_download(lfg_kpz_sharded* h, uint64_t* x, uint64_t* y, size_t nwords);
+/* n_mcs DTr MCS over all strips; out: NULL or this call's counters. */
+LFG_API int lfg_kpz_sharded_sweep(lfg_kpz_sharded* h, int64_t n_mcs, lfg_counters* out);
+LFG_API int lfg_kpz_sharded_counters(lfg_kpz_sharded* h, lfg_counters* out);
+/* interface_width (kpz.cpp:62-81): exact int64 sums assembled from the strips. */
+LFG_API int lfg_kpz_sharded_width_sums(lfg_kpz_sharded* h, int64_t* sum, int64_t* sum2);
+LFG_API int lfg_kpz_sharded_interface_width(lfg_kpz_sharded* h, double* w2);
+/* Next MCS index (set before init_flat / upload). */
+LFG_API int lfg_kpz_sharded_set_sweep_index(lfg_kpz_sharded* h, uint64_t sweep);
+LFG_API int lfg_kpz_sharded_get_sweep_index(const lfg_kpz_sharded* h, uint64_t* sweep);
+
 /* ------------------------------------------------------------ peer memory
  * Single-node shard exchange without a collective library (one process per
  * GPU; NVLink peer access through CUDA IPC).  Handles are 64 opaque bytes. */

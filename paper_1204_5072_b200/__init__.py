@@ -20,7 +20,7 @@ from . import _native
 from ._native import (ClosureError, Counters, CudaError, DeviceOutOfMemory, DomainError,  # noqa: F401
                       InvalidArgument, KmcPlan, KpzPlan, LfgError, TransportError, check, device_count)
 
-__all__ = ["KpzLattice", "KmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
+__all__ = ["KpzLattice", "ShardedKpzLattice", "KmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
            "DomainError", "CudaError", "device_count", "words2", "words3", "interface_width",
            "width_sums", "reconstruct_heights", "open_bond_sums", "open_bonds_per_particle"]
 
@@ -263,6 +263,86 @@ class KpzLattice:
         p, n = C.c_void_p(), C.c_size_t()
         check(_native.lib().lfg_kpz_device_spins(self._h, replica, C.byref(p), C.byref(n)))
         return int(p.value or 0), int(n.value)
+
+
+class ShardedKpzLattice:
+    """BASELINE configs[2]: one lattice split into y-strips over several GPUs, driven by
+    this one process through the C ABI (lfg_kpz_create_sharded).  Same trajectory, bit
+    for bit, as KpzLattice with the same L, p, q, seed and plan.  ``devices``: one CUDA
+    device per strip (may repeat, e.g. [0, 0] for two strips on one GPU)."""
+
+    def __init__(self, L: int, p: float = 1.0, q: float = 0.0, seed: int = 1, *, devices=(0, 1),
+                 block_x: int = 0, block_y: int = 0, sub: int = 0):
+        self._h = None
+        devs = [int(d) for d in devices]
+        arr = (C.c_int32 * len(devs))(*devs)
+        plan = KpzPlan(block_x, block_y, sub)
+        h = C.c_void_p()
+        check(_native.lib().lfg_kpz_create_sharded(C.byref(h), L, float(p), float(q), int(seed), C.byref(plan),
+                                                   len(devs), arr))
+        self._h, self.L, self.devices = h, int(L), devs
+
+    def close(self) -> None:
+        if self._h is not None:
+            _native.lib().lfg_kpz_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def make_flat_slopes(self) -> "ShardedKpzLattice":
+        check(_native.lib().lfg_kpz_sharded_init_flat(self._h))
+        return self
+
+    def upload(self, x, y) -> None:
+        x, y = _u64(x), _u64(y)
+        check(_native.lib().lfg_kpz_sharded_upload(self._h, x.ctypes.data, y.ctypes.data, x.size))
+
+    def download(self):
+        n = words2(self.L)
+        x = np.empty(n, np.uint64)
+        y = np.empty(n, np.uint64)
+        check(_native.lib().lfg_kpz_sharded_download(self._h, x.ctypes.data, y.ctypes.data, n))
+        return x, y
+
+    def sweep(self, sweeps: int = 1) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kpz_sharded_sweep(self._h, int(sweeps), C.byref(c)))
+        return c
+
+    def counters(self) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kpz_sharded_counters(self._h, C.byref(c)))
+        return c
+
+    def width_sums(self):
+        s, s2 = C.c_int64(), C.c_int64()
+        check(_native.lib().lfg_kpz_sharded_width_sums(self._h, C.byref(s), C.byref(s2)))
+        return int(s.value), int(s2.value)
+
+    def interface_width(self) -> float:
+        w = C.c_double()
+        check(_native.lib().lfg_kpz_sharded_interface_width(self._h, C.byref(w)))
+        return float(w.value)
+
+    @property
+    def sweep_index(self) -> int:
+        v = C.c_uint64()
+        check(_native.lib().lfg_kpz_sharded_get_sweep_index(self._h, C.byref(v)))
+        return int(v.value)
+
+    @sweep_index.setter
+    def sweep_index(self, v: int) -> None:
+        check(_native.lib().lfg_kpz_sharded_set_sweep_index(self._h, int(v)))
 
 
 class KmcLattice:

@@ -140,6 +140,18 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_strip_width_partials", P, P, I32, I32, I32, I32, P, P, P)
     _sig(L, "lfg_kpz_width_combine", P, P, P, P, P, I32, C.POINTER(I64), C.POINTER(I64))
     _sig(L, "lfg_kpz_strip_width_rows", P, P, I32, I32, I32, C.POINTER(I64))
+    # sharded lattice: one process, N GPUs (include/lfg.h)
+    _sig(L, "lfg_kpz_create_sharded", C.POINTER(P), I32, D, D, U64, C.POINTER(KpzPlan), I32, C.POINTER(I32))
+    _sig(L, "lfg_kpz_sharded_destroy", P)
+    _sig(L, "lfg_kpz_sharded_init_flat", P)
+    _sig(L, "lfg_kpz_sharded_upload", P, P, P, C.c_size_t)
+    _sig(L, "lfg_kpz_sharded_download", P, P, P, C.c_size_t)
+    _sig(L, "lfg_kpz_sharded_sweep", P, C.c_int64, C.POINTER(Counters))
+    _sig(L, "lfg_kpz_sharded_counters", P, C.POINTER(Counters))
+    _sig(L, "lfg_kpz_sharded_width_sums", P, C.POINTER(I64), C.POINTER(I64))
+    _sig(L, "lfg_kpz_sharded_interface_width", P, C.POINTER(D))
+    _sig(L, "lfg_kpz_sharded_set_sweep_index", P, U64)
+    _sig(L, "lfg_kpz_sharded_get_sweep_index", P, C.POINTER(U64))
     _sig(L, "lfg_kpz_set_abort_flag", P, P)
     # readouts of host lattices (no handle)
     _sig(L, "lfg_kpz_width_sums_host", I32, I32, P, P, SZ, C.POINTER(I64), C.POINTER(I64))

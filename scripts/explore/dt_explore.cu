@@ -197,6 +197,14 @@ __global__ void dt_kernel(Cfg c, int8_t* gH, double* w2, double* hm) {
                         n = int(lrint(mean_n + sh + sg * g));
                         if (c.counts == 3) n = min(n, int(lrint(mean_n + sh + k * sg)));
                         n = max(0, min(n, 2047));
+                    } else if (c.counts == 7) {
+                        // generic Poisson law: N = tc - td K, K ~ Poisson((tc - mu) / td) by inversion
+                        const double lam = (c.tc - mean_n) / c.td;
+                        const double u = curand_uniform_double(&st);
+                        double pk = exp(-lam), cdf = pk;
+                        int K = 0;
+                        while (u > cdf && K < 64) { ++K; pk *= lam / K; cdf += pk; }
+                        n = max(0, c.tc - c.td * K);
                     } else if (c.counts == 6) {
                         n = s_mn[a];
                     } else if (c.counts == 5) {

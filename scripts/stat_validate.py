@@ -53,7 +53,7 @@ def ref_run(args):
     return w2, hm
 
 
-def gpu_runs(L, p, q, seeds, ts, block_x, block_y):
+def gpu_runs(L, p, q, seeds, ts, block_x, block_y, sub=0):
     import paper_1204_5072_b200 as lfg
 
     w2 = np.zeros((len(seeds), len(ts)))
@@ -61,7 +61,7 @@ def gpu_runs(L, p, q, seeds, ts, block_x, block_y):
     chunk = 64
     for c0 in range(0, len(seeds), chunk):
         ss = seeds[c0:c0 + chunk]
-        with lfg.KpzLattice(L, p, q, seeds=ss, block_x=block_x, block_y=block_y) as k:
+        with lfg.KpzLattice(L, p, q, seeds=ss, block_x=block_x, block_y=block_y, sub=sub) as k:
             k.make_flat_slopes()
             t = 0
             for j, tt in enumerate(ts):
@@ -101,14 +101,18 @@ def main():
     ap.add_argument("--beta-lo", type=int, default=32)
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-ref", action="store_true")
+    ap.add_argument("--seed-base", type=int, default=0, help="offset of the GPU and reference seed sets")
+    ap.add_argument("--sub", type=int, default=0, help="DTr sub-sweeps per MCS (0: plan default 4; 1: paper)")
+    ap.add_argument("--ref-json", default=None,
+                    help="reuse the reference ensemble (t, ref means / SEs, ref_seeds) of an earlier report")
     ap.add_argument("--save-samples", action="store_true", help="store per-seed W^2(t) and <h>(t)")
     a = ap.parse_args()
     ts = sample_times(a.t)
-    seeds = [1000003 * (i + 1) for i in range(a.seeds)]
+    seeds = [1000003 * (i + 1) + a.seed_base for i in range(a.seeds)]
     t0 = time.time()
-    gw, gh = gpu_runs(a.L, a.p, a.q, seeds, ts, a.block_x, a.block_y)
+    gw, gh = gpu_runs(a.L, a.p, a.q, seeds, ts, a.block_x, a.block_y, a.sub)
     tg = time.time() - t0
-    rep = {"L": a.L, "p": a.p, "q": a.q, "t": ts, "gpu_seeds": a.seeds, "gpu_seconds": tg,
+    rep = {"L": a.L, "p": a.p, "q": a.q, "t": ts, "gpu_seeds": a.seeds, "gpu_seconds": tg, "sub": a.sub or 4,
            "gpu": {"w2_mean": gw.mean(0).tolist(), "w2_se": (gw.std(0, ddof=1) / math.sqrt(len(seeds))).tolist(),
                    "h_mean": gh.mean(0).tolist(), "h_se": (gh.std(0, ddof=1) / math.sqrt(len(seeds))).tolist()}}
     if a.save_samples:
@@ -121,11 +125,31 @@ def main():
                        "gpu": beta_fit(ts, gw.mean(0), lo, hi),
                        "gpu_per_seed_mean": float(sg.mean()) if len(sg) else None,
                        "gpu_per_seed_se": float(sg.std(ddof=1) / math.sqrt(len(sg))) if len(sg) > 1 else None}
-    if not a.no_ref:
+    if a.ref_json:
+        with open(a.ref_json) as f:
+            old = json.load(f)
+        assert old["t"] == ts and old["L"] == a.L and old["p"] == a.p and old["q"] == a.q, "incompatible reference"
+        R = old["ref"]
+        rep["ref_seeds"] = old["ref_seeds"]
+        rep["ref_source"] = a.ref_json
+        rep["ref"] = R
+        g = rep["gpu"]
+        zw = (np.array(g["w2_mean"]) - np.array(R["w2_mean"])) / np.hypot(g["w2_se"], R["w2_se"])
+        rep["z_w2"] = zw.tolist()
+        rep["max_abs_z_w2"] = float(np.max(np.abs(zw)))
+        if "h_mean" in R:
+            zh = (np.array(g["h_mean"]) - np.array(R["h_mean"])) / np.hypot(g["h_se"], R["h_se"])
+            rep["z_h"] = zh.tolist()
+            rep["max_abs_z_h"] = float(np.max(np.abs(zh)))
+        lo, hi = a.beta_lo, a.t
+        rep["beta"] = {"window": [lo, hi], "estimator": "slope of log <W^2> vs log t, /2",
+                       "gpu": beta_fit(ts, gw.mean(0), lo, hi), "ref": beta_fit(ts, R["w2_mean"], lo, hi)}
+        rep["beta"]["diff"] = rep["beta"]["gpu"] - rep["beta"]["ref"]
+    elif not a.no_ref:
         nref = a.ref_seeds or a.seeds
         t0 = time.time()
         with ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:
-            res = list(ex.map(ref_run, [(a.L, a.p, a.q, 7 * i + 1, ts) for i in range(nref)]))
+            res = list(ex.map(ref_run, [(a.L, a.p, a.q, 7 * i + 1 + a.seed_base, ts) for i in range(nref)]))
         tr = time.time() - t0
         rw = np.array([r[0] for r in res])
         rh = np.array([r[1] for r in res]) if a.q == 0.0 else None

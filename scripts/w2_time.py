@@ -2,7 +2,10 @@
 with CUDA events on the handle's stream; print JSON.  Usage: python scripts/w2_time.py [L] [reps]"""
 import ctypes as C
 import json
+import os
 import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np
 import torch
