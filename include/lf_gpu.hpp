@@ -79,6 +79,10 @@ struct DtrPlan {
     std::int32_t block_x = 0, block_y = 0;  // KPZ device block (0 = auto)
     std::int32_t sub = 0;                   // KPZ sub-sweeps per MCS (0 = 4; 1 = the paper's scheme)
     std::int32_t block = 0;                 // KMC device block edge (0 = auto)
+    // KPZ over several GPUs from this one thread (lfg_kpz_create_sharded, y-strips):
+    // devices 0..n_gpus-1, or the explicit list `devices` (a device may repeat).
+    std::int32_t n_gpus = 1;
+    std::vector<std::int32_t> devices;
 };
 
 template <class Rng>
@@ -90,61 +94,86 @@ std::uint64_t key_from(Rng& rng) {
 // ------------------------------------------------------------------ KPZ
 class KpzDevice {
 public:
+    // plan.n_gpus > 1 or plan.devices with > 1 entry: the lattice is split into
+    // y-strips over those GPUs (BASELINE configs[2]), same trajectory bit for bit.
     KpzDevice(std::int32_t L, double p, double q, std::uint64_t seed, const DtrPlan& plan = {}, int device = 0) {
         lfg_kpz_plan pl{plan.block_x, plan.block_y, plan.sub};
-        check(lfg_kpz_create(&h_, L, p, q, seed, &pl, device));
+        std::vector<std::int32_t> devs = plan.devices;
+        if (devs.empty())
+            for (std::int32_t g = 0; g < plan.n_gpus; ++g) devs.push_back(plan.n_gpus > 1 ? g : device);
+        if (devs.size() > 1) check(lfg_kpz_create_sharded(&s_, L, p, q, seed, &pl, std::int32_t(devs.size()), devs.data()));
+        else check(lfg_kpz_create(&h_, L, p, q, seed, &pl, devs[0]));
         L_ = L;
     }
     KpzDevice(const KpzDevice&) = delete;
     KpzDevice& operator=(const KpzDevice&) = delete;
-    ~KpzDevice() { lfg_kpz_destroy(h_); }
+    ~KpzDevice() {
+        if (h_) lfg_kpz_destroy(h_);
+        if (s_) lfg_kpz_sharded_destroy(s_);
+    }
 
     std::int32_t size() const { return L_; }
-    void make_flat_slopes() { check(lfg_kpz_init_flat(h_)); }
+    bool sharded() const { return s_ != nullptr; }
+    void make_flat_slopes() { check(s_ ? lfg_kpz_sharded_init_flat(s_) : lfg_kpz_init_flat(h_)); }
 
     template <class Field>
     void upload(const Field& f) {
         if (f.size() != L_) throw std::invalid_argument("KpzDevice: lattice size mismatch");
-        check(lfg_kpz_upload(h_, 0, f.words_x(), f.words_y(), nwords()));
+        check(s_ ? lfg_kpz_sharded_upload(s_, f.words_x(), f.words_y(), nwords())
+                 : lfg_kpz_upload(h_, 0, f.words_x(), f.words_y(), nwords()));
     }
     template <class Field>
     void download(Field& f) const {
         if (f.size() != L_) throw std::invalid_argument("KpzDevice: lattice size mismatch");
-        check(lfg_kpz_download(h_, 0, f.words_x(), f.words_y(), nwords()));
+        check(s_ ? lfg_kpz_sharded_download(s_, f.words_x(), f.words_y(), nwords())
+                 : lfg_kpz_download(h_, 0, f.words_x(), f.words_y(), nwords()));
     }
 
     Counters sweep(int sweeps = 1) {
         lfg_counters c{};
-        check(lfg_kpz_sweep(h_, sweeps, &c));
+        check(s_ ? lfg_kpz_sharded_sweep(s_, sweeps, &c) : lfg_kpz_sweep(h_, sweeps, &c));
         return Counters{c.attempts, c.successes};
     }
     lfg_counters counters_detail() {
         lfg_counters c{};
-        check(lfg_kpz_counters(h_, 0, &c));
+        check(s_ ? lfg_kpz_sharded_counters(s_, &c) : lfg_kpz_counters(h_, 0, &c));
         return c;
     }
     double interface_width() {
         double w = 0;
-        check(lfg_kpz_interface_width(h_, 0, &w));
+        check(s_ ? lfg_kpz_sharded_interface_width(s_, &w) : lfg_kpz_interface_width(h_, 0, &w));
         return w;
     }
     std::vector<std::int32_t> reconstruct_heights() {
         std::vector<std::int32_t> out(std::size_t(L_) * std::size_t(L_));
-        check(lfg_kpz_heights(h_, 0, out.data(), out.size()));
+        if (s_) {  // through the slope planes (the readout checks closure like kpz.cpp:35-47)
+            std::vector<std::uint64_t> x(nwords()), y(nwords());
+            check(lfg_kpz_sharded_download(s_, x.data(), y.data(), nwords()));
+            check(lfg_kpz_heights_host(0, L_, x.data(), y.data(), nwords(), out.data(), out.size()));
+        } else {
+            check(lfg_kpz_heights(h_, 0, out.data(), out.size()));
+        }
         return out;
     }
-    void set_params(double p, double q) { check(lfg_kpz_set_params(h_, p, q)); }
+    void set_params(double p, double q) {
+        if (s_) throw std::invalid_argument("KpzDevice: set_params on a sharded lattice is not supported");
+        check(lfg_kpz_set_params(h_, p, q));
+    }
     std::uint64_t sweep_index() const {
         std::uint64_t s = 0;
-        check(lfg_kpz_get_sweep_index(h_, &s));
+        check(s_ ? lfg_kpz_sharded_get_sweep_index(s_, &s) : lfg_kpz_get_sweep_index(h_, &s));
         return s;
     }
-    void set_sweep_index(std::uint64_t s) { check(lfg_kpz_set_sweep_index(h_, s)); }
+    void set_sweep_index(std::uint64_t s) {
+        check(s_ ? lfg_kpz_sharded_set_sweep_index(s_, s) : lfg_kpz_set_sweep_index(h_, s));
+    }
     lfg_kpz* handle() { return h_; }
+    lfg_kpz_sharded* sharded_handle() { return s_; }
 
 private:
     std::size_t nwords() const { return std::size_t(L_) * std::size_t(L_) / 64; }
     lfg_kpz* h_ = nullptr;
+    lfg_kpz_sharded* s_ = nullptr;
     std::int32_t L_ = 0;
 };
 

@@ -19,7 +19,8 @@ s1 = subprocess.run([sys.executable, os.path.join(here, "ncu_summary.py"), rep],
 s2 = subprocess.run([sys.executable, os.path.join(here, "ncu_insts.py"), rep], capture_output=True, text=True).stdout
 out = os.path.join(ROOT, "profiles", f"{tag}_kpz_ncu.txt")
 with open(out, "w") as f:
-    f.write(f"# ncu --set full --clock-control none, one kpz_dtr_phase_kernel launch (L=65536, p=1 q=0)\n")
+    f.write(f"# ncu --set full --clock-control none, one kpz_dtr_phase_kernel launch (L=65536, p=1 q=0, "
+            f"default plan 1024x128, sub=4)\n")
     f.write(f"# source report: {os.path.relpath(rep, ROOT)} (not committed; regenerate with scripts/ncu_kpz.sh)\n\n")
     f.write(s1 + "\n# instruction groups by execution count\n" + s2)
 vals = {}
@@ -27,6 +28,9 @@ for ln in s1.splitlines():
     parts = ln.split()
     if len(parts) >= 2:
         vals[parts[0]] = parts[1]
+        if parts[0] == "gpu__time_duration.sum" and len(parts) > 2:  # -> ms
+            scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(parts[2], 1.0)
+            vals[parts[0]] = str(float(parts[1]) * scale)
 summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
 summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
 mb = 1e6
@@ -39,7 +43,12 @@ try:
                              "issue_active_pct": float(vals["sm__issue_active.avg.pct_of_peak_sustained_elapsed"]),
                              "alu_pipe_pct": float(vals["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"]),
                              "smem_wavefront_pct": float(vals["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]),
-                             "note": "one launch = one DT phase = L^2/4 attempts"}
+                             "sub": int(os.environ.get("LFG_PROFILE_SUB", "4")),
+                             "note": "one launch = one DT phase of a sub-sweep = L^2/(4 sub) attempts on average"}
+    k = summ["kpz_dtr_phase"]
+    dram_pct = 100.0 * (rd + wr) / (k["duration_ms"] * 1e-3) / 7.7e12 if k["duration_ms"] else 0.0
+    k["binding"] = (f"SM issue / ALU pipe (profiles/{tag}_kpz_ncu.txt: issue {k['issue_active_pct']:.0f}%, "
+                    f"ALU {k['alu_pipe_pct']:.0f}%, DRAM {dram_pct:.0f}% of 7.7 TB/s)")
 except KeyError as e:
     print("missing", e)
 json.dump(summ, open(summ_path, "w"), indent=1)

@@ -8,6 +8,7 @@
 // CPU functions.  Without it, minimal stand-in types are used.  Exit 0 = pass.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 #include <vector>
 
@@ -140,6 +141,30 @@ int main() {
     REQUIRE(kc.attempts == 2LL * 64 * 64 * 64 / 2);
     REQUIRE(ob0 > 0.0);
 #endif
+    {   // configs[2] through the C++ API: the same lattice on 1 GPU and split into 2 strips
+        // (lfg_kpz_create_sharded; both strips on device 0 of the test box) -> identical.
+        const int32_t Ls = 2048;
+        lf::gpu::DtrPlan two;
+        two.devices = {0, 0};
+        lf::gpu::KpzDevice one_gpu(Ls, 0.95, 0.05, 4242), strips(Ls, 0.95, 0.05, 4242, two);
+        REQUIRE(strips.sharded() && !one_gpu.sharded());
+        one_gpu.make_flat_slopes();
+        strips.make_flat_slopes();
+        const auto c1 = one_gpu.sweep(2);
+        const auto c2 = strips.sweep(2);
+        REQUIRE(c1.attempts == c2.attempts && c1.successes == c2.successes);
+#ifdef LF_WITH_REFERENCE
+        lf::SlopeField f1(Ls), f2(Ls);
+#else
+        SlopeField f1(Ls), f2(Ls);
+#endif
+        one_gpu.download(f1);
+        strips.download(f2);
+        REQUIRE(std::memcmp(f1.words_x(), f2.words_x(), size_t(Ls) * Ls / 8) == 0);
+        REQUIRE(std::memcmp(f1.words_y(), f2.words_y(), size_t(Ls) * Ls / 8) == 0);
+        REQUIRE(one_gpu.interface_width() == strips.interface_width());
+        std::printf("sharded OK: 2 strips == 1 lattice, successes=%lld\n", (long long)c2.successes);
+    }
     std::printf("dropin OK: KPZ W2=%.6f successes=%lld; KMC exchanges=%lld\n", w2, (long long)c.successes,
                 (long long)kc.successes);
     return 0;
