@@ -97,6 +97,15 @@ LFG_API int lfg_kmc_slab_open_bond_sums(lfg_kmc* h, const void* planes, int32_t 
 /* Abort flag of the slab step barrier (see lfg_kpz_set_abort_flag). */
 LFG_API int lfg_kmc_set_abort_flag(lfg_kmc* h, const void* dev_flag);
 
+/* Debug instrumentation for the write-disjointness check (the
+ * reference's WriteLog, write_log.hpp:10-60; KMC write hooks kmc.hpp:105-110):
+ * while enabled (dev_buf != NULL, >= L^3 device words, 16^3 block plan), every
+ * sweep writes, per phase k at offset k * L^3/8 words, [256 rounds][active
+ * blocks][8 tiles][2] uint32: the two simple-cubic site indices (z L + y) L + x
+ * an exchange writes, or 0xFFFFFFFF twice for an attempt that did not
+ * exchange.  Block order within a round = launch order (x fastest). */
+LFG_API int lfg_kmc_debug_record_writes(lfg_kmc* h, void* dev_buf, size_t capacity_words);
+
 #ifdef __cplusplus
 }
 #endif

@@ -344,17 +344,26 @@ int64_t kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, ui
                 for (int32_t tx = 0; tx < tb; ++tx) {
                     const int32_t gx = bxi * tb + tx, gy = byi * tb + ty, gz = bzi * tb + tz;
                     const uint32_t tile_id = (uint32_t(gz) * uint32_t(tl) + uint32_t(gy)) * uint32_t(tl) + uint32_t(gx);
+                    // One Philox draw serves the tile's rounds 2m and 2m + 1:
+                    //   even: site bits W0[0..5), direction word W1, acceptance word W2
+                    //   odd:  site bits W0[5..10), direction from W0[10..32) (22 bits;
+                    //         below(W0 & ~1023, 12) = floor(W0[10..32) * 12 / 2^22)),
+                    //         acceptance word W3
                     uint32_t w[4];
-                    draw(seed, sweep, TAG_KMC_SITE, tile_id, uint32_t(r), w);
+                    draw(seed, sweep, TAG_KMC_SITE, tile_id, uint32_t(r >> 1), w);
+                    const bool odd = (r & 1) != 0;
+                    const uint32_t s5 = odd ? (w[0] >> 5) & 31u : w[0] & 31u;
+                    const uint32_t dword = odd ? (w[0] & ~1023u) : w[1];
+                    const uint32_t aword = odd ? w[3] : w[2];
                     const int32_t x0 = d.ox + kKmcTile * gx + kKmcDom * hx;
                     const int32_t y0 = d.oy + kKmcTile * gy + kKmcDom * hy;
                     const int32_t z0 = d.oz + kKmcTile * gz + kKmcDom * hz;
-                    const int32_t x = (x0 + int32_t(w[0] & 3u)) & mask;
-                    const int32_t y = (y0 + int32_t((w[0] >> 2) & 3u)) & mask;
+                    const int32_t x = (x0 + int32_t(s5 & 3u)) & mask;
+                    const int32_t y = (y0 + int32_t((s5 >> 2) & 3u)) & mask;
                     const int32_t t = (x ^ y) & 1;
                     const int32_t zfirst = z0 + (((z0 & 1) == t) ? 0 : 1);
-                    const int32_t z = (zfirst + 2 * int32_t((w[0] >> 4) & 1u)) & mask;
-                    acc.dep += attempt(x, y, z, w[1], w[2]) == 0;
+                    const int32_t z = (zfirst + 2 * int32_t((s5 >> 4) & 1u)) & mask;
+                    acc.dep += attempt(x, y, z, dword, aword) == 0;
                 }
             }
         }

@@ -187,6 +187,7 @@ def _bind_kmc(L) -> None:
     _sig(L, "lfg_kmc_set_seed", P, U64)
     _sig(L, "lfg_kmc_set_stream", P, P)
     _sig(L, "lfg_kmc_set_concurrency", P, I32)
+    _sig(L, "lfg_kmc_debug_record_writes", P, P, C.c_size_t)
     _sig(L, "lfg_kmc_set_abort_flag", P, P)
     _sig(L, "lfg_kmc_synchronize", P)
     _sig(L, "lfg_kmc_device_words", P, C.POINTER(P), C.POINTER(SZ))

@@ -30,6 +30,7 @@ struct lfg_kmc {
     unsigned long long* hpin = nullptr; // pinned [2]
     int64_t attempts = 0;
     const uint32_t* abort_flag = nullptr;  // slab step-barrier abort flag (lfg_kmc_set_abort_flag)
+    uint32_t* wlog = nullptr;           // debug write-set records (lfg_kmc_debug_record_writes) or nullptr
     uint64_t thr[13] = {};
     bool slab_only = false;             // created by lfg_kmc_create_slab: no resident lattice
     int32_t share = 1;                  // lfg_kmc_set_concurrency
@@ -94,6 +95,8 @@ void enqueue(lfg_kmc* h, int64_t n) {
         a.sweep = h->sweep + uint64_t(s);
         for (int k = 0; k < 8; ++k) {
             a.phase = k;
+            // one MCS of records: phase k at k * (L^3/2 attempts / 8) * 2 words
+            a.wlog = h->wlog ? h->wlog + size_t(k) * (size_t(h->L) * h->L * h->L / 8) : nullptr;
             cuda_check(kmc_launch_phase(a, h->stream), "kmc_dt_phase launch");
         }
     }
@@ -445,6 +448,22 @@ int lfg_kmc_set_stream(lfg_kmc* h, void* stream) {
         if (h->own_stream) cudaStreamDestroy(h->stream);
         h->own_stream = false;
         h->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int lfg_kmc_debug_record_writes(lfg_kmc* h, void* dev_buf, size_t capacity_words) {
+    return guarded([&] {
+        check_handle(h);
+        if (!dev_buf) {
+            h->wlog = nullptr;
+            return;
+        }
+        if (h->slab_only) throw Error(LFG_EINVAL, "debug_record_writes: resident lattices only");
+        if (h->bk != 16) throw Error(LFG_EINVAL, "debug_record_writes: needs the 16^3 block plan (the default)");
+        const size_t need = size_t(h->L) * h->L * h->L;  // L^3/2 attempts x 2 words
+        if (capacity_words < need)
+            throw Error(LFG_EINVAL, "debug_record_writes: buffer must hold L^3 words (one MCS of records)");
+        h->wlog = static_cast<uint32_t*>(dev_buf);
     });
 }
 

@@ -47,6 +47,7 @@ struct lfg_kpz {
     uint32_t* fnew = nullptr;               // [L][L/32]
     unsigned long long* dmis = nullptr;     // mismatch counter
     int32_t* H0 = nullptr;                  // [L]
+    void* wscr = nullptr;                   // W^2 row-pass scratch (kpz_width_scratch_bytes(L))
     int32_t* P1 = nullptr;                  // [G][L]
     int32_t* Dd = nullptr;                  // [G][L]
     int32_t* seglen = nullptr;              // [G]
@@ -144,6 +145,7 @@ void ensure_slope_scratch(lfg_kpz* h) {
 void ensure_width_scratch(lfg_kpz* h) {
     if (!h->H0) h->H0 = dmalloc<int32_t>(size_t(h->L), "alloc width scratch");
     if (!h->wout) h->wout = dmalloc<unsigned long long>(3, "alloc width scratch");
+    if (!h->wscr) h->wscr = dmalloc<uint8_t>(kpz_width_scratch_bytes(h->L), "alloc width scratch");
 }
 
 void sync(lfg_kpz* h) { cuda_check(cudaStreamSynchronize(h->stream), "kernel execution"); }
@@ -155,7 +157,7 @@ void enqueue_width(lfg_kpz* h, int32_t r, unsigned long long* out3) {
     ensure_width_scratch(h);
     if (!out3) out3 = h->wout;
     cuda_check(cudaMemsetAsync(out3, 0, 24, h->stream), "memset");
-    cuda_check(kpz_launch_width_rows(h->rep(r), h->L, h->L - 1, 0, h->L, h->H0, out3, h->stream), "width scan");
+    cuda_check(kpz_launch_width_rows(h->rep(r), h->L, h->L - 1, 0, h->L, h->wscr, out3, h->stream), "width scan");
     cuda_check(cudaMemsetAsync(out3 + 2, 0, 8, h->stream), "memset");
 }
 
@@ -307,6 +309,7 @@ int lfg_kpz_destroy(lfg_kpz* h) {
         dfree(h->fnew);
         dfree(h->dmis);
         dfree(h->H0);
+        dfree(h->wscr);
         dfree(h->P1);
         dfree(h->Dd);
         dfree(h->wout);
@@ -811,7 +814,7 @@ int lfg_kpz_strip_width_rows(lfg_kpz* h, const void* rows, int32_t cap, int32_t 
         ensure_width_scratch(h);
         cuda_check(cudaMemsetAsync(h->wout, 0, 24, h->stream), "memset");
         cuda_check(kpz_launch_width_rows(static_cast<const uint32_t*>(rows), h->L, cap - 1, row_begin, row_count,
-                                         h->H0, h->wout, h->stream),
+                                         h->wscr, h->wout, h->stream),
                    "width rows");
         cuda_check(cudaMemcpyAsync(h->hpin, h->wout, 24, cudaMemcpyDeviceToHost, h->stream), "readback");
         sync(h);

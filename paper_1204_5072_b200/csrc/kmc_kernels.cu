@@ -126,20 +126,22 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;  // parity offset of the block frame
     uint32_t nsucc = 0;
     U4 V = {0, 0, 0, 0};
-    U4 Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
+    U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u), Wn = W;  // one draw per two rounds
 #pragma unroll 1
     for (int r = 0; r < kKmcRounds; ++r) {
-        const U4 W = Wn;
+        const bool odd = (r & 1) != 0;
         if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
-        Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r + 1));  // next round (unused after the last)
+        if (odd) Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t((r >> 1) + 1));  // next pair
+        uint32_t s5, dirw, accw;
+        kmc_round_words(W, odd, s5, dirw, accw);
         const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
         const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
         // KmcKernel::draw_site (kmc.hpp:154-171) over the domain box: x, y
         // uniform, z uniform over the two planes of matching parity.
-        const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
+        const int lx = lx0 + int(s5 & 3u), ly = ly0 + int((s5 >> 2) & 3u);
         const int tpar = (lx ^ ly ^ lz0 ^ zpar0) & 1;  // 1 iff plane lz0 has the wrong parity
-        const int lz = lz0 + tpar + 2 * int((W.x >> 4) & 1u);
-        const int dir = int(below(W.y, 12));
+        const int lz = lz0 + tpar + 2 * int((s5 >> 4) & 1u);
+        const int dir = int(dirw);
         int dx, dy, dz;
         fcc_offset(dir, dx, dy, dz);
         const int px = lx + dx, py = ly + dy, pz = lz + dz;
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
         if ((BOTH || here) && pb != here) {
             // n_i (B site, its A partner excluded: no B there), n_f (A site, its B partner excluded)
             const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
-            const bool acc = d <= 0 || uint64_t(W.z) < s_thr[d];
+            const bool acc = d <= 0 || uint64_t(accw) < s_thr[d];
             if (acc) {
                 atomicXor(R.ptr(ly, lz), 1ull << (lx + 16));
                 atomicXor(R.ptr(py, pz), 1ull << (px + 16));
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
                 ++nsucc;
             }
         }
+        if (odd) W = Wn;
         if (WARP_SYNC) __syncwarp();
         else __syncthreads();
     }
@@ -234,7 +237,7 @@ __device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, 
     }
 }
 
-template <bool BOTH>
+template <bool BOTH, bool WLOG = false>
 __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
     if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     extern __shared__ __align__(16) uint32_t sk16[];
@@ -267,18 +270,15 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;
     uint32_t nsucc = 0;
     U4 V = {0, 0, 0, 0};
-    U4 Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
-#pragma unroll 1
-    for (int r = 0; r < kKmcRounds; ++r) {
-        const U4 W = Wn;
-        if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
+    // One round; (s5, dirw, accw) are its kmc_round_words, static per parity.
+    auto round = [&](int r, uint32_t s5, uint32_t dirw, uint32_t accw) {
         const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
         const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
         // KmcKernel::draw_site (kmc.hpp:154-171) over the domain box.
-        const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
-        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((W.x >> 4) & 1u);
+        const int lx = lx0 + int(s5 & 3u), ly = ly0 + int((s5 >> 2) & 3u);
+        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((s5 >> 4) & 1u);
         int dx, dy, dz;
-        fcc_offset(int(below(W.y, 12)), dx, dy, dz);
+        fcc_offset(int(dirw), dx, dy, dz);
         const int px = lx + dx, py = ly + dy, pz = lz + dz;
         const int sr = k16_row(ly, lz), pr = k16_row(py, pz);
         // every shared load of the attempt, issued before any use
@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         const uint32_t se[4] = {cur[sr - kK16E - 1], cur[sr + kK16E - 1], cur[sr - kK16E + 1], cur[sr + kK16E + 1]};
         const uint32_t pf[4] = {cur[pr - 1], cur[pr + 1], cur[pr - kK16E], cur[pr + kK16E]};
         const uint32_t pe[4] = {cur[pr - kK16E - 1], cur[pr + kK16E - 1], cur[pr - kK16E + 1], cur[pr + kK16E + 1]};
-        Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r + 1));  // next round, overlaps the loads
         const int here = int((own >> (lx + kK16Ofs)) & 1u), pb = int((par >> (px + kK16Ofs)) & 1u);
         const int n_site = k16_count(sf, se, lx), n_part = k16_count(pf, pe, px);
         // kmc_attempt_impl (kmc.hpp:84-111), branch-free: every lane loads its
@@ -295,11 +294,32 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         // possibly-empty mask, so the round has no divergent control flow.
         const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
         const int di = d < 0 ? 0 : d;  // d <= 12
-        const bool acc = (BOTH || here) && pb != here && uint64_t(W.z) < lds_u64(thr_sh + 8u * uint32_t(di));
+        const bool acc = (BOTH || here) && pb != here && uint64_t(accw) < lds_u64(thr_sh + 8u * uint32_t(di));
         atomicXor(cur + sr, acc ? 1u << (lx + kK16Ofs) : 0u);
         atomicXor(cur + pr, acc ? 1u << (px + kK16Ofs) : 0u);
         nsucc += acc ? 1u : 0u;
+        if (WLOG) {  // the two sites the exchange writes (global sc indices)
+            const size_t o = (size_t(r) * size_t(gridDim.x * (blockDim.x >> 3)) + size_t(blin)) * 16 + 2 * t;
+            const auto sidx = [&](int x, int y, int z) {
+                return uint32_t((size_t((Z0 + z) & Lm) * L + size_t((Y0 + y) & Lm)) * L + size_t((X0 + x) & Lm));
+            };
+            a.wlog[o] = acc ? sidx(lx, ly, lz) : 0xFFFFFFFFu;
+            a.wlog[o + 1] = acc ? sidx(px, py, pz) : 0xFFFFFFFFu;
+        }
         __syncwarp(wmask);
+    };
+    // Round pairs: one draw serves rounds 2m (W.x[0..5), W.y, W.z) and 2m + 1
+    // (W.x[5..10), W.x[10..32), W.w) -- lfg_common.cuh kmc_round_words; the
+    // next pair's draw is issued before the odd round (its latency hides there).
+    U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
+#pragma unroll 1
+    for (int m = 0; m < kKmcRounds / 2; ++m) {
+        const int r = 2 * m;
+        if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
+        round(r, W.x & 31u, below(W.y, 12), W.z);
+        const U4 Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(m + 1));  // unused after the last pair
+        round(r + 1, (W.x >> 5) & 31u, below(W.x & ~1023u, 12), W.w);
+        W = Wn;
     }
     // Write-back of the 1-ring-extended block: bits lx in [-1, 17) of rows
     // (ly, lz) in [-1, 17)^2, as XOR differences.
@@ -335,7 +355,7 @@ __device__ __forceinline__ int k16_count_at(const uint32_t (&f)[4], const uint32
            __popc(e[1] & m1) + __popc(e[2] & m1) + __popc(e[3] & m1);
 }
 
-template <bool BOTH>
+template <bool BOTH, bool WLOG = false>
 __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
     if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
     extern __shared__ __align__(16) uint32_t sk16[];
@@ -365,24 +385,26 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     U4 V = {0, 0, 0, 0};
     // This lane's attempt of batch bb: tile t, round 4 bb + j (KmcKernel::draw_site,
     // kmc.hpp:154-171), packed as rows (< 512) and bit positions (lx + 8, px + 8 in
-    // [7, 24]); accm bit d is the Metropolis verdict W.z < threshold(d) for every
+    // [7, 24]); accm bit d is the Metropolis verdict accw < threshold(d) for every
     // possible d (64-bit compare against the constant-bank thresholds), so a round
     // looks its d up in a register.
     auto prepare = [&](int bb, uint32_t& pack, uint32_t& accm) {
         if ((bb & 7) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(bb >> 3));
         const int r = 4 * bb + j;
-        const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r));
+        const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r >> 1));  // pair (r, r ^ 1)
+        uint32_t s5, dirw, accw;
+        kmc_round_words(W, (r & 1) != 0, s5, dirw, accw);
         const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
         const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1), lz0 = 8 * tz + 4 * (inner >> 2);
-        const int lx = lx0 + int(W.x & 3u), ly = ly0 + int((W.x >> 2) & 3u);
-        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((W.x >> 4) & 1u);
+        const int lx = lx0 + int(s5 & 3u), ly = ly0 + int((s5 >> 2) & 3u);
+        const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((s5 >> 4) & 1u);
         int dx, dy, dz;
-        fcc_offset(int(below(W.y, 12)), dx, dy, dz);
+        fcc_offset(int(dirw), dx, dy, dz);
         pack = uint32_t(k16_row(ly, lz)) | (uint32_t(k16_row(ly + dy, lz + dz)) << 9) |
                (uint32_t(lx + kK16Ofs) << 18) | (uint32_t(lx + dx + kK16Ofs) << 23);
         accm = 0;
 #pragma unroll
-        for (int dd = 0; dd < 13; ++dd) accm |= (a.thr_hi[dd] != 0u || W.z < a.thr_lo[dd]) ? 1u << dd : 0u;
+        for (int dd = 0; dd < 13; ++dd) accm |= (a.thr_hi[dd] != 0u || accw < a.thr_lo[dd]) ? 1u << dd : 0u;
     };
     uint32_t pk[4], am[4];
     auto exchange = [&](uint32_t pack, uint32_t accm) {  // round q of the batch comes from group q
@@ -427,6 +449,15 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
             atomicXor(cur + sr, acc ? 1u << bs : 0u);
             atomicXor(cur + pr, acc ? 1u << bp : 0u);
             nsucc += acc ? 1u : 0u;
+            if (WLOG && apply) {  // the two sites the exchange writes (global sc indices)
+                const size_t o = (size_t(4 * b + q) * size_t(gridDim.x) + size_t(blin)) * 16 + 2 * t;
+                const auto sidx = [&](int row, uint32_t bit) {
+                    const int ly = row % kK16E - 2, lz = row / kK16E - 2, lx = int(bit) - kK16Ofs;
+                    return uint32_t((size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * L + size_t((X0 + lx) & Lm));
+                };
+                a.wlog[o] = acc ? sidx(sr, bs) : 0xFFFFFFFFu;
+                a.wlog[o + 1] = acc ? sidx(pr, bp) : 0xFFFFFFFFu;
+            }
             __syncwarp();
         }
         exchange(pack_n, accm_n);
@@ -524,13 +555,22 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         if ((per == 1 && wide == 1) || wide == 2) {  // one block per full warp (see kmc_dt16w_phase_kernel)
             const dim3 gw = dim3(unsigned(active));
             const size_t smw = 2 * kK16Rows * sizeof(uint32_t);
+            if (a.wlog)
+                return launch_pdl(a.both ? kmc_dt16w_phase_kernel<true, true> : kmc_dt16w_phase_kernel<false, true>, gw,
+                                  dim3(32), smw, st, a);
             return launch_pdl(a.both ? kmc_dt16w_phase_kernel<true> : kmc_dt16w_phase_kernel<false>, gw, dim3(32), smw,
                               st, a);
         }
         // (no PDL here: with blocks filling the GPU, early-launched CTAs of the
         // next phase land unevenly on the SMs -- 48 vs 86 att/ns at 512^3)
-        if (a.both) kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
-        else kmc_dt16_phase_kernel<false><<<g16, b16, sm16, st>>>(a);
+        if (a.wlog) {
+            if (a.both) kmc_dt16_phase_kernel<true, true><<<g16, b16, sm16, st>>>(a);
+            else kmc_dt16_phase_kernel<false, true><<<g16, b16, sm16, st>>>(a);
+        } else if (a.both) {
+            kmc_dt16_phase_kernel<true><<<g16, b16, sm16, st>>>(a);
+        } else {
+            kmc_dt16_phase_kernel<false><<<g16, b16, sm16, st>>>(a);
+        }
         return cudaGetLastError();
     }
     const bool ws = bpc * tpb <= 32;

@@ -21,6 +21,11 @@ struct KmcPhaseArgs {
     int32_t bz0, nbz;              // block z-rows [bz0, bz0 + nbz) of the shifted frame (slabs)
     int32_t share;                 // lattices sharing the GPU at once (kernel choice; >= 1)
     const uint32_t* abort_flag;    // slab step-barrier abort flag (see KpzPhaseArgs), or nullptr
+    // Debug write-set recording (lfg_kmc_debug_record_writes; 16^3 plans): this
+    // phase's [256 rounds][active blocks][8 tiles][2] u32 -- the two sc site
+    // indices an exchange writes (kmc.hpp:105-110), 0xFFFFFFFF when the attempt
+    // did not exchange -- or nullptr.
+    uint32_t* wlog;
 };
 
 int kmc_blocks_per_cta(int bk);

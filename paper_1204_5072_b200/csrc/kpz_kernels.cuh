@@ -97,8 +97,9 @@ cudaError_t kpz_launch_fill_rows(uint32_t* f, int L, int rmask, int row_begin, i
 // rows [row_begin, +row_count) of a ring buffer (slot = row & rmask), heights
 // relative to the column-0 height of the row below the piece (0 at global row
 // 0).  out3[0] += sum h, out3[1] += sum h^2, out3[2] = net column-0 step of
-// the piece (as int64); V: int32[row_count] scratch.
-cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int32_t* V,
+// the piece (as int64); scratch: kpz_width_scratch_bytes(row_count) bytes.
+size_t kpz_width_scratch_bytes(int row_count);
+cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, void* scratch,
                                   unsigned long long* out3, cudaStream_t st);
 // Closure of two uploaded slope planes: plaquettes that do not close ->
 // *local_bad; row 0 / column 0 sums != 0 -> *global_bad (kpz.cpp:35-47).

@@ -9,7 +9,7 @@
 // move preserves every plaquette sum -- so the height of site (i, j) is the
 // same along any path inside [0, L)^2 from (0, 0): up column 0, then along
 // row j.  That order reads each row contiguously:
-//   V(j)   = sum_{k=1..j} s_y(0, k)                        (kpz_col0_steps_kernel)
+//   V(j)   = sum_{k=1..j} s_y(0, k)                        (kpz_width_tiles_kernel / kpz_width_chain_kernel)
 //   h(i,j) = V(j) + sum_{k=1..i} s_x(k, j)                 (kpz_width_rows_kernel)
 // and sum h, sum h^2 are exact int64, finished on the host as kpz.cpp:78-80.
 //
@@ -28,9 +28,12 @@
 
 namespace lfg {
 
-// Per-byte table entry: byte 0 = S2 (0..204), byte 1 = S1 (signed, -36..36),
-// byte 2 = D (signed, -8..8), for the 8 steps s_t = 2 b_t - 1 of the byte
-// (bit t = +1 step), prefix heights m_t = sum_{u <= t} s_u.
+// Per-byte table entry, three biased fields added as one packed word across a
+// lane's 16 bytes: bits 0..11 = S2 (0..204; 16 x 204 < 2^12), bits 12..22 =
+// S1 + 36 (0..72; 16 x 72 < 2^11), bits 23..31 = D + 8 (0..16; used per byte
+// only), for the 8 steps s_t = 2 b_t - 1
+// of the byte (bit t = +1 step) with prefix heights m_t = sum_{u <= t} s_u:
+// S1 = sum m_t, S2 = sum m_t^2, D = m_7.
 __device__ __forceinline__ uint32_t width_byte_entry(uint32_t v) {
     int m = 0, s1 = 0, s2 = 0;
 #pragma unroll
@@ -39,71 +42,25 @@ __device__ __forceinline__ uint32_t width_byte_entry(uint32_t v) {
         s1 += m;
         s2 += m * m;
     }
-    return uint32_t(s2) | (uint32_t(s1 & 0xFF) << 8) | (uint32_t(m & 0xFF) << 16);
+    return uint32_t(s2) | (uint32_t(s1 + 36) << 12) | (uint32_t(m + 8) << 23);
 }
 
-__device__ __forceinline__ int32_t prmt_s(uint32_t e, uint32_t sel) {
-    uint32_t r;
-    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(e), "r"(sel));
-    return int32_t(r);
-}
-
-// Column-0 heights of global rows row_begin + k (k < n), relative to the row
-// below the piece: V[k] = sum_{m <= k} s_y(0, row_begin + m), where the step
-// into global row 0 is 0 (interface_width anchors h(0, 0) = 0).  One CTA.
-// out_d (may be null): V[n-1], the piece's net column-0 step.
-__global__ void __launch_bounds__(1024) kpz_col0_steps_kernel(const uint32_t* __restrict__ f, int L, int rmask,
-                                                              int row_begin, int n, int32_t* __restrict__ V,
-                                                              long long* __restrict__ out_d) {
-    __shared__ int32_t wsum[32];
-    const int wpr = L >> 5, Lm = L - 1;
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int chunk = (n + 1023) / 1024;
-    const int k0 = t * chunk, k1 = min(n, k0 + chunk);
-    auto step = [&](int k) -> int32_t {
-        const int g = (row_begin + k) & Lm;
-        if (g == 0) return 0;
-        const uint32_t a = f[size_t(g & rmask) * wpr] & 1u;
-        const uint32_t b = f[size_t(((g - 1) & Lm) & rmask) * wpr] & 1u;
-        return a == b ? 1 : -1;
-    };
-    int32_t s = 0;
-    for (int k = k0; k < k1; ++k) s += step(k);
-    // block exclusive scan of s
-    int32_t inc = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= o) inc += v;
-    }
-    if (lane == 31) wsum[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        int32_t w = wsum[lane], wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-            if (lane >= o) wi += v;
-        }
-        wsum[lane] = wi - w;
-    }
-    __syncthreads();
-    int32_t acc = wsum[warp] + inc - s;
-    for (int k = k0; k < k1; ++k) {
-        acc += step(k);
-        V[k] = acc;
-    }
-    if (out_d && k1 == n && k0 < k1) *out_d = acc;
-    if (out_d && n == 0 && t == 0) *out_d = 0;
-}
-
-// Sum of heights and of squared heights over global rows row_begin + k (k < n),
-// heights relative to V (see kpz_col0_steps_kernel).  out2[0] += sum h,
-// out2[1] += sum h^2 (two's complement; exact as int64).
+// Row pass (kpz_width_rows_kernel): one warp per row, 128 words (4096 sites)
+// per step, one 16-byte load per lane.  A lane turns its words into s_x bits
+// and walks its 16 bytes with the running offset o (height before the byte,
+// relative to the lane's first site): with per-byte table entries (S1, S2, D),
+//   sum over the byte of (o + m_t)   = 8 o + S1
+//   sum over the byte of (o + m_t)^2 = 8 o^2 + 2 o S1 + S2,
+// so per byte it needs o, o^2 and o S1; the S1, S2 (and D) sums of the 16 bytes
+// are one packed add.  Tables: 32 bank-private copies (conflict-free random
+// reads).  A warp scan of the lanes' net steps gives their start heights.  Per
+// row the pass stores (sum h, sum h^2) relative to the row's column-0 height
+// and the column-0 step into the row (kpz_width_tiles_kernel / _chain_kernel chain
+// them: no serial column pass on the critical path).
 template <bool VEC>
 __global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __restrict__ f, int L, int rmask,
-                                                             int row_begin, int n, const int32_t* __restrict__ V,
-                                                             unsigned long long* __restrict__ out2) {
+                                                             int row_begin, int n, long long* __restrict__ rs,
+                                                             int32_t* __restrict__ rstep) {
     __shared__ uint32_t tab[256 * 32];  // entry v of lane l at word v * 32 + l (bank l)
     for (int v = threadIdx.x; v < 256; v += blockDim.x) {
         const uint32_t e = width_byte_entry(uint32_t(v));
@@ -114,14 +71,14 @@ __global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __r
     const int wpr = L >> 5, Lm = L - 1;
     const int lane = threadIdx.x & 31;
     const int wpb = int(blockDim.x >> 5);
-    long long s1 = 0, s2 = 0;
     // grid-stride over rows (the grid is sized to the resident CTAs, so each
     // CTA builds its table once)
     for (int k = int(blockIdx.x) * wpb + int(threadIdx.x >> 5); k < n; k += int(gridDim.x) * wpb) {
         const int g = (row_begin + k) & Lm;
         const uint32_t* __restrict__ row = f + size_t(g & rmask) * wpr;
-        int32_t base = V[k] - 1;   // site 0 enters as a +1 step from V - 1
-        uint32_t top = 0;          // bit 31 of the previous chunk's last word
+        int32_t base = -1;   // site 0 enters as a +1 step from -1: heights relative to h(0, g)
+        uint32_t top = 0;    // bit 31 of the previous chunk's last word
+        long long s1 = 0, s2 = 0;
         for (int c = 0; c < wpr; c += 128) {
             uint32_t F[4];
             int nw = 4;  // valid words of this lane (all four when VEC)
@@ -137,27 +94,34 @@ __global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __r
             const uint32_t prev_lane = __shfl_up_sync(0xFFFFFFFFu, F[3], 1);
             uint32_t prev = lane == 0 ? top : prev_lane;
             top = __shfl_sync(0xFFFFFFFFu, F[3], 31);
-            int32_t o = 0, a1 = 0, a2 = 0;
+            int32_t o = 0, so = 0, so2 = 0, sos1 = 0;
+            uint32_t pk = 0;   // packed sums of the byte entries
+            int32_t nb = 0;    // bytes summed (bias removal)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 uint32_t X = ~(F[u] ^ ((F[u] << 1) | (prev >> 31)));  // bit b: s_x of site b is +1
                 prev = F[u];
                 if (c == 0 && lane == 0 && u == 0) X |= 1u;
                 if (!VEC && u >= nw) continue;
+                nb += 4;
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
                     uint32_t v;
                     asm("prmt.b32 %0, %1, 0, %2;" : "=r"(v) : "r"(X), "r"(0x4440u + uint32_t(b)));
                     const uint32_t e = tab[(v << 5) + uint32_t(lane)];
-                    const int32_t S2 = prmt_s(e, 0x4440u);
-                    const int32_t S1 = prmt_s(e, 0x9991u);
-                    const int32_t D = prmt_s(e, 0xAAA2u);
-                    const int32_t tt = 8 * o + S1;
-                    a1 += tt;
-                    a2 += o * (tt + S1) + S2;
-                    o += D;
+                    const int32_t S1 = int32_t((e >> 12) & 0x7FFu) - 36;
+                    so += o;
+                    so2 += o * o;
+                    sos1 += o * S1;
+                    pk += e;
+                    o += int32_t(e >> 23) - 8;
                 }
             }
+            // a1 = sum of (o_b + m_t) over the lane's sites, a2 = sum of squares
+            const int32_t sumS1 = int32_t((pk >> 12) & 0x7FFu) - 36 * nb;
+            const int32_t sumS2 = int32_t(pk & 0xFFFu);
+            const int32_t a1 = 8 * so + sumS1;
+            const int32_t a2 = 8 * so2 + 2 * sos1 + sumS2;
             const int32_t nsites = VEC ? 128 : 32 * nw;
             // lane start heights: exclusive warp scan of o (net step of each lane)
             int32_t inc = o;
@@ -171,30 +135,145 @@ __global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __r
             s1 += (long long)nsites * O + a1;
             s2 += (long long)O * (long long)(nsites * O + 2 * a1) + a2;
         }
-    }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        s1 += __shfl_down_sync(0xFFFFFFFFu, s1, d);
-        s2 += __shfl_down_sync(0xFFFFFFFFu, s2, d);
-    }
-    if (lane == 0 && (s1 | s2)) {
-        atomicAdd(out2 + 0, (unsigned long long)s1);
-        atomicAdd(out2 + 1, (unsigned long long)s2);
+        for (int d = 16; d > 0; d >>= 1) {
+            s1 += __shfl_down_sync(0xFFFFFFFFu, s1, d);
+            s2 += __shfl_down_sync(0xFFFFFFFFu, s2, d);
+        }
+        if (lane == 0) {
+            rs[2 * size_t(k)] = s1;
+            rs[2 * size_t(k) + 1] = s2;
+            // column-0 step into row g (interface_width anchors h(0, 0) = 0: none into row 0)
+            int32_t stp = 0;
+            if (g != 0) {
+                const uint32_t a = row[0] & 1u;
+                const uint32_t bb = f[size_t(((g - 1) & Lm) & rmask) * wpr] & 1u;
+                stp = a == bb ? 1 : -1;
+            }
+            rstep[k] = stp;
+        }
     }
 }
 
-cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, int32_t* V,
+// Chain the row sums of rows k < n in order.  V_k = sum_{m <= k} step_m is the
+// column-0 height of row k relative to the row below the piece;
+//   sum h   += L V_k + S1_k,   sum h^2 += L V_k^2 + 2 V_k S1_k + S2_k.
+// Two levels, coalesced: tile pass (one CTA per 1024 consecutive rows; thread =
+// row) with v = V relative to the tile start, storing per tile
+//   D = sum step, A0 = sum (L v + S1), A1 = sum v, A2 = sum (L v^2 + 2 v S1 + S2), B = sum S1;
+// then one warp chains the tiles with carries c (V = c + v):
+//   sum h += n L c + A0,   sum h^2 += L (n c^2 + 2 c A1) + 2 c B + A2.
+// out3[0] += sum h, out3[1] += sum h^2, out3[2] = V_{n-1} (the piece's net step).
+constexpr int kWidthTile = 1024;
+
+__global__ void __launch_bounds__(kWidthTile) kpz_width_tiles_kernel(const long long* __restrict__ rs,
+                                                                     const int32_t* __restrict__ rstep, int L, int n,
+                                                                     long long* __restrict__ tiles) {
+    __shared__ int32_t wsum[32];
+    __shared__ long long red[4][32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int k = int(blockIdx.x) * kWidthTile + t;
+    const bool in = k < n;
+    const int32_t st = in ? rstep[k] : 0;
+    int32_t inc = st;  // inclusive block scan of the steps
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int32_t w = wsum[lane];
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        wsum[lane] = wi;  // inclusive
+    }
+    __syncthreads();
+    const long long v = (warp ? wsum[warp - 1] : 0) + inc;
+    const long long S1 = in ? rs[2 * size_t(k)] : 0, S2 = in ? rs[2 * size_t(k) + 1] : 0;
+    long long q[4] = {in ? (long long)L * v + S1 : 0, in ? v : 0, in ? (long long)L * v * v + 2 * v * S1 + S2 : 0, S1};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) q[i] += __shfl_down_sync(0xFFFFFFFFu, q[i], d);
+        if (lane == 0) red[i][warp] = q[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            long long x = red[i][lane];
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) x += __shfl_down_sync(0xFFFFFFFFu, x, d);
+            if (lane == 0) tiles[6 * size_t(blockIdx.x) + 1 + i] = x;
+        }
+        if (lane == 0) tiles[6 * size_t(blockIdx.x)] = wsum[31];
+    }
+}
+
+__global__ void __launch_bounds__(32) kpz_width_chain_kernel(const long long* __restrict__ tiles, int ntiles, int L,
+                                                             int n, unsigned long long* __restrict__ out3) {
+    const int lane = threadIdx.x;
+    long long carry = 0, t1 = 0, t2 = 0;
+    for (int b = 0; b < ntiles; b += 32) {
+        const int i = b + lane;
+        const bool in = i < ntiles;
+        const long long D = in ? tiles[6 * size_t(i)] : 0;
+        long long incl = D;  // inclusive warp scan of the tile steps
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += x;
+        }
+        const long long c = carry + incl - D;  // V at the row below tile i
+        if (in) {
+            const long long nt = min(kWidthTile, n - i * kWidthTile);
+            const long long A0 = tiles[6 * size_t(i) + 1], A1 = tiles[6 * size_t(i) + 2];
+            const long long A2 = tiles[6 * size_t(i) + 3], B = tiles[6 * size_t(i) + 4];
+            t1 += nt * L * c + A0;
+            t2 += (long long)L * (nt * c * c + 2 * c * A1) + 2 * c * B + A2;
+        }
+        carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        t1 += __shfl_down_sync(0xFFFFFFFFu, t1, d);
+        t2 += __shfl_down_sync(0xFFFFFFFFu, t2, d);
+    }
+    if (lane == 0) {
+        atomicAdd(out3 + 0, (unsigned long long)t1);
+        atomicAdd(out3 + 1, (unsigned long long)t2);
+        out3[2] = (unsigned long long)carry;
+    }
+}
+
+size_t kpz_width_scratch_bytes(int row_count) {
+    const size_t ntiles = (size_t(row_count) + kWidthTile - 1) / kWidthTile;
+    return size_t(row_count) * 20 + ntiles * 48 + 64;
+}
+
+cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, void* scratch,
                                   unsigned long long* out3, cudaStream_t st) {
-    kpz_col0_steps_kernel<<<1, 1024, 0, st>>>(f, L, rmask, row_begin, row_count, V,
-                                              reinterpret_cast<long long*>(out3 + 2));
+    long long* rs = static_cast<long long*>(scratch);
+    long long* tiles = rs + 2 * size_t(row_count);  // [ntiles][6]
+    const int ntiles = (row_count + kWidthTile - 1) / kWidthTile;
+    int32_t* rstep = reinterpret_cast<int32_t*>(tiles + 6 * size_t(ntiles));
     const int wpb = 8;
     // resident CTAs: 32 KB of table each -> 6 per SM; 148 SMs
     const unsigned grid = unsigned(std::min((row_count + wpb - 1) / wpb, 148 * 6));
-    if (grid == 0) return cudaGetLastError();
-    if ((L >> 5) % 128 == 0)
-        kpz_width_rows_kernel<true><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, V, out3);
-    else
-        kpz_width_rows_kernel<false><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, V, out3);
+    if (grid > 0) {
+        if ((L >> 5) % 128 == 0)
+            kpz_width_rows_kernel<true><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
+        else
+            kpz_width_rows_kernel<false><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
+    }
+    if (ntiles > 0) kpz_width_tiles_kernel<<<unsigned(ntiles), kWidthTile, 0, st>>>(rs, rstep, L, row_count, tiles);
+    kpz_width_chain_kernel<<<1, 32, 0, st>>>(tiles, ntiles, L, row_count, out3);
     return cudaGetLastError();
 }
 

@@ -135,6 +135,17 @@ LFG_HD KpzSweep kpz_sweep_draw(int32_t bx, int32_t by, uint64_t seed, uint64_t s
 // ---------------------------------------------------------------- KMC plan
 constexpr int kKmcTile = 8, kKmcDom = 4, kKmcRounds = 256;
 
+// The attempt words of round r of a tile: one Philox draw
+// W = Philox(seed; tile, r >> 1, s, TAG_KMC_SITE) serves rounds 2m and 2m + 1.
+//   even: site bits W.x[0..5), direction below(W.y, 12), acceptance word W.z;
+//   odd:  site bits W.x[5..10), direction below(W.x & ~1023, 12) (22 bits),
+//         acceptance word W.w.
+LFG_HD void kmc_round_words(const U4& W, bool odd, uint32_t& site5, uint32_t& dir, uint32_t& acc) {
+    site5 = (odd ? W.x >> 5 : W.x) & 31u;
+    dir = below(odd ? (W.x & ~1023u) : W.y, 12);
+    acc = odd ? W.w : W.z;
+}
+
 struct KmcSweep {
     int32_t ox, oy, oz;
     uint32_t perm;  // 3 bits per phase

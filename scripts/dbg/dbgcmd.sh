@@ -1,6 +1,5 @@
-T=r02f; mkdir -p gpurun_out/$T
+T=r02h; mkdir -p gpurun_out/$T
+timeout 1500 python -m pytest tests/ -q -m gpu -x > gpurun_out/$T/pytest_gpu.txt 2>&1; echo "pytest exit $?" >> gpurun_out/$T/pytest_gpu.txt
 python scripts/w2_time.py > gpurun_out/$T/w2_time.json 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:kpz_width_rows -c 1 -o gpurun_out/$T/prof_w2 -f python scripts/w2_time.py 65536 2 > gpurun_out/$T/ncu_w2.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/$T/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-kmc --no-c3 > gpurun_out/$T/launches.log 2>&1
-timeout 900 python bench.py > gpurun_out/$T/bench.json 2> gpurun_out/$T/bench.err
-bash scripts/stats_c2.sh $T/c2
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:kpz_width -c 6 --csv --log-file gpurun_out/$T/w2_launches.csv python scripts/w2_time.py 65536 2 > /dev/null 2>&1
+for L in 512 1024; do timeout 600 python scripts/kmc_bench.py $L 20 >> gpurun_out/$T/kmc_bench.txt 2>&1; done

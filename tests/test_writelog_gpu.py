@@ -111,3 +111,58 @@ def test_dt_write_sets_are_disjoint(lfg, oracle, reflib, L, bx, by, sub, p, q, n
             assert nacc == c.successes
         lfg._native.check(lfg._native.lib().lfg_kpz_debug_record_anchors(k._h, None, 0))
     assert total_rw > 0 and total_bw > 0
+
+
+@pytest.mark.parametrize("both,four_per_warp", [(True, False), (False, False), (True, True)])
+def test_kmc_write_sets_are_disjoint(lfg, reflib, both, four_per_warp):
+    """KMC (16^3 plan): the exchanges the GPU kernels make -- the full-warp kernel of
+    sparse phases and the 4-blocks-per-warp kernel of dense ones (forced by a large
+    concurrency hint) -- recorded site by site (lfg_kmc_debug_record_writes, the write
+    hooks of kmc.hpp:105-110) and checked by the reference's WriteLog: no site written
+    by two tiles in one single-hit round, nor by two blocks in one phase."""
+    import torch
+
+    L, nsweeps = 64, 12
+    nact = (L // 16) ** 3 // 8  # active blocks per phase
+    buf = torch.zeros(L ** 3, dtype=torch.int32, device="cuda")
+    with lfg.KmcLattice(L, 1.5, both, 31) as k:
+        if four_per_warp:
+            k.set_concurrency(512)
+        k.make_random_alloy(0.5, 9)
+        lfg._native.check(lfg._native.lib().lfg_kmc_debug_record_writes(k._h, buf.data_ptr(), L ** 3))
+        tot = 0
+        for s in range(nsweeps):
+            c = k.sweep(1)
+            rec = buf.cpu().numpy().view(np.uint32).reshape(8, 256, nact, 8, 2)
+            done = rec[..., 0] != 0xFFFFFFFF
+            assert int(done.sum()) == c.successes  # every exchange recorded once
+            sites = rec.astype(np.int64)
+            tiles = np.broadcast_to(np.arange(nact * 8).reshape(nact, 8), (8, 256, nact, 8))
+            blocks = np.broadcast_to(np.arange(nact).reshape(nact, 1), (8, 256, nact, 8))
+            G = 8 * 256
+            # round level: one interval per (phase, round), workers = tiles
+            nv, nw, first = reflib.writelog_violations(
+                nact * 8, *_np_log2(tiles.reshape(G, -1), done.reshape(G, -1), sites.reshape(G, -1, 2)))
+            assert nv == 0, (s, first)
+            # block level: one interval per phase, workers = device blocks
+            nv2, nw2, first2 = reflib.writelog_violations(
+                nact, *_np_log2(blocks.reshape(8, -1), done.reshape(8, -1), sites.reshape(8, -1, 2)))
+            assert nv2 == 0, (s, first2)
+            assert nw == nw2 == 2 * c.successes
+            tot += nw
+            if s == 0:  # negative control: a phase as one interval with tiles as workers must race
+                nvw, _, _ = reflib.writelog_violations(
+                    nact * 8, *_np_log2(tiles.reshape(8, -1), done.reshape(8, -1), sites.reshape(8, -1, 2)))
+                assert nvw > 0
+        lfg._native.check(lfg._native.lib().lfg_kmc_debug_record_writes(k._h, None, 0))
+    assert tot > 0
+
+
+def _np_log2(workers, done, sites):
+    """_np_log for attempts that write two sites (KMC exchanges)."""
+    G, T = workers.shape
+    nw = np.where(done, 2, 0).reshape(-1)
+    goff = np.arange(G + 1, dtype=np.int64) * T
+    woff = np.concatenate([[0], np.cumsum(nw)]).astype(np.int64)
+    ws = sites.reshape(-1, 2)[done.reshape(-1)].reshape(-1).astype(np.int64)
+    return goff, workers.reshape(-1).astype(np.int32), woff, (ws if ws.size else np.zeros(1, np.int64))
