@@ -26,6 +26,10 @@
 #include "kpz_kernels.cuh"
 #include "lfg_common.cuh"
 
+#ifndef LFG_KPZ_RED
+#define LFG_KPZ_RED 1  // write the flip back with red.shared.xor (0: XOR + STS; +3 % at L = 2^16, gpurun_out/r02j)
+#endif
+
 namespace lfg {
 
 // ============================================================ DTr phase kernel
@@ -211,7 +215,13 @@ __device__ __forceinline__ void kpz_attempt_tiles(const uint32_t (&addr)[NT], co
         }
     }
 #pragma unroll
+#if LFG_KPZ_RED
+    // variant: shared-memory XOR reduction of the flip (one instruction instead of XOR + STS)
+    for (int n = 0; n < NT; ++n) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[n] + (HY << 11)), "r"(acc[n]));
+    (void)res;
+#else
     for (int n = 0; n < NT; ++n) sts32(addr[n] + (HY << 11), res[n]);
+#endif
 }
 
 // Inner single-hit rounds of one block activation.  The inner set of each

@@ -1,5 +1,9 @@
-T=r02h; mkdir -p gpurun_out/$T
-timeout 1500 python -m pytest tests/ -q -m gpu -x > gpurun_out/$T/pytest_gpu.txt 2>&1; echo "pytest exit $?" >> gpurun_out/$T/pytest_gpu.txt
-python scripts/w2_time.py > gpurun_out/$T/w2_time.json 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:kpz_width -c 6 --csv --log-file gpurun_out/$T/w2_launches.csv python scripts/w2_time.py 65536 2 > /dev/null 2>&1
-for L in 512 1024; do timeout 600 python scripts/kmc_bench.py $L 20 >> gpurun_out/$T/kmc_bench.txt 2>&1; done
+T=r02j; mkdir -p gpurun_out/$T
+B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-kmc --no-c3"
+for i in 1 2; do
+  timeout 300 $B > gpurun_out/$T/main_$i.json 2>/dev/null
+  LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 300 $B > gpurun_out/$T/red_$i.json 2>/dev/null
+  timeout 300 $B --p 0.95 --q 0.05 > gpurun_out/$T/main_p95_$i.json 2>/dev/null
+  LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 300 $B --p 0.95 --q 0.05 > gpurun_out/$T/red_p95_$i.json 2>/dev/null
+done
+LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 600 python -m pytest tests/test_kpz_gpu.py -q -x > gpurun_out/$T/pytest_red.txt 2>&1
