@@ -1,9 +1,3 @@
-T=r02j; mkdir -p gpurun_out/$T
-B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-kmc --no-c3"
-for i in 1 2; do
-  timeout 300 $B > gpurun_out/$T/main_$i.json 2>/dev/null
-  LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 300 $B > gpurun_out/$T/red_$i.json 2>/dev/null
-  timeout 300 $B --p 0.95 --q 0.05 > gpurun_out/$T/main_p95_$i.json 2>/dev/null
-  LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 300 $B --p 0.95 --q 0.05 > gpurun_out/$T/red_p95_$i.json 2>/dev/null
-done
-LFG_LIB=$PWD/paper_1204_5072_b200/_lib/variants/red/liblfg.so timeout 600 python -m pytest tests/test_kpz_gpu.py -q -x > gpurun_out/$T/pytest_red.txt 2>&1
+T=r02l; mkdir -p gpurun_out/$T
+python scripts/sharded_one_gpu.py > gpurun_out/$T/sharded_one_gpu.txt 2>&1
+bash scripts/sanitize.sh $T/san > /dev/null 2>&1

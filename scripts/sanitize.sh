@@ -14,8 +14,11 @@ for tool in racecheck memcheck synccheck initcheck; do
   run $tool kpz_full
   run $tool kpz_general
   run $tool kpz_small
-  run $tool kpz_sweep LFG_KPZ_SWEEP_KERNEL=1
+  run $tool kpz_sub1
+  run $tool kpz_sharded
   run $tool kmc_wide
   run $tool kmc_narrow LFG_KMC_WIDE=0
   run $tool kmc_32
 done
+run memcheck kpz_tensor
+run initcheck kpz_tensor

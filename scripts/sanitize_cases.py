@@ -5,8 +5,8 @@
 
 Each case runs a few sweeps through the C ABI and compares the lattice and
 counters with the CPU oracle (test infrastructure, oracle/), so a sanitizer
-pass is also a parity pass.  Kernel selection knobs (LFG_KPZ_SWEEP_KERNEL,
-LFG_KMC_WIDE) are set by sanitize.sh per case."""
+pass is also a parity pass.  Kernel selection knobs (LFG_KMC_WIDE) are set by
+sanitize.sh per case."""
 import os
 import sys
 
@@ -21,10 +21,20 @@ import pyoracle  # noqa: E402
 orc = pyoracle.Oracle()
 
 
-def kpz(L, p, q, bx, by, sweeps=1, seed=11):
+def kpz(L, p, q, bx, by, sweeps=1, seed=11, sub=4, strips=0):
     x, y = orc.kpz_flat(L)
-    c_ref = orc.kpz_sweep_dtr(L, x, y, p, q, seed, 0, sweeps, bx, by)
-    with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by) as k:
+    c_ref = orc.kpz_sweep_dtr(L, x, y, p, q, seed, 0, sweeps, bx, by, sub)
+    if strips:  # one-process sharded handle, all strips on device 0
+        with lfg.ShardedKpzLattice(L, p, q, seed, devices=[0] * strips, block_x=bx, block_y=by, sub=sub) as k:
+            k.make_flat_slopes()
+            c = k.sweep(sweeps)
+            gx, gy = k.download()
+            w2 = k.interface_width()
+        assert [c.attempts, c.successes, c.deposits, c.detaches] == c_ref.tolist(), (c, c_ref)
+        assert np.array_equal(gx, x) and np.array_equal(gy, y)
+        assert w2 == orc.interface_width(L, x, y)
+        return
+    with lfg.KpzLattice(L, p, q, seed, block_x=bx, block_y=by, sub=sub) as k:
         k.make_flat_slopes()
         c = k.sweep(sweeps)
         gx, gy = k.download()
@@ -49,10 +59,12 @@ def kmc(L, both, bk, sweeps=1, seed=3):
 
 
 CASES = {
-    "kpz_full": lambda: kpz(2048, 1.0, 0.0, 1024, 128),          # TMA-staged FULL path, chained phases
+    "kpz_full": lambda: kpz(2048, 1.0, 0.0, 1024, 128),          # 1024-wide path (bulk copies at the wrap), chained phases
     "kpz_general": lambda: kpz(2048, 0.95, 0.05, 1024, 128),     # p < 1 acceptance draws
+    "kpz_tensor": lambda: kpz(4096, 1.0, 0.0, 1024, 128),        # TMA tensor-map staging / write-back away from the wrap
     "kpz_small": lambda: kpz(256, 0.95, 0.05, 128, 64),          # generic staging (block narrower than 1024)
-    "kpz_sweep": lambda: kpz(2048, 1.0, 0.0, 1024, 128),         # persistent whole-sweep kernel (env)
+    "kpz_sub1": lambda: kpz(2048, 0.95, 0.05, 1024, 128, sub=1),  # the paper's scheme (512 rounds, no skips)
+    "kpz_sharded": lambda: kpz(2048, 0.95, 0.05, 1024, 128, strips=4),  # one-process sharded handle
     "kmc_wide": lambda: kmc(64, True, 16),                       # full-warp 16^3 kernel
     "kmc_narrow": lambda: kmc(64, False, 16),                    # 8-lane 16^3 kernel (env LFG_KMC_WIDE=0)
     "kmc_32": lambda: kmc(64, True, 32),                         # 32^3 blocks
