@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # A/B of KPZ bench arms selected by environment: ab_env.sh TAG "NAME=ENV ..." ...
-# e.g. scripts/ab_env.sh s1 "pdl=" "sweep=LFG_KPZ_SWEEP_KERNEL=1" "plain=LFG_KPZ_PDL=0"
+# e.g. scripts/ab_env.sh s1 "pdl=" "plain=LFG_KPZ_PDL=0"
 TAG=$1; shift; OUT=gpurun_out/$TAG; mkdir -p $OUT
 [ -n "$TESTS" ] && timeout 900 python -m pytest $TESTS -x -q -m gpu > $OUT/pytest.txt 2>&1
 B="python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-kmc"

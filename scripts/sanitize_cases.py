@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Small runs of every sweep-kernel path, for compute-sanitizer (scripts/sanitize.sh).
 
-    python scripts/sanitize_cases.py kpz_full|kpz_general|kpz_small|kpz_sweep|kmc_wide|kmc_narrow|kmc_32|readouts
+    python scripts/sanitize_cases.py [case ...]   (cases: see CASES below)
 
 Each case runs a few sweeps through the C ABI and compares the lattice and
 counters with the CPU oracle (test infrastructure, oracle/), so a sanitizer
