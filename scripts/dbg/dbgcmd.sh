@@ -1,3 +1,3 @@
-T=r02l; mkdir -p gpurun_out/$T
-python scripts/sharded_one_gpu.py > gpurun_out/$T/sharded_one_gpu.txt 2>&1
-bash scripts/sanitize.sh $T/san > /dev/null 2>&1
+T=r02m; mkdir -p gpurun_out/$T
+python scripts/shard_compute_proxy.py > gpurun_out/$T/proxy_p1.json 2>&1
+python scripts/shard_compute_proxy.py 0.95 0.05 > gpurun_out/$T/proxy_p095.json 2>&1

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Compute side of the strip-sharded KPZ sweep (BASELINE configs[2], L = 2^17) on one GPU.
 
-One rank's share of a sweep on N GPUs is its strip: 4 phase launches over L/N rows
+One rank's share of an MCS on N GPUs is its strip: 4 phase launches per sub-sweep over L/N rows
 (lfg_kpz_strip_phase).  Timing rank 0's launches alone on one B200 gives the per-GPU
 compute time of an N-GPU run (each GPU runs exactly this workload); against the
 single-lattice sweep it bounds the strong-scaling efficiency from the compute side:
@@ -52,8 +52,8 @@ for world in (2, 4, 8):
     try:
         # the ring buffer starts all-zero (a valid spin field); its content does not change the cost
 
-        def run(n, s0):
-            for s in range(s0, s0 + n):
+        def run(n, s0):  # n MCS from MCS s0: pl.sub sub-sweeps of 4 phases each
+            for s in range(s0 * pl.sub, (s0 + n) * pl.sub):
                 for kk in range(4):
                     b0, nb = pl.block_rows(0)
                     e.phase(s, kk, b0, nb)
