@@ -79,8 +79,9 @@ struct DtrPlan {
     std::int32_t block_x = 0, block_y = 0;  // KPZ device block (0 = auto)
     std::int32_t sub = 0;                   // KPZ sub-sweeps per MCS (0 = 4; 1 = the paper's scheme)
     std::int32_t block = 0;                 // KMC device block edge (0 = auto)
-    // KPZ over several GPUs from this one thread (lfg_kpz_create_sharded, y-strips):
-    // devices 0..n_gpus-1, or the explicit list `devices` (a device may repeat).
+    // KPZ y-strips / KMC z-slabs over several GPUs from this one thread
+    // (lfg_kpz_create_sharded / lfg_kmc_create_sharded): devices 0..n_gpus-1, or the
+    // explicit list `devices` (a device may repeat).
     std::int32_t n_gpus = 1;
     std::vector<std::int32_t> devices;
 };
@@ -214,54 +215,78 @@ std::vector<std::int32_t> reconstruct_heights(const Field& f, int device = 0) {
 // ------------------------------------------------------------------ KMC
 class KmcDevice {
 public:
+    // plan.n_gpus > 1 or plan.devices with > 1 entry: z-slabs over those GPUs
+    // (BASELINE configs[4]), same trajectory bit for bit.
     KmcDevice(std::int32_t L, double eps, bool both_active, std::uint64_t seed, const DtrPlan& plan = {},
               int device = 0) {
         lfg_kmc_plan pl{plan.block};
-        check(lfg_kmc_create(&h_, L, eps, both_active ? 1 : 0, seed, &pl, device));
+        std::vector<std::int32_t> devs = plan.devices;
+        if (devs.empty())
+            for (std::int32_t g = 0; g < plan.n_gpus; ++g) devs.push_back(plan.n_gpus > 1 ? g : device);
+        if (devs.size() > 1)
+            check(lfg_kmc_create_sharded(&s_, L, eps, both_active ? 1 : 0, seed, &pl, std::int32_t(devs.size()),
+                                         devs.data()));
+        else
+            check(lfg_kmc_create(&h_, L, eps, both_active ? 1 : 0, seed, &pl, devs[0]));
         L_ = L;
     }
     KmcDevice(const KmcDevice&) = delete;
     KmcDevice& operator=(const KmcDevice&) = delete;
-    ~KmcDevice() { lfg_kmc_destroy(h_); }
+    ~KmcDevice() {
+        if (h_) lfg_kmc_destroy(h_);
+        if (s_) lfg_kmc_sharded_destroy(s_);
+    }
 
     std::int32_t size() const { return L_; }
+    bool sharded() const { return s_ != nullptr; }
     template <class Lattice>
     void upload(const Lattice& lat) {
         if (lat.size() != L_) throw std::invalid_argument("KmcDevice: lattice size mismatch");
-        check(lfg_kmc_upload(h_, lat.words(), nwords()));
+        check(s_ ? lfg_kmc_sharded_upload(s_, lat.words(), nwords()) : lfg_kmc_upload(h_, lat.words(), nwords()));
     }
     template <class Lattice>
     void download(Lattice& lat) const {
         if (lat.size() != L_) throw std::invalid_argument("KmcDevice: lattice size mismatch");
-        check(lfg_kmc_download(h_, lat.words(), nwords()));
+        check(s_ ? lfg_kmc_sharded_download(s_, lat.words(), nwords()) : lfg_kmc_download(h_, lat.words(), nwords()));
     }
-    void make_random_alloy(double c, std::uint64_t seed) { check(lfg_kmc_init_random_alloy(h_, c, seed)); }
+    void make_random_alloy(double c, std::uint64_t seed) {
+        check(s_ ? lfg_kmc_sharded_init_random_alloy(s_, c, seed) : lfg_kmc_init_random_alloy(h_, c, seed));
+    }
     Counters sweep(int steps = 1) {
         lfg_counters c{};
-        check(lfg_kmc_sweep(h_, steps, &c));
+        check(s_ ? lfg_kmc_sharded_sweep(s_, steps, &c) : lfg_kmc_sweep(h_, steps, &c));
         return Counters{c.attempts, c.successes};
     }
     double open_bonds_per_particle() {
         double v = 0;
-        check(lfg_kmc_open_bonds_per_particle(h_, &v));
+        check(s_ ? lfg_kmc_sharded_open_bonds_per_particle(s_, &v) : lfg_kmc_open_bonds_per_particle(h_, &v));
         return v;
     }
     std::int64_t count_b() {
         std::int64_t n = 0;
-        check(lfg_kmc_count_b(h_, &n));
+        if (s_) {
+            std::int64_t open = 0;
+            check(lfg_kmc_sharded_open_bond_sums(s_, &n, &open));
+        } else {
+            check(lfg_kmc_count_b(h_, &n));
+        }
         return n;
     }
     std::uint64_t sweep_index() const {
         std::uint64_t s = 0;
-        check(lfg_kmc_get_sweep_index(h_, &s));
+        check(s_ ? lfg_kmc_sharded_get_sweep_index(s_, &s) : lfg_kmc_get_sweep_index(h_, &s));
         return s;
     }
-    void set_sweep_index(std::uint64_t s) { check(lfg_kmc_set_sweep_index(h_, s)); }
+    void set_sweep_index(std::uint64_t s) {
+        check(s_ ? lfg_kmc_sharded_set_sweep_index(s_, s) : lfg_kmc_set_sweep_index(h_, s));
+    }
     lfg_kmc* handle() { return h_; }
+    lfg_kmc_sharded* sharded_handle() { return s_; }
 
 private:
     std::size_t nwords() const { return std::size_t(L_) * std::size_t(L_) * std::size_t(L_) / 64; }
     lfg_kmc* h_ = nullptr;
+    lfg_kmc_sharded* s_ = nullptr;
     std::int32_t L_ = 0;
 };
 

@@ -106,6 +106,29 @@ LFG_API int lfg_kmc_set_abort_flag(lfg_kmc* h, const void* dev_flag);
  * exchange.  Block order within a round = launch order (x fastest). */
 LFG_API int lfg_kmc_debug_record_writes(lfg_kmc* h, void* dev_buf, size_t capacity_words);
 
+/* ------------------------------------------------------------ sharded lattice (one process, N GPUs)
+ * BASELINE configs[4]: the lattice cut into N z-slabs (slab g on devices[g];
+ * NULL: devices 0..N-1; a device may repeat) driven by ONE host thread -- the
+ * caller of kmc_mcs_sequential / open_bonds_per_particle (kmc.hpp:128-129) gets
+ * the same lattice, bit for bit, as lfg_kmc_create's single-GPU handle.  Per MCS
+ * the plane ownership rolls with the DT origin; around each phase the two ghost
+ * planes on the active side are refreshed and the one the phase may have
+ * modified goes back to its owner (peer copies over NVLink, event-ordered).
+ * L/N must be a multiple of 2 * block. */
+typedef struct lfg_kmc_sharded lfg_kmc_sharded;
+LFG_API int lfg_kmc_create_sharded(lfg_kmc_sharded** h, int32_t L, double eps, int32_t both_active, uint64_t seed,
+                                   const lfg_kmc_plan* plan, int32_t n_shards, const int32_t* devices);
+LFG_API int lfg_kmc_sharded_destroy(lfg_kmc_sharded* h);
+LFG_API int lfg_kmc_sharded_init_random_alloy(lfg_kmc_sharded* h, double c, uint64_t alloy_seed);
+LFG_API int lfg_kmc_sharded_upload(lfg_kmc_sharded* h, const uint64_t* words, size_t nwords);
+LFG_API int lfg_kmc_sharded_download(lfg_kmc_sharded* h, uint64_t* words, size_t nwords);
+LFG_API int lfg_kmc_sharded_sweep(lfg_kmc_sharded* h, int64_t n_mcs, lfg_counters* out);
+LFG_API int lfg_kmc_sharded_counters(lfg_kmc_sharded* h, lfg_counters* out);
+LFG_API int lfg_kmc_sharded_open_bond_sums(lfg_kmc_sharded* h, int64_t* particles, int64_t* open_bonds);
+LFG_API int lfg_kmc_sharded_open_bonds_per_particle(lfg_kmc_sharded* h, double* value);
+LFG_API int lfg_kmc_sharded_set_sweep_index(lfg_kmc_sharded* h, uint64_t sweep);
+LFG_API int lfg_kmc_sharded_get_sweep_index(const lfg_kmc_sharded* h, uint64_t* sweep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ from . import _native
 from ._native import (ClosureError, Counters, CudaError, DeviceOutOfMemory, DomainError,  # noqa: F401
                       InvalidArgument, KmcPlan, KpzPlan, LfgError, TransportError, check, device_count)
 
-__all__ = ["KpzLattice", "ShardedKpzLattice", "KmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
+__all__ = ["KpzLattice", "ShardedKpzLattice", "KmcLattice", "ShardedKmcLattice", "Counters", "LfgError", "InvalidArgument", "ClosureError",
            "DomainError", "CudaError", "device_count", "words2", "words3", "interface_width",
            "width_sums", "reconstruct_heights", "open_bond_sums", "open_bonds_per_particle"]
 
@@ -489,3 +489,80 @@ class KmcLattice:
         p, n = C.c_void_p(), C.c_size_t()
         check(_native.lib().lfg_kmc_device_words(self._h, C.byref(p), C.byref(n)))
         return int(p.value or 0), int(n.value)
+class ShardedKmcLattice:
+    """BASELINE configs[4]: one KMC lattice cut into z-slabs over several GPUs, driven by
+    this one process through the C ABI (lfg_kmc_create_sharded).  Same trajectory, bit for
+    bit, as KmcLattice with the same L, eps, mode, seed and plan."""
+
+    def __init__(self, L: int, eps: float = 1.5, both_active: bool = True, seed: int = 1, *, devices=(0, 1),
+                 block: int = 0):
+        self._h = None
+        devs = [int(d) for d in devices]
+        arr = (C.c_int32 * len(devs))(*devs)
+        plan = KmcPlan(block)
+        h = C.c_void_p()
+        check(_native.lib().lfg_kmc_create_sharded(C.byref(h), L, float(eps), int(bool(both_active)), int(seed),
+                                                   C.byref(plan), len(devs), arr))
+        self._h, self.L, self.devices = h, int(L), devs
+
+    def close(self) -> None:
+        if self._h is not None:
+            _native.lib().lfg_kmc_sharded_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def make_random_alloy(self, c: float, alloy_seed: int) -> "ShardedKmcLattice":
+        check(_native.lib().lfg_kmc_sharded_init_random_alloy(self._h, float(c), int(alloy_seed)))
+        return self
+
+    def upload(self, words) -> None:
+        w = _u64(words)
+        check(_native.lib().lfg_kmc_sharded_upload(self._h, w.ctypes.data, w.size))
+
+    def download(self):
+        w = np.empty(self.L ** 3 // 64, np.uint64)
+        check(_native.lib().lfg_kmc_sharded_download(self._h, w.ctypes.data, w.size))
+        return w
+
+    def sweep(self, sweeps: int = 1) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kmc_sharded_sweep(self._h, int(sweeps), C.byref(c)))
+        return c
+
+    def counters(self) -> Counters:
+        c = Counters()
+        check(_native.lib().lfg_kmc_sharded_counters(self._h, C.byref(c)))
+        return c
+
+    def open_bond_sums(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(_native.lib().lfg_kmc_sharded_open_bond_sums(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
+    def open_bonds_per_particle(self) -> float:
+        v = C.c_double()
+        check(_native.lib().lfg_kmc_sharded_open_bonds_per_particle(self._h, C.byref(v)))
+        return float(v.value)
+
+    @property
+    def sweep_index(self) -> int:
+        v = C.c_uint64()
+        check(_native.lib().lfg_kmc_sharded_get_sweep_index(self._h, C.byref(v)))
+        return int(v.value)
+
+    @sweep_index.setter
+    def sweep_index(self, v: int) -> None:
+        check(_native.lib().lfg_kmc_sharded_set_sweep_index(self._h, int(v)))
+
+

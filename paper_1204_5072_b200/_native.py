@@ -152,6 +152,17 @@ def lib() -> C.CDLL:
     _sig(L, "lfg_kpz_sharded_interface_width", P, C.POINTER(D))
     _sig(L, "lfg_kpz_sharded_set_sweep_index", P, U64)
     _sig(L, "lfg_kpz_sharded_get_sweep_index", P, C.POINTER(U64))
+    _sig(L, "lfg_kmc_create_sharded", C.POINTER(P), I32, D, I32, U64, C.POINTER(KmcPlan), I32, C.POINTER(I32))
+    _sig(L, "lfg_kmc_sharded_destroy", P)
+    _sig(L, "lfg_kmc_sharded_init_random_alloy", P, D, U64)
+    _sig(L, "lfg_kmc_sharded_upload", P, P, C.c_size_t)
+    _sig(L, "lfg_kmc_sharded_download", P, P, C.c_size_t)
+    _sig(L, "lfg_kmc_sharded_sweep", P, C.c_int64, C.POINTER(Counters))
+    _sig(L, "lfg_kmc_sharded_counters", P, C.POINTER(Counters))
+    _sig(L, "lfg_kmc_sharded_open_bond_sums", P, C.POINTER(I64), C.POINTER(I64))
+    _sig(L, "lfg_kmc_sharded_open_bonds_per_particle", P, C.POINTER(D))
+    _sig(L, "lfg_kmc_sharded_set_sweep_index", P, U64)
+    _sig(L, "lfg_kmc_sharded_get_sweep_index", P, C.POINTER(U64))
     _sig(L, "lfg_kpz_set_abort_flag", P, P)
     # readouts of host lattices (no handle)
     _sig(L, "lfg_kpz_width_sums_host", I32, I32, P, P, SZ, C.POINTER(I64), C.POINTER(I64))

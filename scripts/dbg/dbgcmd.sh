@@ -1,3 +1,2 @@
-T=r02m; mkdir -p gpurun_out/$T
-python scripts/shard_compute_proxy.py > gpurun_out/$T/proxy_p1.json 2>&1
-python scripts/shard_compute_proxy.py 0.95 0.05 > gpurun_out/$T/proxy_p095.json 2>&1
+T=r02n; mkdir -p gpurun_out/$T
+timeout 1200 python -m pytest tests/test_sharded_capi_gpu.py tests/test_cpp_dropin.py tests/test_kpz_gpu.py -q > gpurun_out/$T/pytest.txt 2>&1; echo "exit $?" >> gpurun_out/$T/pytest.txt

@@ -165,6 +165,20 @@ int main() {
         REQUIRE(one_gpu.interface_width() == strips.interface_width());
         std::printf("sharded OK: 2 strips == 1 lattice, successes=%lld\n", (long long)c2.successes);
     }
+    {   // configs[4] through the C++ API: a KMC lattice on 1 GPU and as 2 z-slabs
+        const int32_t Lk = 128;
+        lf::gpu::DtrPlan two;
+        two.devices = {0, 0};
+        lf::gpu::KmcDevice one_gpu(Lk, 1.5, true, 77), slabs(Lk, 1.5, true, 77, two);
+        REQUIRE(slabs.sharded() && !one_gpu.sharded());
+        one_gpu.make_random_alloy(0.5, 5);
+        slabs.make_random_alloy(0.5, 5);
+        const auto k1 = one_gpu.sweep(2);
+        const auto k2 = slabs.sweep(2);
+        REQUIRE(k1.attempts == k2.attempts && k1.successes == k2.successes);
+        REQUIRE(one_gpu.open_bonds_per_particle() == slabs.open_bonds_per_particle());
+        std::printf("sharded KMC OK: 2 slabs == 1 lattice, exchanges=%lld\n", (long long)k2.successes);
+    }
     std::printf("dropin OK: KPZ W2=%.6f successes=%lld; KMC exchanges=%lld\n", w2, (long long)c.successes,
                 (long long)kc.successes);
     return 0;

@@ -55,3 +55,31 @@ def test_sharded_upload_resume(lfg, oracle):
 def test_sharded_rejects_bad_geometry(lfg):
     with pytest.raises(lfg.InvalidArgument):
         lfg.ShardedKpzLattice(1024, devices=[0] * 8)  # strip height 128 < 2 * block_y
+
+
+@pytest.mark.parametrize("n,both,L", [(2, True, 128), (4, False, 128), (8, True, 256)])
+def test_sharded_kmc_equals_single(lfg, n, both, L):
+    """KMC z-slabs (lfg_kmc_create_sharded) == one lattice, bit for bit."""
+    with lfg.KmcLattice(L, 1.5, both, 21) as k, lfg.ShardedKmcLattice(L, 1.5, both, 21, devices=[0] * n) as s:
+        k.make_random_alloy(0.5, 4)
+        s.make_random_alloy(0.5, 4)
+        assert np.array_equal(k.download(), s.download())
+        c1 = k.sweep(3)
+        c2 = s.sweep(3)
+        assert (c1.attempts, c1.successes) == (c2.attempts, c2.successes)
+        assert np.array_equal(k.download(), s.download())
+        assert k.open_bond_sums() == s.open_bond_sums()
+        assert s.open_bonds_per_particle() == k.open_bonds_per_particle()
+
+
+def test_sharded_kmc_upload_vs_oracle(lfg, oracle):
+    L = 128
+    w, _ = oracle.kmc_random_alloy(L, 0.5, "lcg64", 8)
+    w_ref = w.copy()
+    c_ref = oracle.kmc_sweep_dt(L, w_ref, 1.5, 1, 17, 4, 2, 16)
+    with lfg.ShardedKmcLattice(L, 1.5, True, 17, devices=[0, 0]) as s:
+        s.sweep_index = 4
+        s.upload(w)
+        c = s.sweep(2)
+        assert [c.attempts, c.successes] == c_ref.tolist()
+        assert np.array_equal(s.download(), w_ref)
