@@ -77,7 +77,7 @@ struct KmcParams {  // kmc.hpp:18-27
 
 struct DtrPlan {
     std::int32_t block_x = 0, block_y = 0;  // KPZ device block (0 = auto)
-    std::int32_t sub = 0;                   // KPZ sub-sweeps per MCS (0 = 4; 1 = the paper's scheme)
+    std::int32_t sub = 0;                   // sub-sweeps per MCS (0 = default: KPZ 4, KMC 1; 1 = the paper's scheme)
     std::int32_t block = 0;                 // KMC device block edge (0 = auto)
     // KPZ y-strips / KMC z-slabs over several GPUs from this one thread
     // (lfg_kpz_create_sharded / lfg_kmc_create_sharded): devices 0..n_gpus-1, or the
@@ -219,7 +219,7 @@ public:
     // (BASELINE configs[4]), same trajectory bit for bit.
     KmcDevice(std::int32_t L, double eps, bool both_active, std::uint64_t seed, const DtrPlan& plan = {},
               int device = 0) {
-        lfg_kmc_plan pl{plan.block};
+        lfg_kmc_plan pl{plan.block, plan.sub};
         std::vector<std::int32_t> devs = plan.devices;
         if (devs.empty())
             for (std::int32_t g = 0; g < plan.n_gpus; ++g) devs.push_back(plan.n_gpus > 1 ? g : device);

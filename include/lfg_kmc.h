@@ -20,6 +20,12 @@ typedef struct lfg_kmc lfg_kmc;
 
 typedef struct lfg_kmc_plan {
     int32_t block; /* device block edge in sc sites (0 = auto) */
+    int32_t sub;   /* sub-sweeps per MCS (0 = auto = 1; 1 or 4): 4 gives every block four
+                      shorter activations per MCS, each sub-sweep with its own origin and
+                      set order -- removes the early-time transient of the frozen block
+                      borders; the sweep index of the phase-level calls
+                      (lfg_kmc_phase, lfg_kmc_slab_phase, lfg_kmc_sweep_origin) is the
+                      sub-sweep index s' = MCS * sub + k */
 } lfg_kmc_plan;
 
 /* OccupancyLattice(L) + KmcParams{eps, active_mode}.validate() (kmc.hpp:18-27). */

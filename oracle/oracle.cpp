@@ -441,13 +441,14 @@ int orc_kmc_sweep_sequential(int32_t L, uint64_t* w, double eps, int both, int k
 }
 
 // Two-layer DT KMC sweeps (oracle_core.hpp) with the restated attempt.
+// MCS sweep0 .. sweep0 + nsweeps - 1, each `sub` sub-sweeps (s' = s * sub + k).
 int orc_kmc_sweep_dt(int32_t L, uint64_t* w, double eps, int both, uint64_t seed, uint64_t sweep0,
-                     int32_t nsweeps, int32_t bk, int64_t* counters) {
-    if (!(eps >= 0.0)) return -1;
-    orc::KmcPlan pl{L, bk};
+                     int32_t nsweeps, int32_t bk, int32_t sub, int64_t* counters) {
+    if (!(eps >= 0.0) || (sub != 1 && sub != 4)) return -1;
+    orc::KmcPlan pl{L, bk, sub};
     int64_t succ = 0;
-    for (int32_t s = 0; s < nsweeps; ++s) {
-        succ += orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
+    for (int64_t s = 0; s < int64_t(nsweeps) * sub; ++s) {
+        succ += orc::kmc_dt_sweep(pl, seed, sweep0 * uint64_t(sub) + uint64_t(s),
                                   [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
                                       const int32_t site[3] = {x, y, z};
                                       return kmc_attempt(w, L, site, eps, both,
@@ -462,10 +463,11 @@ int orc_kmc_sweep_dt(int32_t L, uint64_t* w, double eps, int both, uint64_t seed
 
 // One DT phase restricted to block z-rows [bz0, bz0 + nbz) (the z-slab
 // driver's unit of work; tests/test_shard_kmc_cpu.py).
+// One phase of sub-sweep `sweep` (s' = MCS * sub + k) on block z-rows [bz0, bz0 + nbz).
 int orc_kmc_dt_phase_rows(int32_t L, uint64_t* w, double eps, int both, uint64_t seed, uint64_t sweep,
-                          int32_t phase, int32_t bk, int32_t bz0, int32_t nbz, int64_t* counters) {
-    if (!(eps >= 0.0) || phase < 0 || phase > 7) return -1;
-    orc::KmcPlan pl{L, bk};
+                          int32_t phase, int32_t bk, int32_t sub, int32_t bz0, int32_t nbz, int64_t* counters) {
+    if (!(eps >= 0.0) || phase < 0 || phase > 7 || (sub != 1 && sub != 4)) return -1;
+    orc::KmcPlan pl{L, bk, sub};
     const orc::KmcSweepDraw d = orc::kmc_sweep_draw(pl, seed, sweep);
     int64_t att = 0;
     {
@@ -473,7 +475,7 @@ int orc_kmc_dt_phase_rows(int32_t L, uint64_t* w, double eps, int both, uint64_t
         const int set = d.perm[phase], sx = set & 1, sy = (set >> 1) & 1, sz = set >> 2;
         for (int32_t bzi = sz; bzi < nb; bzi += 2)
             if (bzi >= bz0 && bzi < bz0 + nbz) att += int64_t((nb - sy + 1) / 2) * ((nb - sx + 1) / 2);
-        att *= int64_t(bk) * bk * bk / 2;
+        att *= int64_t(bk) * bk * bk / 2 / sub;
     }
     const int64_t succ = orc::kmc_dt_phase(pl, d, seed, sweep, phase, bz0, bz0 + nbz,
                       [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {

@@ -276,6 +276,7 @@ constexpr int kKmcTile = 8, kKmcDom = 4, kKmcRounds = 256;
 struct KmcPlan {
     int32_t L = 0;
     int32_t bk = 0;  // device block edge (multiple of 8, L % (2 bk) == 0)
+    int32_t sub = 1; // sub-sweeps per MCS (1 or 4): kKmcRounds / sub rounds per activation
 };
 
 struct KmcSweepDraw {
@@ -335,7 +336,7 @@ int64_t kmc_dt_phase(const KmcPlan& pl, const KmcSweepDraw& d, uint64_t seed, ui
         for (int32_t bxi = sx; bxi < nb; bxi += 2) {
             const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
             uint32_t sw[4] = {0, 0, 0, 0};
-            for (int r = 0; r < kKmcRounds; ++r) {
+            for (int r = 0; r < kKmcRounds / pl.sub; ++r) {
                 if ((r & 31) == 0) draw(seed, sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5), sw);
                 const int inner = int((sw[(r >> 3) & 3] >> (4 * (r & 7))) & 7u);
                 const int hx = inner & 1, hy = (inner >> 1) & 1, hz = inner >> 2;

@@ -68,8 +68,8 @@ class Oracle:
         _sig(lib, "orc_kpz_sweep_draw", None, I32, I32, I32, U64, U64, i32p)
         _sig(lib, "orc_kmc_random_alloy", I, I32, D, I, U64, U32, u64p, C.POINTER(U64))
         _sig(lib, "orc_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
-        _sig(lib, "orc_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, i64p)
-        _sig(lib, "orc_kmc_dt_phase_rows", I, I32, u64p, D, I, U64, U64, I32, I32, I32, I32, i64p)
+        _sig(lib, "orc_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, I32, i64p)
+        _sig(lib, "orc_kmc_dt_phase_rows", I, I32, u64p, D, I, U64, U64, I32, I32, I32, I32, I32, i64p)
         _sig(lib, "orc_kmc_sweep_draw", None, I32, I32, U64, U64, i32p)
         _sig(lib, "orc_kmc_open_bond_sums_planes", None, I32, u64p, I32, I32, C.POINTER(I64), C.POINTER(I64))
         _sig(lib, "orc_kmc_open_bond_sums", None, I32, u64p, C.POINTER(I64), C.POINTER(I64))
@@ -155,15 +155,16 @@ class Oracle:
         assert self.lib.orc_kmc_sweep_sequential(L, w, eps, int(both), KIND[kind], C.byref(st), steps, c) == 0
         return c, st.value
 
-    def kmc_sweep_dt(self, L, w, eps, both, seed, sweep0, nsweeps, bk):
+    def kmc_sweep_dt(self, L, w, eps, both, seed, sweep0, nsweeps, bk, sub=1):
+        """MCS sweep0 .. sweep0+nsweeps-1 of the KMC DT schedule (sub sub-sweeps each)."""
         c = np.zeros(2, np.int64)
-        assert self.lib.orc_kmc_sweep_dt(L, w, eps, int(both), seed, sweep0, nsweeps, bk, c) == 0
+        assert self.lib.orc_kmc_sweep_dt(L, w, eps, int(both), seed, sweep0, nsweeps, bk, sub, c) == 0
         return c
 
-    def kmc_dt_phase_rows(self, L, w, eps, both, seed, sweep, phase, bk, bz0, nbz):
-        """One DT phase on block z-rows [bz0, bz0 + nbz); returns [attempts, successes]."""
+    def kmc_dt_phase_rows(self, L, w, eps, both, seed, sweep, phase, bk, bz0, nbz, sub=1):
+        """One DT phase of sub-sweep `sweep` on block z-rows [bz0, bz0 + nbz); returns [attempts, successes]."""
         c = np.zeros(2, np.int64)
-        assert self.lib.orc_kmc_dt_phase_rows(L, w, eps, int(both), seed, sweep, phase, bk, bz0, nbz, c) == 0
+        assert self.lib.orc_kmc_dt_phase_rows(L, w, eps, int(both), seed, sweep, phase, bk, sub, bz0, nbz, c) == 0
         return c
 
     def kmc_sweep_draw(self, L, bk, seed, sweep):
@@ -218,7 +219,7 @@ class RefLib:
         _sig(lib, "ref_kpz_sweep_dtr", I, I32, u64p, u64p, D, D, U64, U64, I32, I32, I32, I32, i64p)
         _sig(lib, "ref_make_random_alloy", I, I32, D, I, U64, u64p, C.POINTER(U64))
         _sig(lib, "ref_kmc_sweep_sequential", I, I32, u64p, D, I, I, C.POINTER(U64), I, i64p)
-        _sig(lib, "ref_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, i64p)
+        _sig(lib, "ref_kmc_sweep_dt", I, I32, u64p, D, I, U64, U64, I32, I32, I32, i64p)
         _sig(lib, "ref_open_bonds_per_particle", I, I32, u64p, C.POINTER(D))
         _sig(lib, "ref_count_b", I, I32, u64p, C.POINTER(I64))
         _sig(lib, "ref_metropolis_prob", I, I, I, D, C.POINTER(D))
@@ -322,9 +323,9 @@ class RefLib:
         self._check(self.lib.ref_kmc_sweep_sequential(L, w, eps, int(both), KIND[kind], C.byref(st), steps, c))
         return c, st.value
 
-    def kmc_sweep_dt(self, L, w, eps, both, seed, sweep0, nsweeps, bk):
+    def kmc_sweep_dt(self, L, w, eps, both, seed, sweep0, nsweeps, bk, sub=1):
         c = np.zeros(2, np.int64)
-        self._check(self.lib.ref_kmc_sweep_dt(L, w, eps, int(both), seed, sweep0, nsweeps, bk, c))
+        self._check(self.lib.ref_kmc_sweep_dt(L, w, eps, int(both), seed, sweep0, nsweeps, bk, sub, c))
         return c
 
     def open_bonds_per_particle(self, L, w):

@@ -301,18 +301,20 @@ int ref_kmc_sweep_sequential(int32_t L, uint64_t* words, double eps, int both, i
 // reference's own exchange_probability (kmc.hpp:70-76) and kFccOffsets
 // (lattice.hpp:147-151).  kmc_attempt_impl itself takes an RngStream& and
 // cannot consume counter-based words, hence this thin restatement.
+// MCS sweep0 .. sweep0 + nsweeps - 1, each `sub` sub-sweeps (s' = s * sub + k).
 int ref_kmc_sweep_dt(int32_t L, uint64_t* words, double eps, int both, uint64_t seed,
-                     uint64_t sweep0, int32_t nsweeps, int32_t bk, int64_t* counters) {
+                     uint64_t sweep0, int32_t nsweeps, int32_t bk, int32_t sub, int64_t* counters) {
     return guarded([&] {
         lf::OccupancyLattice lat(L);
         std::memcpy(lat.words(), words, words3(L) * 8);
         lf::KmcParams params{eps, both ? lf::ActiveMode::both : lf::ActiveMode::b_only};
         params.validate();
         const int32_t mask = L - 1;
-        orc::KmcPlan pl{L, bk};
+        if (sub != 1 && sub != 4) throw std::invalid_argument("DtPlan: sub must be 1 or 4");
+        orc::KmcPlan pl{L, bk, sub};
         int64_t succ = 0;
-        for (int32_t s = 0; s < nsweeps; ++s) {
-            succ += orc::kmc_dt_sweep(pl, seed, sweep0 + uint64_t(s),
+        for (int64_t s = 0; s < int64_t(nsweeps) * sub; ++s) {
+            succ += orc::kmc_dt_sweep(pl, seed, sweep0 * uint64_t(sub) + uint64_t(s),
                                       [&](int32_t x, int32_t y, int32_t z, uint32_t dir_w, uint32_t acc_w) {
                 const lf::Coord3 site{x, y, z};
                 const bool here_b = lat.is_b(x, y, z);

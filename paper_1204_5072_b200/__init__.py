@@ -349,12 +349,12 @@ class KmcLattice:
     """Device-resident fcc binary-alloy occupancy advanced by the two-layer DT sweep."""
 
     def __init__(self, L: int, eps: float = 1.5, both_active: bool = False, seed: int = 1, *,
-                 block: int = 0, device: int = 0):
+                 block: int = 0, sub: int = 0, device: int = 0):
         self._h = None
         L_ = _native.lib()
         if not hasattr(L_, "lfg_kmc_create"):
             raise ImportError("liblfg.so was built without the KMC path")
-        plan = KmcPlan(block)
+        plan = KmcPlan(block, sub)
         h = C.c_void_p()
         check(L_.lfg_kmc_create(C.byref(h), L, float(eps), int(bool(both_active)), int(seed), C.byref(plan),
                                 device))
@@ -366,6 +366,7 @@ class KmcLattice:
         got = KmcPlan()
         check(L_.lfg_kmc_get_plan(h, C.byref(got)))
         self.plan = int(got.block)
+        self.sub = int(got.sub)
 
     def close(self) -> None:
         if self._h is not None:
@@ -495,11 +496,11 @@ class ShardedKmcLattice:
     bit, as KmcLattice with the same L, eps, mode, seed and plan."""
 
     def __init__(self, L: int, eps: float = 1.5, both_active: bool = True, seed: int = 1, *, devices=(0, 1),
-                 block: int = 0):
+                 block: int = 0, sub: int = 0):
         self._h = None
         devs = [int(d) for d in devices]
         arr = (C.c_int32 * len(devs))(*devs)
-        plan = KmcPlan(block)
+        plan = KmcPlan(block, sub)
         h = C.c_void_p()
         check(_native.lib().lfg_kmc_create_sharded(C.byref(h), L, float(eps), int(bool(both_active)), int(seed),
                                                    C.byref(plan), len(devs), arr))

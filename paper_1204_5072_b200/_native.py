@@ -70,7 +70,8 @@ class KpzPlan(C.Structure):
 
 
 class KmcPlan(C.Structure):
-    _fields_ = [("block", C.c_int32)]
+    """lfg_kmc_plan (include/lfg_kmc.h): block, sub (0 = defaults)."""
+    _fields_ = [("block", C.c_int32), ("sub", C.c_int32)]
 
 
 _lib = None

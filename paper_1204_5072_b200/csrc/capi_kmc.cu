@@ -20,7 +20,7 @@ struct lfg_kmc {
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    int32_t L = 0, bk = 0;
+    int32_t L = 0, bk = 0, sub = 1;  // sub: sub-sweeps per MCS (plan)
     double eps = 1.5;
     int both = 0;
     uint64_t seed = 0, sweep = 0;
@@ -75,6 +75,7 @@ KmcPhaseArgs base_args(const lfg_kmc* h) {
     a.counters = h->dcnt;
     a.L = h->L;
     a.bk = h->bk;
+    a.rounds = kKmcRounds / h->sub;
     a.seed = h->seed;
     a.both = h->both;
     for (int d = 0; d <= 12; ++d) {
@@ -91,12 +92,13 @@ KmcPhaseArgs base_args(const lfg_kmc* h) {
 
 void enqueue(lfg_kmc* h, int64_t n) {
     KmcPhaseArgs a = base_args(h);
-    for (int64_t s = 0; s < n; ++s) {
-        a.sweep = h->sweep + uint64_t(s);
+    for (int64_t s = 0; s < n * h->sub; ++s) {
+        a.sweep = h->sweep * uint64_t(h->sub) + uint64_t(s);  // global sub-sweep index
         for (int k = 0; k < 8; ++k) {
             a.phase = k;
-            // one MCS of records: phase k at k * (L^3/2 attempts / 8) * 2 words
-            a.wlog = h->wlog ? h->wlog + size_t(k) * (size_t(h->L) * h->L * h->L / 8) : nullptr;
+            // one MCS of records: phase k of sub-sweep j at (8 j + k) * (L^3/2 attempts / (8 sub)) * 2 words
+            a.wlog = h->wlog ? h->wlog + size_t((s % h->sub) * 8 + k) * (size_t(h->L) * h->L * h->L / 8 / h->sub)
+                             : nullptr;
             cuda_check(kmc_launch_phase(a, h->stream), "kmc_dt_phase launch");
         }
     }
@@ -128,6 +130,8 @@ int32_t validate_create(int32_t L, double eps, const lfg_kmc_plan* plan) {
     const int32_t bk = plan && plan->block ? plan->block : 16;  // 16^3 blocks: SURVEY §7.1 (+0.03 %, z=+0.3)
     if (!(bk == 16 || bk == 32) || L % (2 * bk))
         throw Error(LFG_EINVAL, "DtPlan: block must be 16 or 32 with L % (2*block) == 0, got " + std::to_string(bk));
+    if (plan && plan->sub && plan->sub != 1 && plan->sub != 4)
+        throw Error(LFG_EINVAL, "DtPlan: sub (sub-sweeps per MCS) must be 1 or 4, got " + std::to_string(plan->sub));
     return bk;
 }
 
@@ -138,6 +142,7 @@ lfg_kmc* create_handle(int32_t L, double eps, int32_t both_active, uint64_t seed
     try {
         h->L = L;
         h->bk = bk;
+        h->sub = plan && plan->sub ? plan->sub : 1;
         h->eps = eps;
         h->both = both_active ? 1 : 0;
         h->seed = seed;
@@ -217,7 +222,7 @@ int lfg_kmc_slab_phase(lfg_kmc* h, void* planes, int32_t cap, int32_t bz0, int32
         a.phase = phase;
         cuda_check(kmc_launch_phase(a, h->stream), "kmc_dt_phase launch");
         const int64_t hh = h->L / h->bk / 2;
-        h->attempts += hh * hh * (nbz / 2) * int64_t(h->bk) * h->bk * h->bk / 2;
+        h->attempts += hh * hh * (nbz / 2) * int64_t(h->bk) * h->bk * h->bk / 2 / h->sub;
     });
 }
 
@@ -275,6 +280,7 @@ int lfg_kmc_get_plan(const lfg_kmc* h, lfg_kmc_plan* out) {
     return guarded([&] {
         check_handle(h);
         out->block = h->bk;
+        out->sub = h->sub;
     });
 }
 
@@ -349,6 +355,7 @@ int lfg_kmc_phase(lfg_kmc* h, uint64_t sweep, int32_t phase) {
         a.sweep = sweep;
         a.phase = phase;
         cuda_check(kmc_launch_phase(a, h->stream), "kmc_dt_phase launch");
+        h->attempts += int64_t(h->L) * h->L * h->L / 16 / h->sub;
     });
 }
 

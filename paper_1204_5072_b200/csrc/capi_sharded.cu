@@ -459,7 +459,7 @@ int lfg_kpz_sharded_get_sweep_index(const lfg_kpz_sharded* h, uint64_t* sweep) {
 #include "../../include/lfg_kmc.h"
 
 struct lfg_kmc_sharded {
-    int32_t L = 0, n = 1, bk = 0, H = 0, cap = 0;
+    int32_t L = 0, n = 1, bk = 0, sub = 1, H = 0, cap = 0;
     size_t wpp = 0;        // uint32 words per plane
     double eps = 0;
     int32_t both = 0;
@@ -522,6 +522,7 @@ int lfg_kmc_create_sharded(lfg_kmc_sharded** out, int32_t L, double eps, int32_t
                 lcheck(lfg_kmc_create_slab(&h->hs[size_t(g)], L, eps, both_active, seed, plan, h->G.dev[size_t(g)]));
             lcheck(lfg_kmc_get_plan(h->hs[0], &h->plan));
             h->bk = h->plan.block;
+            h->sub = h->plan.sub;
             if (L % n_shards) throw Error(LFG_EINVAL, "n_shards must divide L");
             h->H = L / n_shards;
             if (n_shards > 1 && h->H % (2 * h->bk))
@@ -566,7 +567,7 @@ int lfg_kmc_sharded_destroy(lfg_kmc_sharded* h) {
 int lfg_kmc_sharded_init_random_alloy(lfg_kmc_sharded* h, double c, uint64_t alloy_seed) {
     return guarded([&] {
         if (!h) throw Error(LFG_EINVAL, "null handle");
-        h->oz = kmc_origin_z(h, h->sweep, nullptr);
+        h->oz = kmc_origin_z(h, h->sweep * uint64_t(h->sub), nullptr);
         for (int g = 0; g < h->n; ++g)
             lcheck(lfg_kmc_slab_init_random_alloy(h->hs[size_t(g)], h->ring[size_t(g)], h->cap,
                                                   (h->win0(g) + h->L) % h->L, h->wlen(), c, alloy_seed));
@@ -579,7 +580,7 @@ int lfg_kmc_sharded_upload(lfg_kmc_sharded* h, const uint64_t* words, size_t nwo
         if (!h || !words) throw Error(LFG_EINVAL, "null argument");
         if (nwords != size_t(h->L) * h->L * h->L / 64)
             throw Error(LFG_EINVAL, "upload: expected L^3/64 words");
-        h->oz = kmc_origin_z(h, h->sweep, nullptr);
+        h->oz = kmc_origin_z(h, h->sweep * uint64_t(h->sub), nullptr);
         const uint32_t* src = reinterpret_cast<const uint32_t*>(words);  // plane z at z * wpp (little-endian)
         for (int g = 0; g < h->n; ++g) {
             DeviceGuard dg(h->G.dev[size_t(g)]);
@@ -636,8 +637,8 @@ int lfg_kmc_sharded_sweep(lfg_kmc_sharded* h, int64_t n_mcs, lfg_counters* out) 
         lfg_counters before{};
         if (out) lcheck(lfg_kmc_sharded_counters(h, &before));
         const int nbz = h->H / h->bk;
-        for (int64_t s = 0; s < n_mcs; ++s) {
-            const uint64_t sw = h->sweep + uint64_t(s);
+        for (int64_t s = 0; s < n_mcs * h->sub; ++s) {
+            const uint64_t sw = h->sweep * uint64_t(h->sub) + uint64_t(s);  // global sub-sweep index
             int32_t order[8];
             const int32_t oz = kmc_origin_z(h, sw, order);
             if (h->n > 1 && oz != h->oz) {  // ownership roll

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
     U4 V = {0, 0, 0, 0};
     U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u), Wn = W;  // one draw per two rounds
 #pragma unroll 1
-    for (int r = 0; r < kKmcRounds; ++r) {
+    for (int r = 0; r < a.rounds; ++r) {
         const bool odd = (r & 1) != 0;
         if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
         if (odd) Wn = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t((r >> 1) + 1));  // next pair
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     // next pair's draw is issued before the odd round (its latency hides there).
     U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, 0u);
 #pragma unroll 1
-    for (int m = 0; m < kKmcRounds / 2; ++m) {
+    for (int m = 0; m < a.rounds / 2; ++m) {
         const int r = 2 * m;
         if ((r & 31) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(r >> 5));
         round(r, W.x & 31u, below(W.y, 12), W.z);
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     k16_stage<32>(a, cur, org, lane, X0, Y0, Z0, zm);
     __syncwarp();
 #pragma unroll 1
-    for (int b = 0; b < kKmcRounds / 4; ++b) {
+    for (int b = 0; b < a.rounds / 4; ++b) {
         // the next batch's draws do not depend on the lattice: software-pipelined
         // one batch ahead so their latency hides under this batch's rounds
         uint32_t pack_n, accm_n;

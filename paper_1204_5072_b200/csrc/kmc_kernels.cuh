@@ -12,6 +12,7 @@ struct KmcPhaseArgs {
     uint32_t* w;                   // occupancy bits, sc layout [L][L][L/32] (z, y, x-words)
     unsigned long long* counters;  // [1] exchanges
     int32_t L, bk;                 // lattice edge, device block edge
+    int32_t rounds;                // single-hit rounds per block activation (kKmcRounds / sub)
     uint64_t seed, sweep;
     int32_t phase;                 // 0..7 position in the sweep's block-set order
     int32_t both;                  // ActiveMode::both

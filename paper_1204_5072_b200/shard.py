@@ -562,6 +562,7 @@ class SlabPlan:
     L: int
     world: int
     bk: int
+    sub: int = 1  # sub-sweeps per MCS (include/lfg_kmc.h lfg_kmc_plan.sub); ownership rolls per sub-sweep
 
     def __post_init__(self):
         if self.L % self.world:
@@ -654,7 +655,7 @@ class CudaSlabEngine:
         self.buf = torch.zeros((plan.cap, plan.wpp), dtype=torch.int32, device=f"cuda:{device}")
         lib = _native.lib()
         h = C.c_void_p()
-        kp = _native.KmcPlan(plan.bk)
+        kp = _native.KmcPlan(plan.bk, plan.sub)
         _native.check(lib.lfg_kmc_create_slab(C.byref(h), plan.L, float(eps), int(bool(both)), int(seed),
                                               C.byref(kp), device))
         self.h = h
@@ -708,8 +709,9 @@ class CudaSlabEngine:
 
 
 def kmc_sweep_origin(plan: SlabPlan, seed: int, sweep: int):
+    """(ox, oy, oz, [set of phase 0..7]) of global sub-sweep `sweep` (= MCS * plan.sub + k)."""
     out = (C.c_int32 * 11)()
-    kp = _native.KmcPlan(plan.bk)
+    kp = _native.KmcPlan(plan.bk, plan.sub)
     _native.check(_native.lib().lfg_kmc_sweep_origin(plan.L, C.byref(kp), int(seed), int(sweep),
                                                      C.cast(out, C.POINTER(C.c_int32))))
     return int(out[0]), int(out[1]), int(out[2]), [int(out[3 + k]) for k in range(8)]
@@ -742,7 +744,7 @@ class ShardedKmc:
     # ---- initial state (no communication: the init is position-keyed) ------
     def make_random_alloy(self, c: float, alloy_seed: int, sweep_index: int = 0):
         self.sweep_index = sweep_index
-        self.oz = self.origin(self.plan, self.seed, sweep_index)[2]
+        self.oz = self.origin(self.plan, self.seed, sweep_index * self.plan.sub)[2]
         for e, r in zip(self.engines, self.ranks):
             z, n = self._window(r)
             e.init_random_alloy(z, n, c, alloy_seed)
@@ -752,7 +754,7 @@ class ShardedKmc:
     def upload(self, words_u64, sweep_index: int = 0):
         """Every rank takes its window of a full host lattice (reference word layout)."""
         self.sweep_index = sweep_index
-        self.oz = self.origin(self.plan, self.seed, sweep_index)[2]
+        self.oz = self.origin(self.plan, self.seed, sweep_index * self.plan.sub)[2]
         for e, r in zip(self.engines, self.ranks):
             z, n = self._window(r)
             e.load_planes(words_u64, z, n)
@@ -763,19 +765,19 @@ class ShardedKmc:
     def sweep(self, n: int = 1):
         pl = self.plan
         for _ in range(n):
-            s = self.sweep_index
-            _, _, oz, order = self.origin(pl, self.seed, s)
-            if oz != self.oz:
-                old = self.oz
-                self._exchange(lambda r: pl.roll(old, oz, r))
-                self.oz = oz
-            for k in range(8):
-                sz = order[k] >> 2
-                self._exchange(lambda r: pl.ghost(oz, r, sz, 2))
-                for e, r in zip(self.engines, self.ranks):
-                    b0, nb = pl.block_rows(r)
-                    e.phase(s, k, b0, nb)
-                self._exchange(lambda r: pl.writeback(oz, r, sz))
+            for s in range(self.sweep_index * pl.sub, (self.sweep_index + 1) * pl.sub):  # sub-sweeps
+                _, _, oz, order = self.origin(pl, self.seed, s)
+                if oz != self.oz:
+                    old = self.oz
+                    self._exchange(lambda r: pl.roll(old, oz, r))
+                    self.oz = oz
+                for k in range(8):
+                    sz = order[k] >> 2
+                    self._exchange(lambda r: pl.ghost(oz, r, sz, 2))
+                    for e, r in zip(self.engines, self.ranks):
+                        b0, nb = pl.block_rows(r)
+                        e.phase(s, k, b0, nb)
+                    self._exchange(lambda r: pl.writeback(oz, r, sz))
             self.sweep_index += 1
         for e in self.engines:
             e.sync()

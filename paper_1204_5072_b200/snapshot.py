@@ -67,7 +67,7 @@ def load_kpz(path: str, device: int = 0):
 
 def save_kmc(k, path: str) -> None:
     c = k.counters()
-    hdr = _header("kmc", L=k.L, eps=k.eps, both_active=k.both_active, seed=k.seed, plan=k.plan,
+    hdr = _header("kmc", L=k.L, eps=k.eps, both_active=k.both_active, seed=k.seed, plan=k.plan, sub=k.sub,
                   sweep_index=k.sweep_index, counters=[int(c.attempts), int(c.successes)])
     np.savez(path, header=hdr, words=k.download())
 
@@ -77,7 +77,7 @@ def load_kmc(path: str, device: int = 0):
 
     hdr, a = _read(path, "kmc")
     k = KmcLattice(int(hdr["L"]), float(hdr["eps"]), bool(hdr["both_active"]), int(hdr["seed"]),
-                   block=int(hdr["plan"]), device=device)
+                   block=int(hdr["plan"]), sub=int(hdr.get("sub", 1)), device=device)
     try:
         k.upload(a["words"])
         k.sweep_index = int(hdr["sweep_index"])

@@ -42,12 +42,12 @@ def ref_run(args):
     return out
 
 
-def gpu_runs(L, c, eps, both, seeds, ts, block):
+def gpu_runs(L, c, eps, both, seeds, ts, block, sub=0):
     import paper_1204_5072_b200 as lfg
 
     ob = np.zeros((len(seeds), len(ts)))
     for i, s in enumerate(seeds):
-        with lfg.KmcLattice(L, eps, bool(both), s, block=block) as k:
+        with lfg.KmcLattice(L, eps, bool(both), s, block=block, sub=sub) as k:
             k.make_random_alloy(c, s ^ 0x5DEECE66D)
             t = 0
             for j, tt in enumerate(ts):
@@ -67,6 +67,7 @@ def main():
     ap.add_argument("--eps", type=float, default=1.5)
     ap.add_argument("--c", type=float, default=0.5)
     ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--sub", type=int, default=0, help="sub-sweeps per MCS (0: plan default 1; 4)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     ts = [t for t in (1, 2, 5, 10, 20, 50, 100, 200, 500, 1000) if t <= a.t]
@@ -74,7 +75,7 @@ def main():
         ts.append(a.t)
     seeds = [7919 * (i + 1) for i in range(a.seeds)]
     t0 = time.time()
-    g = gpu_runs(a.L, a.c, a.eps, a.both, seeds, ts, a.block)
+    g = gpu_runs(a.L, a.c, a.eps, a.both, seeds, ts, a.block, a.sub)
     tg = time.time() - t0
     nref = a.ref_seeds or a.seeds
     t0 = time.time()
@@ -84,7 +85,7 @@ def main():
     gm, gs = g.mean(0), g.std(0, ddof=1) / math.sqrt(len(seeds))
     rm, rs = r.mean(0), r.std(0, ddof=1) / math.sqrt(nref)
     z = (gm - rm) / np.sqrt(gs ** 2 + rs ** 2)
-    rep = {"L": a.L, "c": a.c, "eps": a.eps, "both": a.both, "t": ts, "gpu_seeds": len(seeds), "ref_seeds": nref,
+    rep = {"L": a.L, "c": a.c, "eps": a.eps, "both": a.both, "sub": a.sub or 1, "t": ts, "gpu_seeds": len(seeds), "ref_seeds": nref,
            "gpu_seconds": tg, "ref_seconds": tr, "gpu": {"mean": gm.tolist(), "se": gs.tolist()},
            "ref": {"mean": rm.tolist(), "se": rs.tolist()}, "z": z.tolist(), "max_abs_z": float(np.max(np.abs(z))),
            "rel_final": float(gm[-1] / rm[-1] - 1.0)}

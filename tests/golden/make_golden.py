@@ -55,12 +55,15 @@ KPZ_DTR_CASES = [
 ]
 
 # (L, bk, eps, both, c, alloy_seed, seed, sweep0, nsweeps)
-KMC_DT_CASES = [
-    (32, 16, 1.5, 0, 0.5, 5, 3, 0, 2),
-    (32, 16, 1.5, 1, 0.5, 5, 3, 0, 2),
-    (64, 16, 1.5, 1, 0.325, 1, 9, 7, 1),
-    (64, 32, 0.5, 0, 0.5, 2, 4, 0, 1),
-    (64, 16, 0.0, 1, 0.5, 3, 4, 0, 1),
+KMC_DT_CASES = [  # (..., sub): sub = 4 is the four-sub-sweep plan option
+    (32, 16, 1.5, 0, 0.5, 5, 3, 0, 2, 1),
+    (32, 16, 1.5, 1, 0.5, 5, 3, 0, 2, 1),
+    (64, 16, 1.5, 1, 0.325, 1, 9, 7, 1, 1),
+    (64, 32, 0.5, 0, 0.5, 2, 4, 0, 1, 1),
+    (64, 16, 0.0, 1, 0.5, 3, 4, 0, 1, 1),
+    (32, 16, 1.5, 1, 0.5, 5, 3, 0, 2, 4),
+    (64, 16, 1.5, 0, 0.325, 1, 9, 7, 1, 4),
+    (64, 32, 1.5, 1, 0.5, 2, 4, 0, 1, 4),
 ]
 
 
@@ -153,10 +156,10 @@ def main() -> None:
     out["kmc_sequential"] = kseq
 
     kdt = []
-    for (L, bk, eps, both, c, aseed, seed, sweep0, ns) in KMC_DT_CASES:
+    for (L, bk, eps, both, c, aseed, seed, sweep0, ns, sub) in KMC_DT_CASES:
         w, _ = ref.make_random_alloy(L, c, "lcg64", aseed)
-        cnt = ref.kmc_sweep_dt(L, w, eps, both, seed, sweep0, ns, bk)
-        kdt.append({"L": L, "bk": bk, "eps": eps, "both": both, "c": c, "alloy_seed": aseed, "seed": seed,
+        cnt = ref.kmc_sweep_dt(L, w, eps, both, seed, sweep0, ns, bk, sub)
+        kdt.append({"L": L, "bk": bk, "eps": eps, "both": both, "c": c, "alloy_seed": aseed, "seed": seed, "sub": sub,
                     "sweep0": sweep0, "nsweeps": ns, "counters": [int(v) for v in cnt], "sha": sha(w),
                     "count_b": ref.count_b(L, w), "open_bonds": ref.open_bonds_per_particle(L, w)})
     out["kmc_dt"] = kdt

@@ -54,7 +54,8 @@ class CpuSlabEngine:
         z0, n = oz + bz0 * pl.bk - 2, nbz * pl.bk + 4
         full = self._expand(z0, n)
         w = full.reshape(-1).view(np.uint64)
-        c = self.orc.kmc_dt_phase_rows(pl.L, w, self.eps, self.both, self.seed, sweep, phase, pl.bk, bz0, nbz)
+        c = self.orc.kmc_dt_phase_rows(pl.L, w, self.eps, self.both, self.seed, sweep, phase, pl.bk, bz0, nbz,
+                                       getattr(pl, "sub", 1))
         self.succ += int(c[1])
         for z, slot in self._planes(z0, n):
             self.buf[slot] = torch.from_numpy(full[z].view(np.int32).copy())

@@ -25,12 +25,12 @@ def lfg():
     return m
 
 
-@pytest.mark.parametrize("case", range(5))
+@pytest.mark.parametrize("case", range(8))
 def test_kmc_dt_golden_bit_exact(lfg, oracle, golden, case):
     g = golden["kmc_dt"][case]
     L = g["L"]
     w, _ = oracle.kmc_random_alloy(L, g["c"], "lcg64", g["alloy_seed"])
-    with lfg.KmcLattice(L, g["eps"], bool(g["both"]), g["seed"], block=g["bk"]) as k:
+    with lfg.KmcLattice(L, g["eps"], bool(g["both"]), g["seed"], block=g["bk"], sub=g["sub"]) as k:
         k.upload(w)
         k.sweep_index = g["sweep0"]
         c = k.sweep(g["nsweeps"])
@@ -50,10 +50,11 @@ def test_kmc_live_oracle_random(lfg, oracle):
         both = bool(rs.randint(2))
         c = float(rs.choice([0.1, 0.325, 0.5, 0.8]))
         seed = int(rs.randint(0, 2**62))
+        sub = int(rs.choice([1, 4]))
         w, _ = oracle.kmc_random_alloy(L, c, "lcg64", int(rs.randint(1, 1000)))
         w_ref = w.copy()
-        c_ref = oracle.kmc_sweep_dt(L, w_ref, eps, both, seed, 3, 2, bk)
-        with lfg.KmcLattice(L, eps, both, seed, block=bk) as k:
+        c_ref = oracle.kmc_sweep_dt(L, w_ref, eps, both, seed, 3, 2, bk, sub)
+        with lfg.KmcLattice(L, eps, both, seed, block=bk, sub=sub) as k:
             k.upload(w)
             k.sweep_index = 3
             cc = k.sweep(2)

@@ -207,7 +207,8 @@ def test_kmc_sequential_golden(oracle, golden):
 def test_kmc_dt_golden(oracle, golden):
     for g in golden["kmc_dt"]:
         w, _ = oracle.kmc_random_alloy(g["L"], g["c"], "lcg64", g["alloy_seed"])
-        c = oracle.kmc_sweep_dt(g["L"], w, g["eps"], g["both"], g["seed"], g["sweep0"], g["nsweeps"], g["bk"])
+        c = oracle.kmc_sweep_dt(g["L"], w, g["eps"], g["both"], g["seed"], g["sweep0"], g["nsweeps"], g["bk"],
+                                g["sub"])
         assert [int(v) for v in c] == g["counters"]
         assert sha(w) == g["sha"]
         assert oracle.kmc_count_b(g["L"], w) == g["count_b"]
@@ -215,11 +216,11 @@ def test_kmc_dt_golden(oracle, golden):
 
 def test_kmc_dt_live_vs_ref(oracle, reflib):
     for both in (0, 1):
-        for eps in (0.0, 1.5, 3.0):
+        for eps, sub in ((0.0, 1), (1.5, 1), (3.0, 1), (1.5, 4)):
             w1, _ = oracle.kmc_random_alloy(32, 0.4, "lcg64", 8)
             w2 = w1.copy()
-            c1 = oracle.kmc_sweep_dt(32, w1, eps, both, 77, 5, 2, 16)
-            c2 = reflib.kmc_sweep_dt(32, w2, eps, both, 77, 5, 2, 16)
+            c1 = oracle.kmc_sweep_dt(32, w1, eps, both, 77, 5, 2, 16, sub)
+            c2 = reflib.kmc_sweep_dt(32, w2, eps, both, 77, 5, 2, 16, sub)
             assert (c1 == c2).all() and (w1 == w2).all()
 
 

@@ -83,3 +83,15 @@ def test_sharded_kmc_upload_vs_oracle(lfg, oracle):
         c = s.sweep(2)
         assert [c.attempts, c.successes] == c_ref.tolist()
         assert np.array_equal(s.download(), w_ref)
+
+
+def test_sharded_kmc_sub4_equals_single(lfg):
+    """KMC plan option sub = 4 (four sub-sweeps per MCS): slabs == one lattice."""
+    L = 128
+    with lfg.KmcLattice(L, 1.5, True, 5, sub=4) as k, lfg.ShardedKmcLattice(L, 1.5, True, 5, devices=[0] * 4,
+                                                                            sub=4) as s:
+        k.make_random_alloy(0.5, 6)
+        s.make_random_alloy(0.5, 6)
+        c1, c2 = k.sweep(2), s.sweep(2)
+        assert (c1.attempts, c1.successes) == (c2.attempts, c2.successes)
+        assert np.array_equal(k.download(), s.download())
