@@ -759,6 +759,7 @@ cudaError_t kpz_phase_kernel_attrs() {
     cudaError_t e = attrs_nt<1>(smem);
     if (e == cudaSuccess) e = attrs_nt<2>(smem);
     if (e == cudaSuccess && LFG_KPZ_NT >= 4) e = attrs_nt<4>(smem);
+    if (e == cudaSuccess) e = kpz_width_kernel_attrs();
     return e;
 }
 

@@ -99,6 +99,7 @@ cudaError_t kpz_launch_fill_rows(uint32_t* f, int L, int rmask, int row_begin, i
 // 0).  out3[0] += sum h, out3[1] += sum h^2, out3[2] = net column-0 step of
 // the piece (as int64); scratch: kpz_width_scratch_bytes(row_count) bytes.
 size_t kpz_width_scratch_bytes(int row_count);
+cudaError_t kpz_width_kernel_attrs();  // called by kpz_phase_kernel_attrs
 cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_begin, int row_count, void* scratch,
                                   unsigned long long* out3, cudaStream_t st);
 // Closure of two uploaded slope planes: plaquettes that do not close ->

@@ -13,11 +13,11 @@
 //   h(i,j) = V(j) + sum_{k=1..i} s_x(k, j)                 (kpz_width_rows_kernel)
 // and sum h, sum h^2 are exact int64, finished on the host as kpz.cpp:78-80.
 //
-// Row kernel: one warp per row, 128 words (4096 sites) per step, one 16-byte
-// load per lane.  A lane turns its four spin words into s_x bits, then sums its
-// 128 sites byte by byte from a 256-entry table of per-byte partial sums
+// Row kernel: one warp per row, 256 words (8192 sites) per step, two 16-byte
+// loads per lane.  A lane turns its eight spin words into s_x bits, then sums its
+// 256 sites byte by byte from a 256-entry table of per-byte partial sums
 // (S1 = sum of prefix heights, S2 = sum of their squares, D = net step), kept
-// in 32 bank-private copies so the random table reads of a warp are
+// in 32 lane-private copies so the random table reads of a warp are
 // conflict-free.  A warp scan of D gives every lane its start height; the lane
 // partials (relative heights, 32-bit) are then shifted to absolute heights in
 // 64-bit: sum (o + d) = n o + S1, sum (o + d)^2 = n o^2 + 2 o S1 + S2.
@@ -28,13 +28,14 @@
 
 namespace lfg {
 
-// Per-byte table entry, three biased fields added as one packed word across a
-// lane's 16 bytes: bits 0..11 = S2 (0..204; 16 x 204 < 2^12), bits 12..22 =
-// S1 + 36 (0..72; 16 x 72 < 2^11), bits 23..31 = D + 8 (0..16; used per byte
-// only), for the 8 steps s_t = 2 b_t - 1
-// of the byte (bit t = +1 step) with prefix heights m_t = sum_{u <= t} s_u:
-// S1 = sum m_t, S2 = sum m_t^2, D = m_7.
-__device__ __forceinline__ uint32_t width_byte_entry(uint32_t v) {
+// Per-byte table entry (two words) for the 8 steps s_t = 2 b_t - 1 of a byte
+// (bit t = +1 step) with prefix heights m_t = sum_{u <= t} s_u:
+// S1 = sum m_t (-36..36), S2 = sum m_t^2 (0..204), D = m_7 (-8..8).
+//   lo = S2 | (S1 + 36) << 13   -- summed over a lane's 32 bytes as one packed
+//                                  word: S2 < 32 x 204 < 2^13, S1 + 36 < 32 x 72 < 2^12
+//   hi = D << 22 + (S1 + 36)    -- D as a signed top field: hi >> 22 (arithmetic)
+//                                  is D, and o x hi = o (S1 + 36) mod 2^22
+__device__ __forceinline__ uint2 width_byte_entry(uint32_t v) {
     int m = 0, s1 = 0, s2 = 0;
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -42,87 +43,101 @@ __device__ __forceinline__ uint32_t width_byte_entry(uint32_t v) {
         s1 += m;
         s2 += m * m;
     }
-    return uint32_t(s2) | (uint32_t(s1 + 36) << 12) | (uint32_t(m + 8) << 23);
+    return make_uint2(uint32_t(s2) | (uint32_t(s1 + 36) << 13), (uint32_t(m) << 22) + uint32_t(s1 + 36));
 }
 
-// Row pass (kpz_width_rows_kernel): one warp per row, 128 words (4096 sites)
-// per step, one 16-byte load per lane.  A lane turns its words into s_x bits
-// and walks its 16 bytes with the running offset o (height before the byte,
-// relative to the lane's first site): with per-byte table entries (S1, S2, D),
+constexpr int kWidthRowWarps = 16;         // warps per CTA of the row pass
+constexpr size_t kWidthTableBytes = 65536;  // 256 entries x 32 lanes x 8 bytes
+
+// Row pass (kpz_width_rows_kernel): one warp per row, 256 words (8192 sites)
+// per step, 8 consecutive words (two 16-byte loads) per lane.  A lane turns its
+// words into s_x bits and walks its 32 bytes with the running offset o (height
+// before the byte, relative to the lane's first site); with the byte's table
+// entry (S1, S2, D)
 //   sum over the byte of (o + m_t)   = 8 o + S1
 //   sum over the byte of (o + m_t)^2 = 8 o^2 + 2 o S1 + S2,
-// so per byte it needs o, o^2 and o S1; the S1, S2 (and D) sums of the 16 bytes
-// are one packed add.  Tables: 32 bank-private copies (conflict-free random
-// reads).  A warp scan of the lanes' net steps gives their start heights.  Per
-// row the pass stores (sum h, sum h^2) relative to the row's column-0 height
-// and the column-0 step into the row (kpz_width_tiles_kernel / _chain_kernel chain
-// them: no serial column pass on the critical path).
+// so per byte it needs o, o^2 and o S1 (one IMAD each against the entry's hi
+// word), o += D (one LEA.HI of the hi word), and one packed add of the lo word.
+// Table: entry v of lane l at byte v * 256 + l * 8 -- the address is one PRMT
+// of the byte and 8 l, and the 32 lanes' 8-byte reads of a warp cover 256
+// consecutive bytes (conflict-free).  A warp scan of the lanes' net steps gives
+// their start heights.  Per row the pass stores (sum h, sum h^2) relative to
+// the row's column-0 height and the column-0 step into the row
+// (kpz_width_tiles_kernel / _chain_kernel chain them: no serial column pass on
+// the critical path).
 template <bool VEC>
-__global__ void __launch_bounds__(256) kpz_width_rows_kernel(const uint32_t* __restrict__ f, int L, int rmask,
-                                                             int row_begin, int n, long long* __restrict__ rs,
-                                                             int32_t* __restrict__ rstep) {
-    __shared__ uint32_t tab[256 * 32];  // entry v of lane l at word v * 32 + l (bank l)
+__global__ void __launch_bounds__(32 * kWidthRowWarps) kpz_width_rows_kernel(const uint32_t* __restrict__ f, int L,
+                                                                             int rmask, int row_begin, int n,
+                                                                             long long* __restrict__ rs,
+                                                                             int32_t* __restrict__ rstep) {
+    extern __shared__ uint2 tab[];  // kWidthTableBytes
     for (int v = threadIdx.x; v < 256; v += blockDim.x) {
-        const uint32_t e = width_byte_entry(uint32_t(v));
+        const uint2 e = width_byte_entry(uint32_t(v));
 #pragma unroll 8
-        for (int l = 0; l < 32; ++l) tab[v * 32 + ((l + v) & 31)] = e;  // rotated: the 32 stores of a warp hit 32 banks
+        for (int l = 0; l < 32; ++l) tab[v * 32 + ((l + v) & 31)] = e;  // rotated: the 32 stores of a warp hit distinct banks
     }
     __syncthreads();
     const int wpr = L >> 5, Lm = L - 1;
     const int lane = threadIdx.x & 31;
-    const int wpb = int(blockDim.x >> 5);
+    const uint32_t lane8 = uint32_t(lane) * 8u;  // byte 0 of every table address
+    const char* const tabc = reinterpret_cast<const char*>(tab);
     // grid-stride over rows (the grid is sized to the resident CTAs, so each
     // CTA builds its table once)
-    for (int k = int(blockIdx.x) * wpb + int(threadIdx.x >> 5); k < n; k += int(gridDim.x) * wpb) {
+    for (int k = int(blockIdx.x) * kWidthRowWarps + int(threadIdx.x >> 5); k < n; k += int(gridDim.x) * kWidthRowWarps) {
         const int g = (row_begin + k) & Lm;
         const uint32_t* __restrict__ row = f + size_t(g & rmask) * wpr;
         int32_t base = -1;   // site 0 enters as a +1 step from -1: heights relative to h(0, g)
         uint32_t top = 0;    // bit 31 of the previous chunk's last word
         long long s1 = 0, s2 = 0;
-        for (int c = 0; c < wpr; c += 128) {
-            uint32_t F[4];
-            int nw = 4;  // valid words of this lane (all four when VEC)
+        for (int c = 0; c < wpr; c += 256) {
+            uint32_t F[8];
+            int nw = 8;  // valid words of this lane (all eight when VEC)
             if (VEC) {
-                const uint4 q = *reinterpret_cast<const uint4*>(row + c + 4 * lane);
-                F[0] = q.x; F[1] = q.y; F[2] = q.z; F[3] = q.w;
+                const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(row + c + 8 * lane));
+                const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(row + c + 8 * lane + 4));
+                F[0] = q0.x; F[1] = q0.y; F[2] = q0.z; F[3] = q0.w;
+                F[4] = q1.x; F[5] = q1.y; F[6] = q1.z; F[7] = q1.w;
             } else {
-                const int w0 = c + 4 * lane;
-                nw = max(0, min(4, wpr - w0));
+                const int w0 = c + 8 * lane;
+                nw = max(0, min(8, wpr - w0));
 #pragma unroll
-                for (int u = 0; u < 4; ++u) F[u] = u < nw ? row[w0 + u] : 0u;
+                for (int u = 0; u < 8; ++u) F[u] = u < nw ? row[w0 + u] : 0u;
             }
-            const uint32_t prev_lane = __shfl_up_sync(0xFFFFFFFFu, F[3], 1);
+            // bit 31 of the word before this lane's first: the previous lane's
+            // last valid word (zero-filled words never precede a valid one)
+            const uint32_t prev_lane = __shfl_up_sync(0xFFFFFFFFu, F[7], 1);
             uint32_t prev = lane == 0 ? top : prev_lane;
-            top = __shfl_sync(0xFFFFFFFFu, F[3], 31);
-            int32_t o = 0, so = 0, so2 = 0, sos1 = 0;
-            uint32_t pk = 0;   // packed sums of the byte entries
-            int32_t nb = 0;    // bytes summed (bias removal)
+            top = __shfl_sync(0xFFFFFFFFu, F[7], 31);
+            int32_t o = 0, so = 0, so2 = 0;
+            uint32_t sos1 = 0;  // sum o (S1 + 36) mod 2^22 in the low bits
+            uint32_t pk = 0;    // packed sums of the lo words
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                uint32_t X = ~(F[u] ^ ((F[u] << 1) | (prev >> 31)));  // bit b: s_x of site b is +1
+            for (int u = 0; u < 8; ++u) {
+                uint32_t X = ~(F[u] ^ __funnelshift_l(prev, F[u], 1));  // bit b: s_x of site b is +1
                 prev = F[u];
-                if (c == 0 && lane == 0 && u == 0) X |= 1u;
+                if (u == 0 && c == 0 && lane == 0) X |= 1u;
                 if (!VEC && u >= nw) continue;
-                nb += 4;
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
-                    uint32_t v;
-                    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(v) : "r"(X), "r"(0x4440u + uint32_t(b)));
-                    const uint32_t e = tab[(v << 5) + uint32_t(lane)];
-                    const int32_t S1 = int32_t((e >> 12) & 0x7FFu) - 36;
+                    uint32_t off;  // byte 0 = 8 lane, byte 1 = byte b of X
+                    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(off) : "r"(X), "r"(lane8), "r"(0x5504u | (uint32_t(b) << 4)));
+                    const uint2 e = *reinterpret_cast<const uint2*>(tabc + off);
                     so += o;
                     so2 += o * o;
-                    sos1 += o * S1;
-                    pk += e;
-                    o += int32_t(e >> 23) - 8;
+                    sos1 += uint32_t(o) * e.y;
+                    pk += e.x;
+                    o += int32_t(e.y) >> 22;
                 }
             }
+            const int32_t nb = VEC ? 32 : 4 * nw;  // bytes summed (bias removal)
+            const int32_t sumS1 = int32_t(pk >> 13) - 36 * nb;
+            const int32_t sumS2 = int32_t(pk & 0x1FFFu);
+            // sum o (S1 + 36): |.| <= 256 x 72 x 32 < 2^21, sign-extended from 22 bits
+            const int32_t sos1x = int32_t(sos1 << 10) >> 10;
             // a1 = sum of (o_b + m_t) over the lane's sites, a2 = sum of squares
-            const int32_t sumS1 = int32_t((pk >> 12) & 0x7FFu) - 36 * nb;
-            const int32_t sumS2 = int32_t(pk & 0xFFFu);
             const int32_t a1 = 8 * so + sumS1;
-            const int32_t a2 = 8 * so2 + 2 * sos1 + sumS2;
-            const int32_t nsites = VEC ? 128 : 32 * nw;
+            const int32_t a2 = 8 * so2 + 2 * (sos1x - 36 * so) + sumS2;
+            const int32_t nsites = 8 * nb;
             // lane start heights: exclusive warp scan of o (net step of each lane)
             int32_t inc = o;
 #pragma unroll
@@ -252,6 +267,15 @@ __global__ void __launch_bounds__(32) kpz_width_chain_kernel(const long long* __
     }
 }
 
+cudaError_t kpz_width_kernel_attrs() {  // 64 KB of dynamic shared memory (table)
+    cudaError_t e = cudaFuncSetAttribute(kpz_width_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kWidthTableBytes));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(kpz_width_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kWidthTableBytes));
+    return e;
+}
+
 size_t kpz_width_scratch_bytes(int row_count) {
     const size_t ntiles = (size_t(row_count) + kWidthTile - 1) / kWidthTile;
     return size_t(row_count) * 20 + ntiles * 48 + 64;
@@ -263,14 +287,16 @@ cudaError_t kpz_launch_width_rows(const uint32_t* f, int L, int rmask, int row_b
     long long* tiles = rs + 2 * size_t(row_count);  // [ntiles][6]
     const int ntiles = (row_count + kWidthTile - 1) / kWidthTile;
     int32_t* rstep = reinterpret_cast<int32_t*>(tiles + 6 * size_t(ntiles));
-    const int wpb = 8;
-    // resident CTAs: 32 KB of table each -> 6 per SM; 148 SMs
-    const unsigned grid = unsigned(std::min((row_count + wpb - 1) / wpb, 148 * 6));
+    constexpr int wpb = kWidthRowWarps;
+    // resident CTAs: 64 KB of table each -> 3 per SM; 148 SMs
+    const unsigned grid = unsigned(std::min((row_count + wpb - 1) / wpb, 148 * 3));
     if (grid > 0) {
-        if ((L >> 5) % 128 == 0)
-            kpz_width_rows_kernel<true><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
+        if ((L >> 5) % 256 == 0)
+            kpz_width_rows_kernel<true>
+                <<<grid, 32 * wpb, kWidthTableBytes, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
         else
-            kpz_width_rows_kernel<false><<<grid, 32 * wpb, 0, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
+            kpz_width_rows_kernel<false>
+                <<<grid, 32 * wpb, kWidthTableBytes, st>>>(f, L, rmask, row_begin, row_count, rs, rstep);
     }
     if (ntiles > 0) kpz_width_tiles_kernel<<<unsigned(ntiles), kWidthTile, 0, st>>>(rs, rstep, L, row_count, tiles);
     kpz_width_chain_kernel<<<1, 32, 0, st>>>(tiles, ntiles, L, row_count, out3);
