@@ -477,6 +477,200 @@ __global__ void __launch_bounds__(32) kmc_dt16w_phase_kernel(const __grid_consta
     if (lane == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
 }
 
+// ---------------------------------------------------------------- bk = 16, producer/consumer
+// Latency-bound phases (the same ones as kmc_dt16w_phase_kernel) with the
+// lattice-independent work moved off the round chain: one block per CTA of two
+// warps.  Warp 1 (producer) draws and precomputes the attempts one batch of
+// four rounds ahead -- the site and partner rows as shared byte addresses,
+// their bit positions, and the 13-bit Metropolis verdict mask of kmc_dt16w's
+// `prepare` -- into a two-slot shared ring, handing slots over with named
+// barriers (full: producer arrives, consumer syncs; empty: the reverse).
+// Warp 0 (consumer) runs the rounds.  A round's neighbour count is split over
+// its four lane groups g: g & 1 picks the site (0) or the partner (1), g >> 1
+// the rows on the z-1 side (0) or the z+1 side (1) of the 3x3 row window:
+// three rows of the z -+ 1 plane (edge, face, edge) plus the y -+ 1 row of the
+// site's plane (face), i.e. rows base-4, base, base+4 and base2 in bytes with
+// the same edge/face masks in every group; two shuffles join the four partial
+// counts.  Group 0 applies the exchange.  Attempt order, draws and acceptance
+// are those of kmc_dt16_phase_kernel (bit-identical lattices).
+constexpr int kPcSlots = 2;
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+template <int OFS>
+__device__ __forceinline__ uint32_t lds_at(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFS) : "memory");
+    return v;
+}
+
+// Partial count of one side of a site's 3x3 row window (row address ca, bytes):
+// rows ca+zo-4 (edge), ca+zo (face), ca+zo+4 (edge) and ca+yo (face).
+__device__ __forceinline__ int k16_side_count(uint32_t ca, int zo, int yo, uint32_t m1, uint32_t m2) {
+    const uint32_t za = ca + uint32_t(zo), ya = ca + uint32_t(yo);
+    return __popc(lds_at<-4>(za) & m1) + __popc(lds_at<0>(za) & m2) + __popc(lds_at<4>(za) & m1) +
+           __popc(lds_at<0>(ya) & m2);
+}
+
+template <bool BOTH, bool WLOG = false, int SPLIT = 4>
+__global__ void __launch_bounds__(64) kmc_dt16p_phase_kernel(const __grid_constant__ KmcPhaseArgs a) {
+    if (a.abort_flag && *reinterpret_cast<const volatile uint32_t*>(a.abort_flag)) return;
+    extern __shared__ __align__(16) uint32_t sk16[];
+    // [slot][q * 8 + t] for round 4 b + q of tile t: the site and partner row
+    // addresses and one-hot bit masks, and the Metropolis verdicts indexed by
+    // n_site - n_part + 12 for a B site (vh) and an A site (va)
+    __shared__ uint4 ring[kPcSlots][32];
+    __shared__ uint2 ringv[kPcSlots][32];
+    __shared__ uint32_t sdummy[32];
+    const int L = a.L, Lm = L - 1, warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    const int t = lane & 7, j = lane >> 3;
+    uint32_t* const cur = sk16;
+    uint32_t* const org = cur + kK16Rows;
+    const uint32_t cur_sh = uint32_t(__cvta_generic_to_shared(cur));
+    const int nb = L >> 4, h = nb >> 1;
+    const int blin = int(blockIdx.x);
+    const KmcSweep sw = kmc_sweep_draw(16, a.seed, a.sweep);
+    const int set = sw.set(a.phase);
+    const int bxi = 2 * (blin % h) + (set & 1);
+    const int byi = 2 * ((blin / h) % h) + ((set >> 1) & 1);
+    const int bzi = a.bz0 + 2 * (blin / (h * h)) + (set >> 2);
+    const uint32_t block_id = (uint32_t(bzi) * uint32_t(nb) + uint32_t(byi)) * uint32_t(nb) + uint32_t(bxi);
+    const int X0 = (sw.ox + bxi * 16) & Lm, Y0 = (sw.oy + byi * 16) & Lm, Z0 = (sw.oz + bzi * 16) & Lm;
+    const int zm = Lm & a.zmask;
+    const int wpr = L >> 5, wm = wpr - 1;
+    const int nbatch = a.rounds / 4;
+    pdl_trigger();
+
+    if (warp == 1) {  // ---- producer: never touches the lattice, so no pdl_wait
+        const int tx = t & 1, ty = (t >> 1) & 1, tz = t >> 2;
+        const uint32_t tl = uint32_t(L / 8);
+        const uint32_t tile_id = (uint32_t(bzi * 2 + tz) * tl + uint32_t(byi * 2 + ty)) * tl + uint32_t(bxi * 2 + tx);
+        const int zpar0 = (X0 ^ Y0 ^ Z0) & 1;
+        U4 V = {0, 0, 0, 0};
+#pragma unroll 1
+        for (int bb = 0; bb < nbatch; ++bb) {
+            // round 4 bb + j of tile t (KmcKernel::draw_site, kmc.hpp:154-171), as kmc_dt16w's prepare
+            if ((bb & 7) == 0) V = draw(a.seed, a.sweep, TAG_KMC_SET, block_id, uint32_t(bb >> 3));
+            const int r = 4 * bb + j;
+            const U4 W = draw(a.seed, a.sweep, TAG_KMC_SITE, tile_id, uint32_t(r >> 1));  // pair (r, r ^ 1)
+            uint32_t s5, dirw, accw;
+            kmc_round_words(W, (r & 1) != 0, s5, dirw, accw);
+            const int inner = int((u4sel(V, (r >> 3) & 3) >> (4 * (r & 7))) & 7u);
+            const int lx0 = 8 * tx + 4 * (inner & 1), ly0 = 8 * ty + 4 * ((inner >> 1) & 1),
+                      lz0 = 8 * tz + 4 * (inner >> 2);
+            const int lx = lx0 + int(s5 & 3u), ly = ly0 + int((s5 >> 2) & 3u);
+            const int lz = lz0 + ((lx ^ ly ^ lz0 ^ zpar0) & 1) + 2 * int((s5 >> 4) & 1u);
+            int dx, dy, dz;
+            fcc_offset(int(dirw), dx, dy, dz);
+            // accm bit d: the verdict accw < threshold(d) (d <= 0 -> entry 0 = 2^32)
+            uint32_t accm = 0;
+#pragma unroll
+            for (int dd = 0; dd < 13; ++dd) accm |= (a.thr_hi[dd] != 0u || accw < a.thr_lo[dd]) ? 1u << dd : 0u;
+            // kmc_attempt_impl's d by k = n_site - n_part + 12 in [0, 24]:
+            //   B site: d = k - 11 -> vh bit k = accm bit max(k - 11, 0)
+            //   A site: d = 13 - k -> va bit k = accm bit max(13 - k, 0)
+            const uint32_t all = (accm & 1u) ? 0xFFFFFFFFu : 0u;
+            const uint32_t vh = (all & 0xFFFu) | ((accm >> 1) << 12);
+            const uint32_t va = ((__brev(accm) >> 18) & 0x3FFFu) | (all & (0x7FFu << 14));
+            const uint4 e = make_uint4(cur_sh + 4u * uint32_t(k16_row(ly, lz)),
+                                       cur_sh + 4u * uint32_t(k16_row(ly + dy, lz + dz)), 1u << (lx + kK16Ofs),
+                                       1u << (lx + dx + kK16Ofs));
+            const int s = bb % kPcSlots;
+            if (bb >= kPcSlots) named_bar_sync(1 + kPcSlots + s, 64);  // the consumer has read slot s
+            ring[s][lane] = e;
+            ringv[s][lane] = make_uint2(vh, va);
+            named_bar_arrive(1 + s, 64);  // slot s holds batch bb
+        }
+        return;
+    }
+
+    // ---- consumer
+    pdl_wait();
+    k16_stage<32>(a, cur, org, lane, X0, Y0, Z0, zm);
+    __syncwarp();
+    const bool part = (j & 1) != 0, apply = j == 0;
+    const uint32_t dummy = uint32_t(__cvta_generic_to_shared(sdummy + lane));
+    const int zo = (j >> 1) ? 4 * kK16E : -4 * kK16E;  // z+1 / z-1 plane (bytes)
+    const int yo = (j >> 1) ? 4 : -4;                  // y+1 / y-1 row of the site's plane
+    uint32_t nsucc = 0;
+#pragma unroll 1
+    for (int b = 0; b < nbatch; ++b) {
+        const int s = b % kPcSlots;
+        named_bar_sync(1 + s, 64);
+        uint4 rq[4];
+        uint2 rv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            rq[q] = ring[s][q * 8 + t];
+            rv[q] = ringv[s][q * 8 + t];
+        }
+        if (b + kPcSlots < nbatch) named_bar_arrive(1 + kPcSlots + s, 64);  // slot s may be refilled
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t sa = rq[q].x, pa = rq[q].y, ms = rq[q].z, mp = rq[q].w;
+            const uint32_t own = lds_at<0>(sa), par = lds_at<0>(pa);
+            // k = n_site - n_part + 12 (valid in the site lanes, which apply the exchange)
+            int k;
+            if (SPLIT == 1) {  // every lane counts both windows
+                const uint32_t s2 = (ms << 1) | (ms >> 1), p2 = (mp << 1) | (mp >> 1);
+                k = k16_side_count(sa, -4 * kK16E, -4, ms, s2) + k16_side_count(sa, 4 * kK16E, 4, ms, s2) + 12 -
+                    k16_side_count(pa, -4 * kK16E, -4, mp, p2) - k16_side_count(pa, 4 * kK16E, 4, mp, p2);
+            } else {
+                const uint32_t ca = part ? pa : sa;
+                const uint32_t m1 = part ? mp : ms, m2 = (m1 << 1) | (m1 >> 1);  // edge bit, face bits
+                int n;
+                if (SPLIT == 2) {
+                    n = k16_side_count(ca, -4 * kK16E, -4, m1, m2) + k16_side_count(ca, 4 * kK16E, 4, m1, m2);
+                } else {
+                    n = k16_side_count(ca, zo, yo, m1, m2);
+                    n += __shfl_xor_sync(0xFFFFFFFFu, n, 16);  // z-1 side + z+1 side
+                }
+                k = n + 12 - __shfl_xor_sync(0xFFFFFFFFu, n, 8);  // site - partner
+            }
+            // kmc_attempt_impl (kmc.hpp:84-111), as in kmc_dt16_phase_kernel
+            const bool here = (own & ms) != 0u, pb = (par & mp) != 0u;
+            const uint32_t v = here ? rv[q].x : rv[q].y;
+            // (bitwise, no short-circuit: no divergent branch in the round)
+            const bool acc = (uint32_t(apply) & uint32_t(BOTH || here) & uint32_t(pb != here) & (v >> k)) & 1u;
+            // branch-free: the other groups XOR 0 into a private word each
+            asm volatile("atom.shared.xor.b32 _, [%0], %1;\n\tatom.shared.xor.b32 _, [%2], %3;" ::"r"(
+                             apply ? sa : dummy),
+                         "r"(acc ? ms : 0u), "r"(apply ? pa : dummy), "r"(acc ? mp : 0u)
+                         : "memory");
+            nsucc += acc ? 1u : 0u;
+            if (WLOG && apply) {  // the two sites the exchange writes (global sc indices)
+                const size_t o = (size_t(4 * b + q) * size_t(gridDim.x) + size_t(blin)) * 16 + 2 * t;
+                const auto sidx = [&](uint32_t addr, uint32_t mask) {
+                    const int row = int((addr - cur_sh) >> 2);
+                    const int ly = row % kK16E - 2, lz = row / kK16E - 2, lx = __ffs(int(mask)) - 1 - kK16Ofs;
+                    return uint32_t((size_t((Z0 + lz) & Lm) * L + size_t((Y0 + ly) & Lm)) * L +
+                                    size_t((X0 + lx) & Lm));
+                };
+                a.wlog[o] = acc ? sidx(sa, ms) : 0xFFFFFFFFu;
+                a.wlog[o + 1] = acc ? sidx(pa, mp) : 0xFFFFFFFFu;
+            }
+            __syncwarp();
+        }
+    }
+    const int gx = (X0 - 1 + L) & Lm, gw = gx >> 5, gb = gx & 31;
+    for (int q = lane; q < 18 * 18; q += 32) {
+        const int ly = q % 18 - 1, lz = q / 18 - 1;
+        const int rr = k16_row(ly, lz);
+        const uint32_t d = ((cur[rr] ^ org[rr]) >> (kK16Ofs - 1)) & 0x3FFFFu;
+        if (d) {
+            uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
+            atomicXor(row + gw, d << gb);
+            if (gb > 14) atomicXor(row + ((gw + 1) & wm), d >> (32 - gb));
+        }
+    }
+    nsucc = __reduce_add_sync(0xFFFFFFFFu, nsucc);
+    if (lane == 0 && nsucc) atomicAdd(a.counters, (unsigned long long)nsucc);
+}
+
 // Blocks per CTA: bk = 16 (8 threads) packs four blocks in one warp; bk = 32
 // (64 threads) is one block per CTA.
 int kmc_blocks_per_cta(int bk) {
@@ -512,6 +706,26 @@ static int kmc_wide_mode() {
         return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
     }();
     return mode;
+}
+
+// LFG_KMC_PC=0 runs latency-bound 16^3 phases on the single-warp wide kernel
+// instead of the producer/consumer pair (A/B).
+static bool kmc_pc_mode() {
+    static const bool on = [] {
+        const char* e = std::getenv("LFG_KMC_PC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// LFG_KMC_PCSPLIT=1/2/4: lanes sharing one attempt's neighbour count in the
+// producer/consumer kernel (A/B).
+static int kmc_pc_split() {
+    static const int sp = [] {
+        const char* e = std::getenv("LFG_KMC_PCSPLIT");
+        return e && (e[0] == '1' || e[0] == '2') ? e[0] - '0' : 4;
+    }();
+    return sp;
 }
 
 // Wide-kernel phase launches carry the programmatic stream-serialisation
@@ -555,6 +769,17 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         if ((per == 1 && wide == 1) || wide == 2) {  // one block per full warp (see kmc_dt16w_phase_kernel)
             const dim3 gw = dim3(unsigned(active));
             const size_t smw = 2 * kK16Rows * sizeof(uint32_t);
+            if (kmc_pc_mode()) {  // producer/consumer pair of warps per block (kmc_dt16p_phase_kernel)
+                if (a.wlog)
+                    return launch_pdl(a.both ? kmc_dt16p_phase_kernel<true, true> : kmc_dt16p_phase_kernel<false, true>,
+                                      gw, dim3(64), smw, st, a);
+                const int sp = kmc_pc_split();
+                auto k = a.both ? (sp == 1 ? kmc_dt16p_phase_kernel<true, false, 1>
+                                           : sp == 2 ? kmc_dt16p_phase_kernel<true, false, 2> : kmc_dt16p_phase_kernel<true>)
+                                : (sp == 1 ? kmc_dt16p_phase_kernel<false, false, 1>
+                                           : sp == 2 ? kmc_dt16p_phase_kernel<false, false, 2> : kmc_dt16p_phase_kernel<false>);
+                return launch_pdl(k, gw, dim3(64), smw, st, a);
+            }
             if (a.wlog)
                 return launch_pdl(a.both ? kmc_dt16w_phase_kernel<true, true> : kmc_dt16w_phase_kernel<false, true>, gw,
                                   dim3(32), smw, st, a);

@@ -170,9 +170,10 @@ print(json.dumps(out))
 
 
 def test_kmc_16_kernels_agree():
-    """The three 16^3 paths -- the full-warp kernel (latency-bound phases), the
-    8-lane kernel with one block per warp, and with four blocks per warp (>= 2368
-    active blocks, L = 512) -- give the same lattice (LFG_KMC_WIDE=0/1/2)."""
+    """The four 16^3 paths -- the producer/consumer warp pair and the single
+    full-warp kernel (latency-bound phases; LFG_KMC_PC=1/0), the 8-lane kernel
+    with one block per warp, and with four blocks per warp (>= 2368 active
+    blocks, L = 512) -- give the same lattice (LFG_KMC_WIDE=0/1/2)."""
     import json
     import os
     import subprocess
@@ -181,10 +182,10 @@ def test_kmc_16_kernels_agree():
     cases = [(64, 1.5, True, 3, 3), (128, 0.3, False, 4, 2), (512, 1.5, True, 5, 1)]
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for mode in ("0", "1", "2"):
-        env = dict(os.environ, LFG_KMC_WIDE=mode)
+    for mode, pc in (("0", "1"), ("1", "1"), ("2", "1"), ("1", "0"), ("2", "0")):
+        env = dict(os.environ, LFG_KMC_WIDE=mode, LFG_KMC_PC=pc)
         r = subprocess.run([sys.executable, "-c", _KMC_PROG, root, json.dumps(cases)], env=env,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    assert outs[0] == outs[1] == outs[2]
+    assert all(o == outs[0] for o in outs[1:])
