@@ -179,7 +179,18 @@ __global__ void __launch_bounds__(128) kmc_dt_phase_kernel(const __grid_constant
 // difference into global memory once, after its last round (RED.XOR on the
 // words holding bits [X0-1, X0+17) of rows y, z in [-1, 17): the write reach
 // of kmc.hpp:140-141; neighbouring active blocks touch disjoint bits).
-constexpr int kK16E = 20, kK16Rows = kK16E * kK16E, kK16Ofs = 8;
+#ifndef LFG_K16E
+#define LFG_K16E 22  // z stride of the staged rows (>= 20; 22 measured best, 20..26 and 32 tried)
+#endif
+// rows (ly, lz) in [-2, 18)^2 at index (lz + 2) * kK16E + (ly + 2)
+#ifndef LFG_K16SKEW
+#define LFG_K16SKEW 8  // extra words between the blocks of a 4-blocks-per-warp CTA (bank skew; 0..16 tried)
+#endif
+#ifndef LFG_K16_PREDATOM
+#define LFG_K16_PREDATOM 0
+#endif
+constexpr int kK16Y = 20, kK16E = LFG_K16E, kK16Rows = kK16E * kK16Y, kK16Ofs = 8;
+constexpr int kK16Blk = 2 * kK16Rows + LFG_K16SKEW;  // words per block (cur, org, skew)
 
 __device__ __forceinline__ int k16_row(int ly, int lz) { return (lz + 2) * kK16E + (ly + 2); }
 
@@ -208,7 +219,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 template <int STRIDE>
 __device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, uint32_t* org, int first, int X0,
                                           int Y0, int Z0, int zm) {
-    constexpr int kIt = (kK16Rows + STRIDE - 1) / STRIDE, kBatch = kIt < 13 ? kIt : 13;
+    constexpr int kN = kK16Y * kK16Y, kIt = (kN + STRIDE - 1) / STRIDE, kBatch = kIt < 13 ? kIt : 13;
     const int L = a.L, Lm = L - 1, wpr = L >> 5, wm = wpr - 1;
     const int xs = (X0 - kK16Ofs + L) & Lm, w0 = xs >> 5, bo = xs & 31;
 #pragma unroll 1
@@ -218,8 +229,8 @@ __device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, 
         for (int i = 0; i < kBatch; ++i) {
             const int rr = first + STRIDE * (i0 + i);
             lo[i] = hi[i] = 0;
-            if (rr < kK16Rows) {
-                const int ly = rr % kK16E - 2, lz = rr / kK16E - 2;
+            if (rr < kN) {
+                const int ly = rr % kK16Y - 2, lz = rr / kK16Y - 2;
                 const uint32_t* row = a.w + (size_t((Z0 + lz) & zm) * L + size_t((Y0 + ly) & Lm)) * wpr;
                 lo[i] = row[w0 & wm];
                 hi[i] = row[(w0 + 1) & wm];
@@ -228,10 +239,11 @@ __device__ __forceinline__ void k16_stage(const KmcPhaseArgs& a, uint32_t* cur, 
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
             const int rr = first + STRIDE * (i0 + i);
-            if (rr < kK16Rows) {
+            if (rr < kN) {
                 const uint32_t v = __funnelshift_r(lo[i], hi[i], bo);
-                cur[rr] = v;
-                org[rr] = v;
+                const int ri = k16_row(rr % kK16Y - 2, rr / kK16Y - 2);
+                cur[ri] = v;
+                org[ri] = v;
             }
         }
     }
@@ -244,7 +256,7 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
     __shared__ unsigned long long s_thr[13];
     const int L = a.L, Lm = L - 1, t = int(threadIdx.x) & 7, sub = int(threadIdx.x) >> 3;
     const unsigned wmask = blockDim.x >= 32 ? 0xFFFFFFFFu : (1u << blockDim.x) - 1u;
-    uint32_t* const cur = sk16 + sub * (2 * kK16Rows);
+    uint32_t* const cur = sk16 + sub * kK16Blk;
     uint32_t* const org = cur + kK16Rows;
     const int nb = L >> 4, h = nb >> 1;
     const int blin = int(blockIdx.x) * int(blockDim.x >> 3) + sub;
@@ -295,8 +307,15 @@ __global__ void __launch_bounds__(32) kmc_dt16_phase_kernel(const __grid_constan
         const int d = here ? n_site - (n_part - 1) : n_part - (n_site - 1);
         const int di = d < 0 ? 0 : d;  // d <= 12
         const bool acc = (BOTH || here) && pb != here && uint64_t(accw) < lds_u64(thr_sh + 8u * uint32_t(di));
+#if LFG_K16_PREDATOM
+        if (acc) {  // only accepted exchanges touch the rows (fewer shared wavefronts)
+            atomicXor(cur + sr, 1u << (lx + kK16Ofs));
+            atomicXor(cur + pr, 1u << (px + kK16Ofs));
+        }
+#else
         atomicXor(cur + sr, acc ? 1u << (lx + kK16Ofs) : 0u);
         atomicXor(cur + pr, acc ? 1u << (px + kK16Ofs) : 0u);
+#endif
         nsucc += acc ? 1u : 0u;
         if (WLOG) {  // the two sites the exchange writes (global sc indices)
             const size_t o = (size_t(r) * size_t(gridDim.x * (blockDim.x >> 3)) + size_t(blin)) * 16 + 2 * t;
@@ -764,7 +783,7 @@ cudaError_t kmc_launch_phase(const KmcPhaseArgs& a, cudaStream_t st) {
         // (`share` lattices running side by side count as that many times the blocks)
         const int per = active * (a.share > 1 ? a.share : 1) >= 4 * 4 * 148 && active >= 4 ? 4 : 1;
         const dim3 g16 = dim3(unsigned(active / per)), b16 = dim3(unsigned(8 * per));
-        const size_t sm16 = size_t(per) * 2 * kK16Rows * sizeof(uint32_t);
+        const size_t sm16 = size_t(per) * kK16Blk * sizeof(uint32_t);
         const int wide = kmc_wide_mode();
         if ((per == 1 && wide == 1) || wide == 2) {  // one block per full warp (see kmc_dt16w_phase_kernel)
             const dim3 gw = dim3(unsigned(active));

@@ -1,3 +1,2 @@
-OUT=gpurun_out/pc4; mkdir -p $OUT
-timeout 200 python scripts/kmc_bench.py 256 30 > $OUT/pc_256.txt 2>&1
-timeout 900 python -m pytest tests/test_kmc_gpu.py tests/test_writelog_gpu.py -x -q > $OUT/pytest.txt 2>&1; echo "exit $?" >> $OUT/pytest.txt
+OUT=gpurun_out/pc6; mkdir -p $OUT
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:kmc_dt16p -s 20 -c 1 -o $OUT/pc256 python scripts/kmc_bench.py 256 3 > $OUT/ncu.log 2>&1; echo "ncu exit $?" >> $OUT/ncu.log
