@@ -17,7 +17,9 @@ for tool in racecheck memcheck synccheck initcheck; do
   run $tool kpz_sub1
   run $tool kpz_sharded
   run $tool kmc_wide
+  run $tool kmc_wide1 LFG_KMC_PC=0
   run $tool kmc_narrow LFG_KMC_WIDE=0
+  run $tool kmc_quad
   run $tool kmc_32
 done
 run memcheck kpz_tensor

@@ -44,11 +44,13 @@ def kpz(L, p, q, bx, by, sweeps=1, seed=11, sub=4, strips=0):
     assert w2 == orc.interface_width(L, x, y)
 
 
-def kmc(L, both, bk, sweeps=1, seed=3):
+def kmc(L, both, bk, sweeps=1, seed=3, share=1):
     w, _ = orc.kmc_random_alloy(L, 0.5, "lcg64", 5)
     w_ref = w.copy()
     c_ref = orc.kmc_sweep_dt(L, w_ref, 1.5, int(both), seed, 0, sweeps, bk)
     with lfg.KmcLattice(L, 1.5, both, seed, block=bk) as k:
+        if share > 1:
+            k.set_concurrency(share)  # launcher sizes its kernel choice as if `share` lattices ran together
         k.upload(w)
         c = k.sweep(sweeps)
         g = k.download()
@@ -65,8 +67,10 @@ CASES = {
     "kpz_small": lambda: kpz(256, 0.95, 0.05, 128, 64),          # generic staging (block narrower than 1024)
     "kpz_sub1": lambda: kpz(2048, 0.95, 0.05, 1024, 128, sub=1),  # the paper's scheme (512 rounds, no skips)
     "kpz_sharded": lambda: kpz(2048, 0.95, 0.05, 1024, 128, strips=4),  # one-process sharded handle
-    "kmc_wide": lambda: kmc(64, True, 16),                       # full-warp 16^3 kernel
+    "kmc_wide": lambda: kmc(64, True, 16),                       # producer/consumer 16^3 kernel (LFG_KMC_PC=0: full warp)
+    "kmc_wide1": lambda: kmc(64, True, 16),                      # (run with LFG_KMC_PC=0: single full-warp kernel)
     "kmc_narrow": lambda: kmc(64, False, 16),                    # 8-lane 16^3 kernel (env LFG_KMC_WIDE=0)
+    "kmc_quad": lambda: kmc(64, True, 16, share=512),            # 4-blocks-per-warp 16^3 kernel (512^3 regime)
     "kmc_32": lambda: kmc(64, True, 32),                         # 32^3 blocks
 }
 
