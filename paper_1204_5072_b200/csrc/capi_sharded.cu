@@ -308,16 +308,21 @@ int lfg_kpz_sharded_download(lfg_kpz_sharded* h, uint64_t* x, uint64_t* y, size_
             sync_all(h);
             const size_t rb = size_t(h->wpr) * 4;
             DeviceGuard dg(h->dev[0]);
+            // The gather is stream-ordered on shard 0's stream and completed before the
+            // temporary handle's own (non-blocking) stream converts the rows: a plain
+            // device-to-device cudaMemcpy returns before the copy is done and is not
+            // ordered against that stream.
             for (int g = 0; g < h->n; ++g) {
                 const int r0 = h->n == 1 ? 0 : h->start(h->oy, g), rows = h->n == 1 ? h->L : h->H;
                 for (int k = 0; k < rows; ++k) {
                     const int yy = (r0 + k) % h->L;
-                    cuda_check(cudaMemcpy(static_cast<uint32_t*>(spins) + size_t(yy) * h->wpr,
-                                          h->ring[size_t(g)] + size_t(yy & (h->cap - 1)) * h->wpr, rb,
-                                          cudaMemcpyDefault),
+                    cuda_check(cudaMemcpyAsync(static_cast<uint32_t*>(spins) + size_t(yy) * h->wpr,
+                                               h->ring[size_t(g)] + size_t(yy & (h->cap - 1)) * h->wpr, rb,
+                                               cudaMemcpyDefault, h->G.st[0]),
                                "gather rows");
                 }
             }
+            cuda_check(cudaStreamSynchronize(h->G.st[0]), "gather rows");
             lcheck(lfg_kpz_download(t, 0, x, y, nwords));
         } catch (...) {
             lfg_kpz_destroy(t);
