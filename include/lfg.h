@@ -72,8 +72,10 @@ typedef struct lfg_kpz lfg_kpz;
  * each with its own random origin and block-set order, and every tile makes a
  * Poisson-distributed number of attempts per activation (mean and variance
  * 128) -- statistically matched to kpz_sweep_sequential (kpz.cpp:5-19) at
- * >= 64 seeds.  1: the paper's scheme, one
- * origin per MCS and exactly 512 single-hit rounds per activation. */
+ * >= 64 seeds.  8: eight sub-sweeps with Poisson counts of mean
+ * and variance 64 (halves the residual <h> bias of 4 at twice the phase
+ * launches).  1: the paper's scheme, one origin per MCS and
+ * exactly 512 single-hit rounds per activation. */
 typedef struct lfg_kpz_plan {
     int32_t block_x;
     int32_t block_y;
@@ -133,7 +135,7 @@ LFG_API int lfg_kpz_width_sums_async(lfg_kpz* h, int32_t replica, int64_t* out3)
  * one uint32 record per (round, tile) into dev_buf (device memory, >=
  * L*L/512 * rounds * sub words; sub-sweep k, phase f at offset
  * (4k + f) * L*L/2048 * rounds, then [rounds][tiles of the launch], rounds =
- * 132 for sub = 4, 512 for sub = 1): global tile id (bits 0-19), anchor column
+ * 68 for sub = 8, 132 for sub = 4, 512 for sub = 1): global tile id (bits 0-19), anchor column
  * in the domain xd (20-23), row yd (24-26), inner set hx (27) / hy (28),
  * accepted (29), skipped round of the tile (30; no attempt).  Single-replica
  * handles, every plan (incl. the 1024-wide TMA path); dev_buf = NULL

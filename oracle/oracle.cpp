@@ -300,7 +300,7 @@ int orc_kpz_sweep_sequential(int32_t L, uint64_t* x, uint64_t* y, double p, doub
 int orc_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, uint64_t seed,
                       uint64_t sweep0, int32_t nsweeps, int32_t bx, int32_t by, int32_t sub, int64_t* counters) {
     if (!(p >= 0.0 && p <= 1.0) || !(q >= 0.0 && q <= 1.0) || p + q <= 0.0) return -1;
-    if (sub != 1 && sub != 4) return -1;
+    if (sub != 1 && sub != 4 && sub != 8) return -1;
     orc::KpzPlan pl{L, bx, by, sub};
     int64_t dep = 0, det = 0, att = 0;
     for (int32_t s = 0; s < nsweeps; ++s) {

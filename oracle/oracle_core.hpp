@@ -135,7 +135,7 @@ Counts parallel_rows(int32_t n, bool allow, Body&& body) {
 // Inner geometry is fixed: domains 16 (x) x 8 (y) sites, tiles 32 x 16 (one
 // 32-bit word per tile row), four inner sets (hx, hy).
 //
-// One MCS = `sub` sub-sweeps (1 or 4).  Sub-sweep s' (global
+// One MCS = `sub` sub-sweeps (1, 4 or 8).  Sub-sweep s' (global
 // counter s' = s * sub + k) draws its own origin and block-set order; each
 // block activation runs kpz_rounds(sub) single-hit rounds:
 //   sub = 1: 512 rounds, every tile attempts once per round;
@@ -144,24 +144,30 @@ Counts parallel_rows(int32_t n, bool allow, Body&& body) {
 //            {7701, 471, 19, 1} / 2^16 and skips the 4-round groups g < 32 whose
 //            bit is set in the mask nibble {0, 8, A, E, F}[K_t] repeated, i.e.
 //            N_t = 132 - 32 K_t attempts: mean 128, variance 128 (the Poisson
-//            count of a 512-site tile over a quarter MCS of kpz.cpp:5-19).
+//            count of a 512-site tile over a quarter MCS of kpz.cpp:5-19);
+//   sub = 8: 68 rounds; P(K >= k) = {14497, 1735, 143, 9} / 2^16 from the same
+//            bits, the nibble repeated over the 4-round groups g < 16, i.e.
+//            N_t = 68 - 16 K_t attempts: mean 64, variance 64 (an eighth MCS).
 // The x origin is a multiple of 128 sites (32 when bx < 64).
 constexpr int kTileW = 32, kTileH = 16, kDomW = 16, kDomH = 8, kRounds = 512;
 
-inline int kpz_rounds(int sub) { return sub == 4 ? 132 : 512; }
+inline int kpz_rounds(int sub) { return sub == 8 ? 68 : (sub == 4 ? 132 : 512); }
 
-inline uint32_t kpz_skip_mask_for(uint32_t v16) {
-    const uint32_t k = uint32_t(v16 >= 57835u) + uint32_t(v16 >= 65065u) + uint32_t(v16 >= 65517u) +
-                       uint32_t(v16 >= 65535u);
+inline uint32_t kpz_skip_mask_for(uint32_t v16, int sub) {
+    static const uint32_t t4[4] = {65536u - 7701u, 65536u - 471u, 65536u - 19u, 65536u - 1u};
+    static const uint32_t t8[4] = {65536u - 14497u, 65536u - 1735u, 65536u - 143u, 65536u - 9u};
+    const uint32_t* t = sub == 8 ? t8 : t4;
+    uint32_t k = 0;
+    for (int i = 0; i < 4; ++i) k += v16 >= t[i] ? 1u : 0u;
     static const uint32_t nib[5] = {0x0u, 0x8u, 0xAu, 0xEu, 0xFu};
-    return nib[k] * 0x11111111u;
+    return nib[k] * (sub == 8 ? 0x1111u : 0x11111111u);
 }
 
 struct KpzPlan {
     int32_t L = 0;
     int32_t bx = 0;  // device block width  (multiple of 32, L % (2 bx) == 0)
     int32_t by = 0;  // device block height (multiple of 16, L % (2 by) == 0)
-    int32_t sub = 1; // sub-sweeps per MCS (1 or 4)
+    int32_t sub = 1; // sub-sweeps per MCS (1, 4 or 8)
 };
 
 struct KpzSweepDraw {
@@ -206,7 +212,7 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
     const int32_t tiles_per_row = L / kTileW;
     const int ntiles = twx * thy;
     const int rounds = kpz_rounds(pl.sub);
-    const bool skip = pl.sub == 4;
+    const bool skip = pl.sub != 1;
     Counts tot;
     for (int k = 0; k < 4; ++k) {
         const int set = d.perm[k];
@@ -230,7 +236,8 @@ Counts kpz_dtr_sweep(const KpzPlan& pl, uint64_t seed, uint64_t sweep, Attempt&&
                             const size_t t = size_t(ty * twx + tx);
                             uint32_t* a4 = anc + t * 4;
                             if ((r & 15) == 0) draw(seed, sweep, TAG_ANCHOR, tile_id, uint32_t(r >> 4), a4);
-                            if (r == 0) smask[t] = skip ? kpz_skip_mask_for((a4[2] & 0xFFu) | ((a4[3] & 0xFFu) << 8)) : 0u;
+                            if (r == 0)
+                                smask[t] = skip ? kpz_skip_mask_for((a4[2] & 0xFFu) | ((a4[3] & 0xFFu) << 8), pl.sub) : 0u;
                             if (r < 128 && ((smask[t] >> (r >> 2)) & 1u)) continue;  // skipped group
                             // Anchor of round r (k = r & 15 within its 16-round batch), fields
                             // consumed from the TOP of each Philox word (h = k >> 3, k' = k & 7):

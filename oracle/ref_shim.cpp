@@ -244,7 +244,7 @@ int ref_kpz_sweep_dtr(int32_t L, uint64_t* x, uint64_t* y, double p, double q, u
     return guarded([&] {
         const lf::KpzParams params{p, q};
         params.validate();
-        if (sub != 1 && sub != 4) throw std::invalid_argument("DtrPlan: sub must be 1 or 4");
+        if (sub != 1 && sub != 4 && sub != 8) throw std::invalid_argument("DtrPlan: sub must be 1, 4 or 8");
         auto f = load_field(L, x, y);
         orc::KpzPlan pl{L, bx, by, sub};
         int64_t dep = 0, det = 0, att = 0;

@@ -86,8 +86,9 @@ class KpzLattice:
 
     ``replicas > 1`` (or ``seeds=[...]``) holds independent lattices that one
     launch advances together (ensembles, e.g. W(t) over 16 seeds).
-    ``sub``: sub-sweeps per MCS (0 = 4, the statistically matched scheme; 1 =
-    the paper's single-origin scheme), include/lfg.h ``lfg_kpz_plan``.
+    ``sub``: sub-sweeps per MCS (0 = 4, the statistically matched scheme; 8 =
+    eight sub-sweeps, half the residual <h> bias; 1 = the paper's single-origin
+    scheme), include/lfg.h ``lfg_kpz_plan``.
     """
 
     def __init__(self, L: int, p: float = 1.0, q: float = 0.0, seed: int = 1, *, seeds=None,

@@ -54,9 +54,9 @@ def _parser() -> argparse.ArgumentParser:
     common(k)
     k.add_argument("--p", type=float, default=1.0)
     k.add_argument("--q", type=float, default=0.0)
-    k.add_argument("--sub", type=int, default=0, choices=[0, 1, 4],
-                   help="DTr sub-sweeps per MCS: 4 (default) statistically matched, 1 the paper's scheme "
-                        "with exact L^2 attempts per MCS")
+    k.add_argument("--sub", type=int, default=0, choices=[0, 1, 4, 8],
+                   help="DTr sub-sweeps per MCS: 4 (default) statistically matched, 8 with half the residual "
+                        "<h> bias, 1 the paper's scheme with exact L^2 attempts per MCS")
     m = sub.add_parser("kmc", help="fcc binary-alloy KMC, open bonds per particle (t)")
     common(m)
     m.add_argument("--conc", type=float, default=0.5)

@@ -96,8 +96,8 @@ void resolve_plan(lfg_kpz* h, const lfg_kpz_plan* plan) {
         throw Error(LFG_EINVAL, "DtrPlan: block_y must be a power of two in [16, min(" +
                                     std::to_string(LFG_KPZ_MAXBY) + ", L/2)], got " + std::to_string(by));
     const int32_t sub = plan && plan->sub ? plan->sub : 4;
-    if (sub != 1 && sub != 4)
-        throw Error(LFG_EINVAL, "DtrPlan: sub (sub-sweeps per MCS) must be 1 or 4, got " + std::to_string(sub));
+    if (sub != 1 && sub != 4 && sub != 8)
+        throw Error(LFG_EINVAL, "DtrPlan: sub (sub-sweeps per MCS) must be 1, 4 or 8, got " + std::to_string(sub));
     h->bx = bx;
     h->by = by;
     h->sub = sub;
@@ -117,7 +117,7 @@ KpzPhaseArgs base_phase_args(const lfg_kpz* h) {
     a.bx = h->bx;
     a.by = h->by;
     a.rounds = kpz_rounds(h->sub);
-    a.skip = h->sub == 4;
+    a.skip = h->sub == 1 ? 0 : h->sub;
     a.thrP = threshold32(h->p);
     a.thrQ = threshold32(h->q);
     a.general = !(h->p == 1.0 && h->q == 0.0);

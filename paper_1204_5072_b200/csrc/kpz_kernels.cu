@@ -248,7 +248,7 @@ template <bool GENERAL, bool FULL, int NT, bool MW, bool WLOG = false>
 __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT], bool active, uint64_t seed,
                                                  uint64_t sweep, uint32_t block_id, const uint32_t (&tile_id)[NT],
                                                  uint64_t thrP, uint64_t thrQ, uint32_t& ndep, uint32_t& ndet,
-                                                 uint32_t& nskip, const int rounds, const bool skip,
+                                                 uint32_t& nskip, const int rounds, const int skip,
                                                  const KpzAnchorLog& wlog = KpzAnchorLog{}) {
     // One-hot bases 1 and 1 << 16.  thrQ <= 2^32, so thrQ >> 33 is 0 -- but not to ptxas:
     // the bases become uniform runtime values instead of immediates rematerialised into a
@@ -272,7 +272,7 @@ __device__ __forceinline__ void kpz_block_rounds(const uint32_t (&lane_base)[NT]
             if (m == 0 && skip) {
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
-                    mk[n] = kpz_skip_mask(kpz_skip_k(kpz_skip_bits(A[n].z, A[n].w)));
+                    mk[n] = kpz_skip_mask(kpz_skip_k(kpz_skip_bits(A[n].z, A[n].w), skip), skip);
                     nskip += 4u * uint32_t(__popc(mk[n]));
                 }
             }
@@ -495,7 +495,7 @@ __device__ __forceinline__ void kpz_block_activation(const KpzPhaseArgs& a, uint
                          uint32_t(tx);
     }
     kpz_block_rounds<GENERAL, FULL, kNT, MW, WLOG>(lane_base, tx < Wt, seed, sweep, block_id, tile_id, a.thrP,
-                                                   a.thrQ, ndep, ndet, nskip, a.rounds, a.skip != 0, wl);
+                                                   a.thrQ, ndep, ndet, nskip, a.rounds, a.skip, wl);
     // Write back block rows 0..by-1: global word w0+1+k = funnel_l(slot k-1, slot k, b).
     // A row that a strip neighbour reads as its ghost is also stored straight
     // into that neighbour's ring buffer (NVLink peer memory): the exchange is

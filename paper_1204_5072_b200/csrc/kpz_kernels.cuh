@@ -29,7 +29,7 @@ struct alignas(64) KpzPhaseArgs {
     unsigned long long* skipped;    // [R] attempts skipped by the sub = 4 count law (device)
     int32_t L, bx, by;
     int32_t rounds;                 // single-hit rounds per block activation (kpz_rounds(sub))
-    int32_t skip;                   // 1: per-tile Poisson attempt counts (sub = 4)
+    int32_t skip;                   // sub (4 or 8): per-tile Poisson attempt counts; 0: none (sub = 1)
     uint64_t sweep;                 // global sub-sweep index s' = MCS * sub + k
     int32_t phase;                  // 0..3 position in the sweep's block-set order
     uint64_t thrP, thrQ;            // ceil(p 2^32), ceil(q 2^32)

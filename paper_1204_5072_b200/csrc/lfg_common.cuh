@@ -83,7 +83,7 @@ LFG_HD uint32_t perm_packed(uint32_t idx, int n, int bits) {
 
 // ---------------------------------------------------------------- KPZ plan
 // Inner layer: 16x8 single-hit domains in 32x16 tiles (one 32-bit word per
-// tile row).  One MCS = `sub` sub-sweeps (plan, 1 or 4); each sub-sweep draws
+// tile row).  One MCS = `sub` sub-sweeps (plan, 1, 4 or 8); each sub-sweep draws
 // its own origin and block-set order (sweep counter s' = s * sub + k) and gives
 // every block one activation of kpz_rounds(sub) single-hit rounds:
 //   sub = 1: 512 rounds, every tile one attempt per round (the paper's scheme,
@@ -93,20 +93,30 @@ LFG_HD uint32_t perm_packed(uint32_t idx, int n, int bits) {
 //            its first anchor draw -> N_t = 132 - 32 K_t attempts with mean 128
 //            and variance 128 exactly: the Poisson count a 512-site tile gets in
 //            a quarter MCS of random-sequential updates (kpz.cpp:5-19).
+//   sub = 8: 68 rounds; tile t skips the groups g < 16 whose bit is set in
+//            kpz_skip_mask(K_t, 8), K_t ~ Poisson(1/4) from the same 16 bits ->
+//            N_t = 68 - 16 K_t attempts with mean 64 and variance 64 (an eighth
+//            of an MCS).
 // DESIGN.md §2.1 / §6 (scripts/explore: why both changes are needed).
 constexpr int kTileW = 32, kTileH = 16, kDomW = 16, kDomH = 8, kRounds = 512;
 
-LFG_HD int kpz_rounds(int sub) { return sub == 4 ? 132 : 512; }
+LFG_HD int kpz_rounds(int sub) { return sub == 8 ? 68 : (sub == 4 ? 132 : 512); }
 
-// K from 16 uniform bits v: P(K >= k) = {7701, 471, 19, 1} / 2^16 (Poisson(1/8)
-// tail rounded so that E[K] = 1/8 and Var[K] = 1/8 hold exactly).
-LFG_HD uint32_t kpz_skip_k(uint32_t v16) {
+// K from 16 uniform bits v (tails rounded so that E[K] = Var[K] hold exactly):
+//   sub = 4: P(K >= k) = {7701, 471, 19, 1} / 2^16, Poisson(1/8);
+//   sub = 8: P(K >= k) = {14497, 1735, 143, 9} / 2^16, Poisson(1/4).
+LFG_HD uint32_t kpz_skip_k(uint32_t v16, int sub) {
+    if (sub == 8)
+        return uint32_t(v16 >= 51039u) + uint32_t(v16 >= 63801u) + uint32_t(v16 >= 65393u) + uint32_t(v16 >= 65527u);
     return uint32_t(v16 >= 57835u) + uint32_t(v16 >= 65065u) + uint32_t(v16 >= 65517u) + uint32_t(v16 >= 65535u);
 }
 
-// Groups g < 32 skipped by a tile with K: nibble {0, 8, A, E, F}[K] repeated
-// (8 K of the 32 groups, spread evenly: 32 K rounds).
-LFG_HD uint32_t kpz_skip_mask(uint32_t k) { return ((0xFEA80u >> (4u * k)) & 0xFu) * 0x11111111u; }
+// 4-round groups skipped by a tile with K: nibble {0, 8, A, E, F}[K] repeated
+// over groups g < 32 (sub = 4: 8 K groups, 32 K rounds) or g < 16 (sub = 8:
+// 4 K groups, 16 K rounds), spread evenly.
+LFG_HD uint32_t kpz_skip_mask(uint32_t k, int sub) {
+    return ((0xFEA80u >> (4u * k)) & 0xFu) * (sub == 8 ? 0x1111u : 0x11111111u);
+}
 
 // The 16 spare bits of anchor word batch 0 (the low bytes of words 2 and 3,
 // which the 3-bit row fields never reach).

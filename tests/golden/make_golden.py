@@ -34,7 +34,8 @@ def sha(a: np.ndarray) -> str:
 
 
 # (L, bx, by, p, q, seed, sweep0, nsweeps, sub): sub = 4 is the default plan
-# (sub-sweeps + Poisson tile counts), sub = 1 the paper's single-origin scheme.
+# (sub-sweeps + Poisson tile counts), sub = 1 the paper's single-origin scheme,
+# sub = 8 eight sub-sweeps per MCS.
 KPZ_DTR_CASES = [
     (64, 32, 32, 1.0, 0.0, 1, 0, 1, 4),
     (64, 32, 32, 1.0, 0.0, 1, 0, 4, 4),
@@ -52,6 +53,10 @@ KPZ_DTR_CASES = [
     (256, 128, 64, 0.95, 0.05, 12, 5, 2, 1),
     (1024, 512, 128, 1.0, 0.0, 1, 0, 1, 1),
     (2048, 1024, 128, 0.25, 0.75, 9, 0, 1, 1),
+    (64, 32, 16, 1.0, 0.0, 4, 0, 3, 8),
+    (256, 128, 64, 0.95, 0.05, 12, 5, 2, 8),
+    (1024, 512, 128, 1.0, 0.0, 1, 0, 1, 8),
+    (2048, 1024, 128, 0.95, 0.05, 9, 3, 1, 8),
 ]
 
 # (L, bk, eps, both, c, alloy_seed, seed, sweep0, nsweeps)

@@ -91,7 +91,7 @@ class CpuStripEngine:
         ox = qx * ((W[0] * (2 * bx // qx)) >> 32)
         oy = (W[1] * 2 * by) >> 32
         sub = getattr(pl, "sub", 4)
-        rounds = 132 if sub == 4 else 512
+        rounds = {1: 512, 4: 132, 8: 68}[sub]
         perm = self.orc.kpz_sweep_draw(L, bx, by, self.seed, sweep)[2:]
         st = int(perm[k])
         sx, sy = st & 1, st >> 1
@@ -120,10 +120,12 @@ class CpuStripEngine:
                             if r % 16 == 0:
                                 anc[tid] = self.draw(sweep, TAG_ANCHOR, tid, r >> 4)
                             a4 = anc[tid]
-                            if r == 0:  # sub = 4: Poisson attempt count via skipped 4-round groups
+                            if r == 0:  # sub = 4 / 8: Poisson attempt count via skipped 4-round groups
                                 v = (a4[2] & 0xFF) | ((a4[3] & 0xFF) << 8)
-                                K = (v >= 57835) + (v >= 65065) + (v >= 65517) + (v >= 65535)
-                                smask[tid] = [0x0, 0x8, 0xA, 0xE, 0xF][K] * 0x11111111 if sub == 4 else 0
+                                tails = (7701, 471, 19, 1) if sub == 4 else (14497, 1735, 143, 9)
+                                K = sum(v >= 65536 - t for t in tails)
+                                rep_ = 0x11111111 if sub == 4 else 0x1111
+                                smask[tid] = [0x0, 0x8, 0xA, 0xE, 0xF][K] * rep_ if sub != 1 else 0
                             if r < 128 and (smask[tid] >> (r >> 2)) & 1:
                                 continue
                             kk, h = r & 15, (r >> 3) & 1

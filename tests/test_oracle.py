@@ -130,7 +130,7 @@ def test_dtr_live_vs_ref(oracle, reflib):
         seed = int(rs.randint(0, 2**63))
         x1, y1 = oracle.kpz_flat(L)
         x2, y2 = reflib.make_flat(L)
-        sub = int(rs.choice([1, 4]))
+        sub = int(rs.choice([1, 4, 8]))
         c1 = oracle.kpz_sweep_dtr(L, x1, y1, p, q, seed, 123, 2, bx, by, sub)
         c2 = reflib.kpz_sweep_dtr(L, x2, y2, p, q, seed, 123, 2, bx, by, sub)
         assert (c1 == c2).all() and (x1 == x2).all() and (y1 == y2).all()
@@ -150,10 +150,11 @@ def test_dtr_attempt_accounting_and_closure(oracle):
         assert c[0] == 5 * L * L and c[1] == c[2] + c[3]
         assert oracle.closure_holds(L, x, y)
     L, n = 256, 40
-    x, y = oracle.kpz_flat(L)
-    c = oracle.kpz_sweep_dtr(L, x, y, 1.0, 0.0, 3, 0, n, 128, 64, 4)
-    assert abs(int(c[0]) - n * L * L) < 5 * L * n ** 0.5 and c[1] == c[2] + c[3]
-    assert oracle.closure_holds(L, x, y)
+    for sub in (4, 8):  # sd per MCS: L (sub = 4, 8 alike: sqrt(64 * 8 * L^2 / 512))
+        x, y = oracle.kpz_flat(L)
+        c = oracle.kpz_sweep_dtr(L, x, y, 1.0, 0.0, 3, 0, n, 128, 64, sub)
+        assert abs(int(c[0]) - n * L * L) < 5 * L * n ** 0.5 and c[1] == c[2] + c[3]
+        assert oracle.closure_holds(L, x, y)
 
 
 def test_skip_law_moments():
@@ -166,6 +167,11 @@ def test_skip_law_moments():
     assert (K * K).sum() * 65536 - K.sum() ** 2 == 65536 ** 2 // 8
     N = 132 - 32 * K
     assert N.mean() == 128 and N.var() == 128
+    # sub = 8: Poisson(1/4) law, N = 68 - 16 K: mean 64, variance 64 exactly
+    K8 = sum((v >= 65536 - t).astype(int) for t in (14497, 1735, 143, 9))
+    assert K8.sum() * 4 == 65536
+    N8 = 68 - 16 * K8
+    assert N8.mean() == 64 and N8.var() == 64
 
 
 def test_sweep_draw_ranges(oracle):

@@ -59,13 +59,14 @@ def _np_log(workers, acc, sites):
 
 @pytest.mark.parametrize("L,bx,by,sub,p,q,nsweeps", [
     (256, 64, 32, 4, 1.0, 0.0, 30), (256, 64, 32, 4, 0.95, 0.05, 30), (256, 64, 32, 1, 0.95, 0.05, 30),
-    (2048, 1024, 128, 4, 1.0, 0.0, 2), (2048, 1024, 128, 4, 0.95, 0.05, 2), (2048, 1024, 128, 1, 1.0, 0.0, 1)])
+    (2048, 1024, 128, 4, 1.0, 0.0, 2), (2048, 1024, 128, 4, 0.95, 0.05, 2), (2048, 1024, 128, 1, 1.0, 0.0, 1),
+    (2048, 1024, 128, 8, 0.95, 0.05, 1), (256, 64, 32, 8, 1.0, 0.0, 10)])
 def test_dt_write_sets_are_disjoint(lfg, oracle, reflib, L, bx, by, sub, p, q, nsweeps):
-    """Every plan incl. the production 1024 x 128 TMA path (L = 2048) and both sub modes."""
+    """Every plan incl. the production 1024 x 128 TMA path (L = 2048) and all sub modes."""
     import torch
 
     seed = 4711
-    rounds = 132 if sub == 4 else 512
+    rounds = {1: 512, 4: 132, 8: 68}[sub]
     ntiles = L * L // 512
     nrec = ntiles * rounds * sub
     buf = torch.zeros(nrec, dtype=torch.int32, device="cuda")
