@@ -114,21 +114,22 @@ def test_dt_write_sets_are_disjoint(lfg, oracle, reflib, L, bx, by, sub, p, q, n
     assert total_rw > 0 and total_bw > 0
 
 
-@pytest.mark.parametrize("both,four_per_warp", [(True, False), (False, False), (True, True)])
-def test_kmc_write_sets_are_disjoint(lfg, reflib, both, four_per_warp):
-    """KMC (16^3 plan): the exchanges the GPU kernels make -- the full-warp kernel of
-    sparse phases and the 4-blocks-per-warp kernel of dense ones (forced by a large
-    concurrency hint) -- recorded site by site (lfg_kmc_debug_record_writes, the write
-    hooks of kmc.hpp:105-110) and checked by the reference's WriteLog: no site written
-    by two tiles in one single-hit round, nor by two blocks in one phase."""
+@pytest.mark.parametrize("both,share", [(True, 1), (False, 1), (True, 512), (True, 2048)])
+def test_kmc_write_sets_are_disjoint(lfg, reflib, both, share):
+    """KMC (16^3 plan): the exchanges the GPU kernels make -- the producer/consumer
+    kernel of sparse phases, and (forced by concurrency hints) the two-blocks-per-lane
+    kernel of mid-sized phases (512: 4096 combined blocks) and the 4-blocks-per-warp
+    kernel of dense ones (2048) -- recorded site by site (lfg_kmc_debug_record_writes,
+    the write hooks of kmc.hpp:105-110) and checked by the reference's WriteLog: no
+    site written by two tiles in one single-hit round, nor by two blocks in one phase."""
     import torch
 
     L, nsweeps = 64, 12
     nact = (L // 16) ** 3 // 8  # active blocks per phase
     buf = torch.zeros(L ** 3, dtype=torch.int32, device="cuda")
     with lfg.KmcLattice(L, 1.5, both, 31) as k:
-        if four_per_warp:
-            k.set_concurrency(512)
+        if share > 1:
+            k.set_concurrency(share)
         k.make_random_alloy(0.5, 9)
         lfg._native.check(lfg._native.lib().lfg_kmc_debug_record_writes(k._h, buf.data_ptr(), L ** 3))
         tot = 0
