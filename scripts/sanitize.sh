@@ -19,7 +19,6 @@ for tool in racecheck memcheck synccheck initcheck; do
   run $tool kmc_wide
   run $tool kmc_wide1 LFG_KMC_PC=0
   run $tool kmc_narrow LFG_KMC_WIDE=0
-  run $tool kmc_x2
   run $tool kmc_quad
   run $tool kmc_32
 done

@@ -70,8 +70,7 @@ CASES = {
     "kmc_wide": lambda: kmc(64, True, 16),                       # producer/consumer 16^3 kernel (LFG_KMC_PC=0: full warp)
     "kmc_wide1": lambda: kmc(64, True, 16),                      # (run with LFG_KMC_PC=0: single full-warp kernel)
     "kmc_narrow": lambda: kmc(64, False, 16),                    # 8-lane 16^3 kernel (env LFG_KMC_WIDE=0)
-    "kmc_x2": lambda: kmc(64, True, 16, share=512),              # two-blocks-per-lane 16^3 kernel (512^3 regime)
-    "kmc_quad": lambda: kmc(64, True, 16, share=2048),           # 4-blocks-per-warp 16^3 kernel (1024^3 regime)
+    "kmc_quad": lambda: kmc(64, True, 16, share=512),            # 4-blocks-per-warp 16^3 kernel (512^3+ regime)
     "kmc_32": lambda: kmc(64, True, 32),                         # 32^3 blocks
 }
 
