@@ -316,6 +316,24 @@ def kmc_measure(lfg, torch, stream, steps, warmup, L=256):
     out["config"] = f"KMC fcc binary alloy {L}^3 sc, c=0.5, eps=1.5, DT blocks 16^3 (BASELINE.json configs[3])"
     out["note"] = ("L2-resident (2 MiB); only L^3/4096 tiles are active per single-hit round, so the 256^3 "
                    "case is latency-bound by construction")
+    # BASELINE configs[4] on one GPU: 1024^3, both active (the 4-blocks-per-warp kernel)
+    L5, s5 = 1024, 5
+    k = lfg.KmcLattice(L5, 1.5, True, 7)
+    k.set_stream(stream.cuda_stream)
+    k.make_random_alloy(0.5, 3)
+    k.sweep_async(2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    k.sweep_async(s5)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out["c5_single_gpu"] = {"value": (L5 ** 3 // 2) * s5 / (ms * 1e6), "unit": "attempts/ns", "ms_per_mcs": ms / s5,
+                            "steps": s5, "open_bonds": k.open_bonds_per_particle(),
+                            "config": "KMC fcc binary alloy 1024^3 sc, c=0.5, eps=1.5, both active, DT blocks 16^3 "
+                                      "(BASELINE.json configs[4] on 1 GPU; 128 MiB lattice > L2)"}
+    k.close()
     return out
 
 
