@@ -15,6 +15,7 @@ for tool in racecheck memcheck synccheck initcheck; do
   run $tool kpz_general
   run $tool kpz_small
   run $tool kpz_sub1
+  run $tool kpz_sub8
   run $tool kpz_sharded
   run $tool kmc_wide
   run $tool kmc_wide1 LFG_KMC_PC=0

@@ -66,6 +66,7 @@ CASES = {
     "kpz_tensor": lambda: kpz(4096, 1.0, 0.0, 1024, 128),        # TMA tensor-map staging / write-back away from the wrap
     "kpz_small": lambda: kpz(256, 0.95, 0.05, 128, 64),          # generic staging (block narrower than 1024)
     "kpz_sub1": lambda: kpz(2048, 0.95, 0.05, 1024, 128, sub=1),  # the paper's scheme (512 rounds, no skips)
+    "kpz_sub8": lambda: kpz(2048, 0.95, 0.05, 1024, 128, sub=8),  # eight sub-sweeps (68 rounds, Poisson(1/4) skips)
     "kpz_sharded": lambda: kpz(2048, 0.95, 0.05, 1024, 128, strips=4),  # one-process sharded handle
     "kmc_wide": lambda: kmc(64, True, 16),                       # producer/consumer 16^3 kernel (LFG_KMC_PC=0: full warp)
     "kmc_wide1": lambda: kmc(64, True, 16),                      # (run with LFG_KMC_PC=0: single full-warp kernel)
