@@ -123,14 +123,15 @@ def test_kpz_c3_strip_shards_one_sweep(lfg, c3, world):
             e.close()
 
 
-@pytest.mark.parametrize("both", [1, 0])
-def test_kmc_c4_two_sweeps(lfg, oracle, both):
-    """configs[3]: 256^3, c = 0.5, eps = 1.5, 2 sweeps, both active modes."""
+@pytest.mark.parametrize("both,sub", [(1, 1), (0, 1), (1, 4)])
+def test_kmc_c4_two_sweeps(lfg, oracle, both, sub):
+    """configs[3]: 256^3, c = 0.5, eps = 1.5, 2 sweeps, both active modes (the
+    producer/consumer kernel), and the four-sub-sweep plan option."""
     L, eps, seed = 256, 1.5, 31 + both
     w0, _ = oracle.kmc_random_alloy(L, 0.5, "lcg64", 7)
     w = w0.copy()
-    cref = oracle.kmc_sweep_dt(L, w, eps, both, seed, 0, 2, 16)
-    with lfg.KmcLattice(L, eps, bool(both), seed, block=16) as k:
+    cref = oracle.kmc_sweep_dt(L, w, eps, both, seed, 0, 2, 16, sub=sub)
+    with lfg.KmcLattice(L, eps, bool(both), seed, block=16, sub=sub) as k:
         k.upload(w0)
         c = k.sweep(2)
         g = k.download()
@@ -140,16 +141,16 @@ def test_kmc_c4_two_sweeps(lfg, oracle, both):
     assert tuple(ob) == tuple(oracle.kmc_open_bond_sums(L, w))
 
 
-@pytest.mark.parametrize("L,both", [(512, 1), (1024, 1), (1024, 0)])
-def test_kmc_four_blocks_per_warp_kernel(lfg, oracle, L, both):
+@pytest.mark.parametrize("L,both,sub", [(512, 1, 1), (1024, 1, 1), (1024, 0, 1), (512, 1, 4)])
+def test_kmc_four_blocks_per_warp_kernel(lfg, oracle, L, both, sub):
     """The 4-blocks-per-warp kernel (>= 2368 active 16^3 blocks per phase: 512^3,
     and configs[4]'s 1024^3 lattice) against the oracle, not against its siblings."""
     eps, seed = 1.5, 900 + L + both
-    with lfg.KmcLattice(L, eps, bool(both), seed, block=16) as k:
+    with lfg.KmcLattice(L, eps, bool(both), seed, block=16, sub=sub) as k:
         k.make_random_alloy(0.5, 11)
         w = k.download()
         c = k.sweep(1)
         g = k.download()
-    cref = oracle.kmc_sweep_dt(L, w, eps, both, seed, 0, 1, 16)
+    cref = oracle.kmc_sweep_dt(L, w, eps, both, seed, 0, 1, 16, sub=sub)
     assert [c.attempts, c.successes] == cref.tolist()
     assert np.array_equal(g, w)
